@@ -1,0 +1,390 @@
+// GPU executor: the engine side of the reference contract (executor.hpp)
+// driven by real prefill/decode forward passes on a B200 instead of the
+// virtual clock (replaces splitsim::Engine::run, engine.hpp:101-172).
+//
+// One host thread runs the reference loop on device time:
+//   poll    cudaEventQuery on every in-flight launch's end event;
+//           arrivals are due when wall time since run start >= arrival_s;
+//   drain   due arrivals and completed launches in time order (arrivals
+//           first on ties, completions in activation order), applying the
+//           exact completion semantics of the core (KV growth, finish, free);
+//   pass    one scheduler pass; every activated task is enqueued as real
+//           work -- a prompt task = prefill_forward over its prompts, a token
+//           step = decode_forward over its running batch.
+// Split phase: prompts go to the prefill stream, token steps to a
+// higher-priority decode stream, so the compute-bound and HBM-bound phases
+// overlap on the SMs and share the one paged KV arena (the handoff is a
+// scheduler list append, no data moves).  Serial mode puts both on one
+// stream: the same task stream, one kernel sequence at a time.
+// Tasks activated in the same pass with the same kind are coalesced into one
+// launch (one weight stream for several lanes' token steps).
+// Timestamps: TaskStart = device time the launch began (event before its
+// first kernel), TaskComplete = device time of its end event, both relative
+// to an event recorded at run start; arrivals carry their nominal time.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../host/capi_util.hpp"
+#include "../host/executor.hpp"
+#include "../host/report.hpp"
+#include "../host/run_text.hpp"
+#include "../host/spec.hpp"
+#include "../kernels/common.cuh"
+#include "model.hpp"
+
+namespace sw {
+
+struct GpuOptions {
+    bool split = true;        // two streams (prefill || decode) vs one
+    bool coalesce = true;     // one launch per kind per pass
+    bool graphs = true;       // CUDA graphs for decode steps
+    double peak_flops = 1.6932e15;
+    double peak_bytes = 6.4469e12;
+};
+
+// Algorithmic work of the real forward passes.
+struct ModelWork {
+    double n_mm = 0, d = 0, V = 0, L = 0, H = 0, hd = 0, kv_tok = 0;
+    explicit ModelWork(const sw_model_desc& m) {
+        d = m.d_model;
+        V = m.vocab;
+        L = m.n_layers;
+        H = m.n_heads;
+        hd = m.head_dim;
+        const double qkv = (m.n_heads + 2.0 * m.n_kv_heads) * m.head_dim;
+        n_mm = L * (d * qkv + m.n_heads * m.head_dim * d + 3.0 * d * m.ffn_dim);
+        kv_tok = 2.0 * L * m.n_kv_heads * m.head_dim * 2.0;
+    }
+    double weight_bytes() const { return 2.0 * (n_mm + d * V); }
+    double prompt_flops(double S) const { return 2.0 * n_mm * S + 2.0 * L * H * hd * S * (S + 1.0) + 2.0 * d * V; }
+    double step_bytes(double b, double sum_ctx) const { return weight_bytes() + 2.0 * d * b + sum_ctx * kv_tok + b * kv_tok; }
+    double step_flops(double b, double sum_ctx) const { return b * 2.0 * (n_mm + d * V) + 4.0 * L * H * hd * sum_ctx; }
+};
+
+class GpuExecutor final : public ExecutorCore {
+public:
+    GpuExecutor(const SimulationInputs& in, Scheduler& sched, sw_model* m, sw_kv* kv, const GpuOptions& opt)
+        : ExecutorCore(in, sched), m_(m), kv_(kv), opt_(opt), work_(m->desc) {
+        if (in_.discipline.mode == SharingDiscipline::Mode::TimeSliced)
+            throw ConfigError("discipline.mode: time_sliced is not a GPU mode");
+        if (static_cast<long long>(entries_.size()) > kv_->n_slots)
+            throw ConfigError("engine: more requests than KV arena slots");
+        if (pages_.n_pages() > kv_->n_pages) throw ConfigError("engine: kv_capacity_blocks exceeds the KV arena");
+        int max_out = 0, max_ctx = 0;
+        for (const Entry& e : entries_) {
+            max_out = std::max(max_out, e.req.output_tokens);
+            max_ctx = std::max(max_ctx, e.req.input_tokens + e.req.output_tokens);
+        }
+        if (max_out + 1 > kv_->max_out) throw ConfigError("engine: output longer than the arena's token buffer");
+        if ((max_ctx + kv_->page_tokens - 1) / kv_->page_tokens > kv_->max_pages)
+            throw ConfigError("engine: context longer than the arena's page-table row");
+        for (std::size_t i = 0; i < entries_.size(); ++i) slot_of_[entries_[i].req.id] = static_cast<int>(i);
+        int lo, hi;
+        SW_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        SW_CUDA(cudaStreamCreateWithPriority(&s_prefill_, cudaStreamNonBlocking, lo));
+        if (opt_.split) SW_CUDA(cudaStreamCreateWithPriority(&s_decode_, cudaStreamNonBlocking, hi));
+        else s_decode_ = s_prefill_;
+    }
+
+    ~GpuExecutor() override {
+        cudaStreamSynchronize(s_prefill_);
+        cudaStreamSynchronize(s_decode_);
+        for (cudaEvent_t e : events_) cudaEventDestroy(e);
+        if (s_decode_ != s_prefill_) cudaStreamDestroy(s_decode_);
+        cudaStreamDestroy(s_prefill_);
+    }
+
+    EventLog run() {
+        using clk = std::chrono::steady_clock;
+        t0_ = new_event();
+        SW_CUDA(cudaEventRecord(events_[t0_], s_prefill_));
+        SW_CUDA(cudaEventSynchronize(events_[t0_]));
+        const auto wall0 = clk::now();
+        seq_ = static_cast<long long>(entries_.size());
+        std::size_t next_arrival = 0;
+        bool first = true;
+        for (;;) {
+            const double now = std::chrono::duration<double>(clk::now() - wall0).count();
+            // ---- poll
+            struct Ev {
+                double t;
+                int kind;  // 0 arrival, 1 completion
+                long long order;
+                std::size_t ref;
+            };
+            std::vector<Ev> evs;
+            while (next_arrival < entries_.size() && entries_[next_arrival].req.arrival_s <= now) {
+                evs.push_back({entries_[next_arrival].req.arrival_s, 0, static_cast<long long>(next_arrival), next_arrival});
+                ++next_arrival;
+            }
+            for (std::size_t i = 0; i < launches_.size(); ++i) {
+                Launch& L = launches_[i];
+                if (L.done) continue;
+                const cudaError_t q = cudaEventQuery(events_[L.end_ev]);
+                if (q == cudaErrorNotReady) continue;
+                SW_CUDA(q);
+                L.done = true;
+                L.t_end = elapsed(L.end_ev);
+                evs.push_back({L.t_end, 1, L.first_seq, i});
+            }
+            std::stable_sort(evs.begin(), evs.end(), [](const Ev& a, const Ev& b) {
+                if (a.t != b.t) return a.t < b.t;
+                if (a.kind != b.kind) return a.kind < b.kind;
+                return a.order < b.order;
+            });
+            for (const Ev& e : evs) {
+                clock_ = std::max(clock_, e.t);
+                if (e.kind == 0) {
+                    log_arrival(entries_[e.ref], {e.t});
+                } else {
+                    for (long long sq : launches_[e.ref].task_seqs) {
+                        std::size_t idx = 0;
+                        while (idx < active_.size() && active_[idx].seq != sq) ++idx;
+                        if (idx == active_.size()) throw ContractViolation("gpu executor: lost task");
+                        complete(idx, {e.t});
+                    }
+                }
+            }
+            if (!evs.empty() || first) {
+                first = false;
+                schedule_pass();
+            }
+            const bool inflight = std::any_of(launches_.begin(), launches_.end(), [](const Launch& l) { return !l.done; });
+            if (!inflight && active_.empty() && next_arrival >= entries_.size()) break;
+            if (!inflight && active_.empty() && evs.empty()) {
+                // idle until the next arrival
+                const double wait = entries_[next_arrival].req.arrival_s - now;
+                if (wait > 2e-4) std::this_thread::sleep_for(std::chrono::duration<double>(wait - 1e-4));
+            } else if (evs.empty()) {
+                std::this_thread::yield();
+            }
+            if (++polls_ > 2'000'000'000ULL) throw ContractViolation("gpu executor: livelock guard");
+        }
+        check_all_finished();
+        double t_end = clock_;
+        LogRecord end;
+        end.kind = LogKind::RunEnd;
+        append(end, {t_end});
+        finalize_times([&](int ev) { return elapsed(ev); });
+        // RunEnd must stay last: after sorting it is (all stamps <= clock_).
+        return log_;
+    }
+
+    std::string extras() const {
+        std::string s;
+        // generated tokens per request: x_1..x_out (device out_tokens[slot][0..out))
+        std::vector<int32_t> host(static_cast<size_t>(kv_->n_slots) * kv_->max_out);
+        SW_CUDA(cudaMemcpy(host.data(), kv_->out_tokens, host.size() * 4, cudaMemcpyDeviceToHost));
+        std::vector<int32_t> table(static_cast<size_t>(kv_->n_slots) * kv_->max_pages);
+        SW_CUDA(cudaMemcpy(table.data(), kv_->page_table, table.size() * 4, cudaMemcpyDeviceToHost));
+        for (const Entry& e : entries_) {
+            const int slot = slot_of_.at(e.req.id);
+            s += "#tokens " + std::to_string(e.req.id) + ":";
+            for (int j = 0; j < e.req.output_tokens; ++j)
+                s += (j ? "|" : "") + std::to_string(host[static_cast<size_t>(slot) * kv_->max_out + j]);
+            s += "\n";
+            const auto it = pages_.final_rows().find(e.req.id);
+            const std::size_t np = it == pages_.final_rows().end() ? 0 : it->second.size();
+            s += "#devpages " + std::to_string(e.req.id) + ":";
+            for (std::size_t j = 0; j < np; ++j)
+                s += (j ? "|" : "") + std::to_string(table[static_cast<size_t>(slot) * kv_->max_pages + j]);
+            s += "\n";
+        }
+        char buf[256];
+        std::snprintf(buf, sizeof buf, "#gpu launches=%zu;prefill_launches=%d;decode_launches=%d;split=%d;coalesce=%d\n",
+                      launches_.size(), n_prefill_, n_decode_, opt_.split ? 1 : 0, opt_.coalesce ? 1 : 0);
+        s += buf;
+        return s;
+    }
+
+protected:
+    PhaseTask price(const TaskRequest& tr, const std::vector<Request>& prompt_batch) override {
+        PhaseTask t;
+        t.kind = tr.kind;
+        t.instance_id = tr.instance_id;
+        t.batch = tr.batch;
+        check_batch(t.batch);
+        if (tr.kind == TaskKind::Prompt) {
+            double flops = 0, toks = 0;
+            for (const Request& r : prompt_batch) {
+                flops += work_.prompt_flops(r.input_tokens);
+                toks += r.input_tokens;
+            }
+            t.compute_demand = flops;
+            t.mem_demand = work_.weight_bytes() + toks * work_.kv_tok;
+        } else {
+            double ctx = 0;
+            for (int rid : tr.batch) {
+                const Entry& e = entry(rid);
+                ctx += e.req.input_tokens + e.generated;  // keys attended (incl. the fed token)
+            }
+            const double b = static_cast<double>(tr.batch.size());
+            t.compute_demand = work_.step_flops(b, ctx);
+            t.mem_demand = work_.step_bytes(b, ctx - b);
+        }
+        t.duration_alone_s = std::max(t.compute_demand / opt_.peak_flops, t.mem_demand / opt_.peak_bytes);
+        return t;
+    }
+
+private:
+    struct Launch {
+        TaskKind kind;
+        int start_ev = -1, end_ev = -1;
+        std::vector<long long> task_seqs;
+        long long first_seq = 0;
+        bool done = false;
+        double t_end = 0;
+    };
+
+    int new_event() {
+        cudaEvent_t e;
+        SW_CUDA(cudaEventCreate(&e));
+        events_.push_back(e);
+        return static_cast<int>(events_.size()) - 1;
+    }
+
+    double elapsed(int ev) const {
+        float ms = 0.f;
+        SW_CUDA(cudaEventElapsedTime(&ms, events_[t0_], events_[ev]));
+        return static_cast<double>(ms) * 1e-3;
+    }
+
+    void schedule_pass() {
+        const std::vector<TaskRequest> trs = sched_.next_tasks(*this);
+        if (trs.empty()) return;
+        // group: coalesced -> one launch per kind; else one per task
+        std::vector<Launch> group;
+        int prompt_launch = -1, step_launch = -1;
+        std::vector<std::pair<int, std::size_t>> placement;  // (launch idx in group, active idx)
+        for (const TaskRequest& tr : trs) {
+            int gi;
+            int& slot = tr.kind == TaskKind::Prompt ? prompt_launch : step_launch;
+            if (opt_.coalesce && slot >= 0) {
+                gi = slot;
+            } else {
+                Launch L;
+                L.kind = tr.kind;
+                L.start_ev = new_event();
+                L.end_ev = new_event();
+                group.push_back(L);
+                gi = static_cast<int>(group.size()) - 1;
+                slot = gi;
+            }
+            const std::size_t ai = activate(tr, {0.0, group[static_cast<std::size_t>(gi)].start_ev});
+            group[static_cast<std::size_t>(gi)].task_seqs.push_back(active_[ai].seq);
+        }
+        for (Launch& L : group) {
+            L.first_seq = L.task_seqs.front();
+            enqueue(L);
+            launches_.push_back(L);
+        }
+    }
+
+    void enqueue(const Launch& L) {
+        std::vector<int> rids;
+        for (long long sq : L.task_seqs) {
+            const Active* a = nullptr;
+            for (const Active& x : active_)
+                if (x.seq == sq) a = &x;
+            if (!a) throw ContractViolation("gpu executor: enqueue of unknown task");
+            rids.insert(rids.end(), a->task.batch.begin(), a->task.batch.end());
+        }
+        const int n = static_cast<int>(rids.size());
+        std::vector<int32_t> slots(n), ntok(n), pos(n), newp(n), oidx(n), toks, prow;
+        sw_batch b{};
+        b.n = n;
+        if (L.kind == TaskKind::Prompt) {
+            for (int i = 0; i < n; ++i) {
+                const Entry& e = entry(rids[i]);
+                slots[i] = slot_of_.at(rids[i]);
+                ntok[i] = e.req.input_tokens;
+                oidx[i] = 0;
+                for (int j = 0; j < e.req.input_tokens; ++j)
+                    toks.push_back(prompt_token(m_->desc.seed, e.req.id, j, m_->desc.vocab));
+                const std::vector<int>& row = pages_.row(rids[i]);
+                const int need = (e.req.input_tokens + kv_->page_tokens - 1) / kv_->page_tokens;
+                for (int j = 0; j < need; ++j) prow.push_back(row.at(static_cast<std::size_t>(j)));
+            }
+            b.slots = slots.data();
+            b.n_tokens = ntok.data();
+            b.tokens = toks.data();
+            b.page_rows = prow.data();
+            b.out_index = oidx.data();
+            SW_CUDA(cudaEventRecord(events_[L.start_ev], s_prefill_));
+            prefill_forward(m_, kv_, b, s_prefill_);
+            SW_CUDA(cudaEventRecord(events_[L.end_ev], s_prefill_));
+            ++n_prefill_;
+        } else {
+            for (int i = 0; i < n; ++i) {
+                const Entry& e = entry(rids[i]);
+                slots[i] = slot_of_.at(rids[i]);
+                pos[i] = e.req.input_tokens + e.generated;  // position of the fed token x_g
+                const int pidx = pos[i] / kv_->page_tokens;
+                newp[i] = pos[i] % kv_->page_tokens == 0 ? pages_.row(rids[i]).at(static_cast<std::size_t>(pidx)) : -1;
+                oidx[i] = e.generated + 1;  // x_{g+1}
+            }
+            b.slots = slots.data();
+            b.positions = pos.data();
+            b.new_page = newp.data();
+            b.out_index = oidx.data();
+            SW_CUDA(cudaEventRecord(events_[L.start_ev], s_decode_));
+            decode_forward(m_, kv_, b, s_decode_, opt_.graphs);
+            SW_CUDA(cudaEventRecord(events_[L.end_ev], s_decode_));
+            ++n_decode_;
+        }
+    }
+
+    sw_model* m_;
+    sw_kv* kv_;
+    GpuOptions opt_;
+    ModelWork work_;
+    cudaStream_t s_prefill_ = nullptr, s_decode_ = nullptr;
+    std::vector<cudaEvent_t> events_;
+    int t0_ = -1;
+    std::vector<Launch> launches_;
+    std::map<int, int> slot_of_;
+    unsigned long long polls_ = 0;
+    int n_prefill_ = 0, n_decode_ = 0;
+};
+
+}  // namespace sw
+
+using namespace sw;
+
+extern "C" int sw_engine_run(sw_model* m, sw_kv* kv, const char* spec, char** out) {
+    return guarded([&] {
+        if (!m || !kv || !spec || !out) throw ConfigError("sw_engine_run: null argument");
+        RunSpec rs = build_spec(parse_spec(spec));
+        GpuOptions opt;
+        for (const auto& [k, v] : rs.rest) {
+            if (k == "engine.split") opt.split = v == "1" || v == "true";
+            else if (k == "engine.coalesce") opt.coalesce = v == "1" || v == "true";
+            else if (k == "engine.graphs") opt.graphs = v == "1" || v == "true";
+            else if (k == "engine.peak_flops") opt.peak_flops = std::stod(v);
+            else if (k == "engine.peak_bytes") opt.peak_bytes = std::stod(v);
+            else throw ConfigError("spec: unknown key '" + k + "'");
+        }
+        // the log's capacities are the real peaks (so alone_s is a roofline time)
+        rs.inputs.gpu.compute_capacity = opt.peak_flops;
+        rs.inputs.gpu.mem_bandwidth = opt.peak_bytes;
+        if (rs.kv_capacity_override <= 0) rs.inputs.gpu.kv_capacity_blocks = kv->n_pages;
+        if (rs.scheduler.policy == PolicyKind::MultiInstance || rs.scheduler.policy == PolicyKind::PipelinedSplitwiser)
+            if (rs.inputs.discipline.mode == SharingDiscipline::Mode::Exclusive && model_instances(rs.scheduler) > 1)
+                rs.inputs.discipline.mode = SharingDiscipline::Mode::MpsConcurrent;
+        PolicyScheduler sched(rs.inputs.requests, rs.scheduler, rs.inputs.cost.kv_handoff_s);
+        GpuExecutor ex(rs.inputs, sched, m, kv, opt);
+        const auto w0 = std::chrono::steady_clock::now();
+        const EventLog log = ex.run();
+        const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - w0).count();
+        const MetricsReport rep = build_report(log);
+        std::string text = serialize_event_log(log) + render_report(rep) + render_pages(ex.pages()) + ex.extras();
+        text += "#wall wall_s=" + fmt17(wall) + "\n";
+        *out = dup_text(text);
+    });
+}

@@ -1,0 +1,594 @@
+// Model runtime: weights, KV arena, the prefill and decode forward passes, and
+// the kernel-level C-ABI (sw_model_create ... sw_decode_enqueue).
+//
+// These two passes are what replaces the reference's task pricing
+// (make_prompt_task / make_token_step_task, splitsim/gpu_model.hpp:154-189):
+// a prompt task runs prefill_forward over the batch's prompts, a token step
+// runs decode_forward over the running batch.
+//
+// HBM layout (bf16 unless noted):
+//   weights  one arena; per layer wqkv [(H+2Hkv)hd, d], wo [d, H hd],
+//            wgu [2 ffn, d] in [gate 64 | up 64] row blocks (SwiGLU fuses into
+//            the GEMM epilogue), wd [d, ffn]; embedding [V, d]; LM head [V, d]
+//            (aliases the embedding when tied).
+//   KV       pages[L][n_pages][K|V][Hkv][16 tokens][hd]: a (layer, page, head)
+//            is one contiguous 16 x hd block, so attention reads whole pages
+//            with 16 B vector loads; page ids come from per-slot page tables
+//            (int32 [slots][max_pages]) shared by both phases -- the prompt
+//            writes the pages, the decode steps read them, nothing is copied
+//            at the phase handoff.
+// Decode steps are captured into one CUDA graph per row bucket; the graph
+// reads the live row count and per-row metadata from a device StepMeta the
+// host refreshes with a single H2D copy per step.
+#include <algorithm>
+#include <cmath>
+#include <cstddef>
+#include <cstring>
+#include <string>
+
+#include "../host/capi_util.hpp"
+#include "../kernels/attention.cuh"
+#include "../kernels/common.cuh"
+#include "../kernels/elementwise.cuh"
+#include "../kernels/gemm_sm100.cuh"
+#include "model.hpp"
+
+namespace sw {
+
+namespace {
+
+constexpr int kLmRowsMax = 256;  // LM-head rows per launch (swap-AB N <= 256)
+
+size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+template <class T>
+T* dalloc(size_t n) {
+    void* p = nullptr;
+    SW_CUDA(cudaMalloc(&p, n * sizeof(T)));
+    return static_cast<T*>(p);
+}
+
+void ring_init(PinnedRing& r, int n, size_t bytes) {
+    r.bytes = bytes;
+    for (int i = 0; i < n; ++i) {
+        void* p = nullptr;
+        SW_CUDA(cudaMallocHost(&p, bytes));
+        cudaEvent_t e;
+        SW_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        SW_CUDA(cudaEventRecord(e, 0));
+        r.slots.push_back(p);
+        r.done.push_back(e);
+    }
+}
+
+// Claim the next staging slot (waits only if its previous copy is still pending).
+void* ring_claim(PinnedRing& r, int& idx) {
+    idx = r.next;
+    r.next = (r.next + 1) % static_cast<int>(r.slots.size());
+    SW_CUDA(cudaEventSynchronize(r.done[idx]));
+    return r.slots[idx];
+}
+
+void ring_release(PinnedRing& r, int idx, cudaStream_t st) { SW_CUDA(cudaEventRecord(r.done[idx], st)); }
+
+void ws_alloc(Workspace& w, const sw_model_desc& d, int rows, bool decode, int max_splits_cap) {
+    const int qkv_w = (d.n_heads + 2 * d.n_kv_heads) * d.head_dim;
+    w.rows = rows;
+    w.x = dalloc<float>(static_cast<size_t>(rows) * d.d_model);
+    w.xn = dalloc<__nv_bfloat16>(static_cast<size_t>(rows) * d.d_model);
+    w.qkv = dalloc<__nv_bfloat16>(static_cast<size_t>(rows) * qkv_w);
+    w.q = dalloc<__nv_bfloat16>(static_cast<size_t>(rows) * d.n_heads * d.head_dim);
+    w.attn = dalloc<__nv_bfloat16>(static_cast<size_t>(rows) * d.n_heads * d.head_dim);
+    w.act = dalloc<__nv_bfloat16>(static_cast<size_t>(rows) * d.ffn_dim);
+    w.xlast = dalloc<__nv_bfloat16>(static_cast<size_t>(kLmRowsMax) * d.d_model);
+    w.keys = dalloc<unsigned long long>(kLmRowsMax);
+    SW_CUDA(cudaMemset(w.keys, 0, kLmRowsMax * sizeof(unsigned long long)));
+    SW_CUDA(cudaMemset(w.x, 0, static_cast<size_t>(rows) * d.d_model * sizeof(float)));
+    SW_CUDA(cudaMemset(w.xn, 0, static_cast<size_t>(rows) * d.d_model * 2));
+    SW_CUDA(cudaMemset(w.attn, 0, static_cast<size_t>(rows) * d.n_heads * d.head_dim * 2));
+    SW_CUDA(cudaMemset(w.act, 0, static_cast<size_t>(rows) * d.ffn_dim * 2));
+    if (decode) {
+        w.meta = dalloc<StepMeta>(1);
+        SW_CUDA(cudaMemset(w.meta, 0, sizeof(StepMeta)));
+        const int G = d.n_heads / d.n_kv_heads;
+        const size_t parts = static_cast<size_t>(kMaxDecodeRows) * d.n_kv_heads * max_splits_cap * G;
+        w.part_o = dalloc<float>(parts * d.head_dim);
+        w.part_ml = dalloc<float>(parts * 2);
+    } else {
+        // header + tokens/pos/slot per token + per-seq arrays + tiles + page rows
+        const size_t T = static_cast<size_t>(rows);
+        w.pmeta_bytes = (16 + 3 * T + 6 * (T + 1) + 2 * (T / 64 + T + 1) + (T / 16 + T + 1)) * sizeof(int32_t);
+        w.pmeta = dalloc<int32_t>(w.pmeta_bytes / sizeof(int32_t));
+    }
+}
+
+GemmProblem gp(const void* X, int64_t x_rows, const void* W, int64_t w_rows, int tokens, int features, int K,
+               int mode, bool swap, void* out, int ldo, const int* live = nullptr) {
+    GemmProblem p{};
+    p.X = X;
+    p.x_rows = x_rows;
+    p.W = W;
+    p.w_rows = w_rows;
+    p.tokens = tokens;
+    p.live_tokens = live;
+    p.features = features;
+    p.K = K;
+    p.mode = mode;
+    p.swap = swap;
+    p.out = out;
+    p.ldo = ldo;
+    return p;
+}
+
+// install staged page-table rows: rows packed back to back, offsets per seq
+__global__ void install_pages_kernel(const int32_t* __restrict__ rows, const int32_t* __restrict__ off,
+                                     const int32_t* __restrict__ seq_slot, int32_t* __restrict__ table,
+                                     int max_pages) {
+    const int s = blockIdx.x;
+    const int b = off[s], e = off[s + 1];
+    int32_t* dst = table + static_cast<int64_t>(seq_slot[s]) * max_pages;
+    for (int i = threadIdx.x; i < e - b; i += blockDim.x) dst[i] = rows[b + i];
+}
+
+void lm_head(sw_model* m, Workspace& w, int rows, const int* live, float* logits_out, cudaStream_t st) {
+    const sw_model_desc& d = m->desc;
+    GemmProblem p = gp(w.xlast, kLmRowsMax, m->lm, d.vocab, rows, d.vocab, d.d_model, EPI_ARGMAX, true, nullptr, 0,
+                       live);
+    p.argmax = w.keys;
+    gemm_run(p, st);
+    if (logits_out) {
+        GemmProblem q = gp(w.xlast, kLmRowsMax, m->lm, d.vocab, rows, d.vocab, d.d_model, EPI_STORE_F32, true,
+                           logits_out, d.vocab, live);
+        gemm_run(q, st);
+    }
+}
+
+}  // namespace
+
+int decode_bucket(int n) {
+    static const int kBuckets[] = {1, 2, 4, 8, 16, 24, 32, 48, 64, 96, 128, 160, 192, 224, 256};
+    for (int b : kBuckets)
+        if (n <= b) return b;
+    throw ContractViolation("decode: batch of " + std::to_string(n) + " rows exceeds 256");
+}
+
+// ------------------------------------------------------------------ prefill
+void prefill_forward(sw_model* m, sw_kv* kv, const sw_batch& b, cudaStream_t st) {
+    const sw_model_desc& d = m->desc;
+    Workspace& w = m->pre;
+    const int B = kv->page_tokens;
+    // Split the batch into chunks of whole prompts that fit the workspace.
+    int first = 0;
+    int64_t tok_off = 0, page_off = 0;
+    while (first < b.n) {
+        int last = first, T = 0;
+        while (last < b.n && T + b.n_tokens[last] <= w.rows && last - first < kLmRowsMax) T += b.n_tokens[last++];
+        if (last == first)
+            throw ConfigError("prefill: prompt of " + std::to_string(b.n_tokens[first]) +
+                              " tokens exceeds model.max_prefill_tokens=" + std::to_string(w.rows));
+        const int S = last - first;
+        // ---- stage metadata (one H2D copy)
+        int idx;
+        int32_t* h = static_cast<int32_t*>(ring_claim(m->pre_ring, idx));
+        int32_t* p = h + 16;
+        auto take = [&](int n) {
+            int32_t* q = p;
+            p += n;
+            return q;
+        };
+        int32_t *tokens = take(T), *tpos = take(T), *tslot = take(T), *cu = take(S + 1), *sslot = take(S),
+                *lastrow = take(S), *oidx = take(S), *poff = take(S + 1);
+        int n_tiles = 0;
+        for (int s = 0; s < S; ++s) n_tiles += cdiv(b.n_tokens[first + s], 64);
+        int32_t *tseq = take(n_tiles), *tq0 = take(n_tiles);
+        int n_pages_total = 0;
+        for (int s = 0; s < S; ++s) n_pages_total += cdiv(b.n_tokens[first + s], B);
+        int32_t* prow = take(n_pages_total);
+        int t = 0, ti = 0, pg = 0;
+        cu[0] = 0;
+        poff[0] = 0;
+        for (int s = 0; s < S; ++s) {
+            const int r = first + s, n = b.n_tokens[r];
+            if (b.slots[r] < 0 || b.slots[r] >= kv->n_slots) throw ContractViolation("prefill: slot out of range");
+            const int np = cdiv(n, B);
+            if (np > kv->max_pages) throw ContractViolation("prefill: prompt exceeds the slot's page-table row");
+            for (int j = 0; j < n; ++j) {
+                tokens[t + j] = b.tokens[tok_off + j];
+                if (tokens[t + j] < 0 || tokens[t + j] >= d.vocab) throw ContractViolation("prefill: token out of range");
+                tpos[t + j] = j;
+                tslot[t + j] = b.slots[r];
+            }
+            for (int j = 0; j < np; ++j) {
+                const int pid = b.page_rows[page_off + j];
+                if (pid < 0 || pid >= kv->n_pages) throw ContractViolation("prefill: page id out of range");
+                prow[pg + j] = pid;
+            }
+            for (int q0 = 0; q0 < n; q0 += 64, ++ti) {
+                tseq[ti] = s;
+                tq0[ti] = q0;
+            }
+            tok_off += n;
+            page_off += np;
+            t += n;
+            pg += np;
+            cu[s + 1] = t;
+            poff[s + 1] = pg;
+            sslot[s] = b.slots[r];
+            lastrow[s] = t - 1;
+            oidx[s] = b.out_index ? b.out_index[r] : 0;
+        }
+        h[0] = T;
+        h[1] = S;
+        h[2] = n_tiles;
+        const size_t bytes = static_cast<size_t>(p - h) * sizeof(int32_t);
+        if (bytes > w.pmeta_bytes || bytes > m->pre_ring.bytes) throw ContractViolation("prefill: metadata overflow");
+        SW_CUDA(cudaMemcpyAsync(w.pmeta, h, bytes, cudaMemcpyHostToDevice, st));
+        ring_release(m->pre_ring, idx, st);
+        auto dev = [&](int32_t* hp) { return w.pmeta + (hp - h); };
+
+        install_pages_kernel<<<S, 64, 0, st>>>(dev(prow), dev(poff), dev(sslot), kv->page_table, kv->max_pages);
+        SW_LAUNCH_CHECK();
+        // ---- layers
+        const int qkv_w = (d.n_heads + 2 * d.n_kv_heads) * d.head_dim;
+        const int hdH = d.n_heads * d.head_dim;
+        embed_tokens(dev(tokens), w.pmeta, T, m->emb, w.x, d.d_model, st);
+        PrefillAttnArgs aa{};
+        aa.n_tiles = w.pmeta + 2;
+        aa.tile_seq = dev(tseq);
+        aa.tile_q0 = dev(tq0);
+        aa.cu_seqlens = dev(cu);
+        aa.seq_slot = dev(sslot);
+        aa.page_table = kv->page_table;
+        aa.max_pages = kv->max_pages;
+        aa.page_tokens = B;
+        aa.page_stride = kv->page_stride;
+        aa.kv_stride = kv->page_stride / 2;
+        aa.H = d.n_heads;
+        aa.Hkv = d.n_kv_heads;
+        aa.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(d.head_dim)));
+        for (int l = 0; l < d.n_layers; ++l) {
+            const LayerWeights& L = m->layers[l];
+            __nv_bfloat16* kvl = kv->pages + l * kv->layer_stride;
+            rmsnorm(w.x, L.g_attn, w.xn, T, d.d_model, d.norm_eps, nullptr, nullptr, st);
+            gemm_run(gp(w.xn, w.rows, L.wqkv, qkv_w, T, qkv_w, d.d_model, EPI_STORE, false, w.qkv, qkv_w), st);
+            rope_kv(w.qkv, w.q, kvl, dev(tpos), dev(tslot), kv->page_table, m->inv_freq, T, nullptr, d.n_heads,
+                    d.n_kv_heads, d.head_dim, kv->max_pages, B, st);
+            attn_prefill(w.q, kvl, w.attn, aa, n_tiles, d.head_dim, st);
+            gemm_run(gp(w.attn, w.rows, L.wo, d.d_model, T, d.d_model, hdH, EPI_RESID, false, w.x, d.d_model), st);
+            rmsnorm(w.x, L.g_mlp, w.xn, T, d.d_model, d.norm_eps, nullptr, nullptr, st);
+            gemm_run(gp(w.xn, w.rows, L.wgu, 2 * d.ffn_dim, T, 2 * d.ffn_dim, d.d_model, EPI_SWIGLU, false, w.act,
+                        d.ffn_dim),
+                     st);
+            gemm_run(gp(w.act, w.rows, L.wd, d.d_model, T, d.d_model, d.ffn_dim, EPI_RESID, false, w.x, d.d_model), st);
+        }
+        // ---- last position of every prompt -> LM head + greedy token
+        rmsnorm(w.x, m->g_final, w.xlast, S, d.d_model, d.norm_eps, nullptr, dev(lastrow), st);
+        lm_head(m, w, S, nullptr, b.logits_out ? b.logits_out + static_cast<int64_t>(first) * d.vocab : nullptr, st);
+        finalize_tokens(w.keys, dev(sslot), dev(oidx), S, nullptr, kv->last_token, kv->out_tokens, kv->max_out, st);
+        first = last;
+    }
+}
+
+// ------------------------------------------------------------------ decode
+namespace {
+
+void decode_layers(sw_model* m, sw_kv* kv, int R, cudaStream_t st) {
+    const sw_model_desc& d = m->desc;
+    Workspace& w = m->dec;
+    const int* live = &w.meta->n;
+    const int qkv_w = (d.n_heads + 2 * d.n_kv_heads) * d.head_dim;
+    const int hdH = d.n_heads * d.head_dim;
+    embed(w.meta, R, m->emb, w.x, d.d_model, kv->last_token, kv->page_table, kv->max_pages, kv->page_tokens, st);
+    DecodeAttnArgs aa{};
+    aa.meta = w.meta;
+    aa.page_table = kv->page_table;
+    aa.max_pages = kv->max_pages;
+    aa.page_tokens = kv->page_tokens;
+    aa.page_stride = kv->page_stride;
+    aa.kv_stride = kv->page_stride / 2;
+    aa.H = d.n_heads;
+    aa.Hkv = d.n_kv_heads;
+    aa.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(d.head_dim)));
+    aa.chunk = kv->chunk;
+    aa.max_splits = kv->max_splits;
+    aa.part_o = w.part_o;
+    aa.part_ml = w.part_ml;
+    for (int l = 0; l < d.n_layers; ++l) {
+        const LayerWeights& L = m->layers[l];
+        __nv_bfloat16* kvl = kv->pages + l * kv->layer_stride;
+        rmsnorm(w.x, L.g_attn, w.xn, R, d.d_model, d.norm_eps, live, nullptr, st);
+        gemm_run(gp(w.xn, w.rows, L.wqkv, qkv_w, R, qkv_w, d.d_model, EPI_STORE, true, w.qkv, qkv_w, live), st);
+        rope_kv(w.qkv, w.q, kvl, w.meta->pos, w.meta->slot, kv->page_table, m->inv_freq, R, live, d.n_heads,
+                d.n_kv_heads, d.head_dim, kv->max_pages, kv->page_tokens, st);
+        attn_decode(w.q, kvl, w.attn, aa, R, d.head_dim, st);
+        gemm_run(gp(w.attn, w.rows, L.wo, d.d_model, R, d.d_model, hdH, EPI_RESID, true, w.x, d.d_model, live), st);
+        rmsnorm(w.x, L.g_mlp, w.xn, R, d.d_model, d.norm_eps, live, nullptr, st);
+        gemm_run(gp(w.xn, w.rows, L.wgu, 2 * d.ffn_dim, R, 2 * d.ffn_dim, d.d_model, EPI_SWIGLU, true, w.act,
+                    d.ffn_dim, live),
+                 st);
+        gemm_run(gp(w.act, w.rows, L.wd, d.d_model, R, d.d_model, d.ffn_dim, EPI_RESID, true, w.x, d.d_model, live),
+                 st);
+    }
+    rmsnorm(w.x, m->g_final, w.xlast, R, d.d_model, d.norm_eps, live, nullptr, st);
+    lm_head(m, w, R, live, nullptr, st);
+    finalize_tokens(w.keys, w.meta->slot, w.meta->out_index, R, live, kv->last_token, kv->out_tokens, kv->max_out, st);
+}
+
+}  // namespace
+
+void decode_forward(sw_model* m, sw_kv* kv, const sw_batch& b, cudaStream_t st, bool use_graph) {
+    const sw_model_desc& d = m->desc;
+    if (b.n < 1 || b.n > kMaxDecodeRows) throw ContractViolation("decode: batch size out of range");
+    if (b.n > m->dec.rows) throw ConfigError("decode: batch exceeds model.max_decode_batch");
+    int idx;
+    StepMeta* h = static_cast<StepMeta*>(ring_claim(m->dec_ring, idx));
+    h->n = b.n;
+    for (int i = 0; i < b.n; ++i) {
+        const int slot = b.slots[i], pos = b.positions[i];
+        if (slot < 0 || slot >= kv->n_slots) throw ContractViolation("decode: slot out of range");
+        if (pos < 0 || pos >= kv->max_pages * kv->page_tokens) throw ContractViolation("decode: position out of range");
+        h->slot[i] = slot;
+        h->pos[i] = pos;
+        h->token[i] = b.tokens ? b.tokens[i] : -1;
+        h->new_page[i] = b.new_page ? b.new_page[i] : -1;
+        if (h->new_page[i] >= kv->n_pages) throw ContractViolation("decode: page id out of range");
+        h->out_index[i] = b.out_index ? b.out_index[i] : -1;
+    }
+    const size_t bytes = offsetof(StepMeta, slot) + sizeof(StepMeta::slot) * 5;
+    SW_CUDA(cudaMemcpyAsync(m->dec.meta, h, bytes, cudaMemcpyHostToDevice, st));
+    ring_release(m->dec_ring, idx, st);
+    const int R = std::min(decode_bucket(b.n), m->dec.rows);
+    DecodeGraph& g = m->graphs[{kv, R}];
+    if (use_graph && g.exec) {
+        SW_CUDA(cudaGraphLaunch(g.exec, st));
+    } else {
+        decode_layers(m, kv, R, st);
+        if (use_graph && ++g.eager_runs >= 1) {
+            // capture once the kernels' attributes are configured (first eager run)
+            cudaStream_t cs;
+            SW_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+            cudaGraph_t graph;
+            SW_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+            decode_layers(m, kv, R, cs);
+            SW_CUDA(cudaStreamEndCapture(cs, &graph));
+            SW_CUDA(cudaGraphInstantiate(&g.exec, graph, 0));
+            SW_CUDA(cudaGraphDestroy(graph));
+            SW_CUDA(cudaStreamDestroy(cs));
+        }
+    }
+    if (b.logits_out) {
+        GemmProblem q = gp(m->dec.xlast, kLmRowsMax, m->lm, d.vocab, b.n, d.vocab, d.d_model, EPI_STORE_F32, true,
+                           b.logits_out, d.vocab);
+        gemm_run(q, st);
+    }
+}
+
+}  // namespace sw
+
+// ====================================================================== C-ABI
+using namespace sw;
+
+extern "C" int sw_model_create(const sw_model_desc* desc, int device, sw_model** out) {
+    return guarded([&] {
+        if (!desc || !out) throw ConfigError("sw_model_create: null argument");
+        const sw_model_desc& d = *desc;
+        if (d.n_layers < 1 || d.d_model % 64 || d.n_heads < 1 || d.n_kv_heads < 1 || d.n_heads % d.n_kv_heads ||
+            (d.head_dim != 64 && d.head_dim != 128) || d.ffn_dim % 64 || d.vocab % 128 || d.vocab < 128)
+            throw ConfigError("model: unsupported shape (d%64, hd in {64,128}, ffn%64, vocab%128, H%Hkv)");
+        if (((d.n_heads + 2 * d.n_kv_heads) * d.head_dim) % 256 || d.d_model % 256 || (2 * d.ffn_dim) % 256)
+            throw ConfigError("model: projection widths must be multiples of 256");
+        if (d.max_prefill_tokens < 64 || d.max_decode_batch < 1 || d.max_decode_batch > kMaxDecodeRows)
+            throw ConfigError("model: bad workspace sizes");
+        SW_CUDA(cudaSetDevice(device));
+        auto m = std::make_unique<sw_model>();
+        m->desc = d;
+        m->device = device;
+        const int64_t D = d.d_model, V = d.vocab, F = d.ffn_dim, hd = d.head_dim;
+        const int64_t qkv_w = (d.n_heads + 2 * d.n_kv_heads) * hd;
+        // carve the weight arena
+        std::vector<std::pair<std::string, int64_t>> plan;
+        plan.push_back({"emb", V * D});
+        if (!d.tied_embeddings) plan.push_back({"lm", V * D});
+        plan.push_back({"g_final", D});
+        for (int l = 0; l < d.n_layers; ++l) {
+            const std::string p = "layer" + std::to_string(l) + ".";
+            plan.push_back({p + "wqkv", qkv_w * D});
+            plan.push_back({p + "wo", D * d.n_heads * hd});
+            plan.push_back({p + "wgu", 2 * F * D});
+            plan.push_back({p + "wd", D * F});
+            plan.push_back({p + "g_attn", D});
+            plan.push_back({p + "g_mlp", D});
+        }
+        size_t total = 0;
+        for (auto& [n, e] : plan) total = align_up(total, 256) + static_cast<size_t>(e) * 2;
+        m->weight_bytes = total;
+        SW_CUDA(cudaMalloc(&m->weight_arena, total));
+        size_t off = 0;
+        for (auto& [n, e] : plan) {
+            off = align_up(off, 256);
+            m->tensors[n] = {static_cast<char*>(m->weight_arena) + off, e};
+            off += static_cast<size_t>(e) * 2;
+        }
+        auto T = [&](const std::string& n) { return static_cast<__nv_bfloat16*>(m->tensors.at(n).first); };
+        m->emb = T("emb");
+        m->lm = d.tied_embeddings ? m->emb : T("lm");
+        m->g_final = T("g_final");
+        cudaStream_t st = nullptr;
+        // synthetic weights: tensor k, element i of the LOGICAL [out, in] shape (oracle/model.py)
+        const uint64_t seed = d.seed;
+        init_tensor(m->emb, V, D, seed, 0, D, 0, 0, 0, st);
+        fill_bf16(m->g_final, D, 1.0f, st);
+        const int H = d.n_heads, Hk = d.n_kv_heads;
+        for (int l = 0; l < d.n_layers; ++l) {
+            const std::string p = "layer" + std::to_string(l) + ".";
+            LayerWeights L{};
+            L.wqkv = T(p + "wqkv");
+            L.wo = T(p + "wo");
+            L.wgu = T(p + "wgu");
+            L.wd = T(p + "wd");
+            L.g_attn = T(p + "g_attn");
+            L.g_mlp = T(p + "g_mlp");
+            const int k0 = 1 + 7 * l;
+            init_tensor(L.wqkv, H * hd, D, seed, k0 + 0, D, 0, 0, 0, st);
+            init_tensor(L.wqkv + H * hd * D, Hk * hd, D, seed, k0 + 1, D, 0, 0, 0, st);
+            init_tensor(L.wqkv + (H + Hk) * hd * D, Hk * hd, D, seed, k0 + 2, D, 0, 0, 0, st);
+            init_tensor(L.wo, D, H * hd, seed, k0 + 3, H * hd, 0, 0, 0, st);
+            init_tensor(L.wgu, F, D, seed, k0 + 4, D, 64, 128, 0, st);   // gate rows -> [128j, 128j+64)
+            init_tensor(L.wgu, F, D, seed, k0 + 5, D, 64, 128, 64, st);  // up rows   -> [128j+64, 128j+128)
+            init_tensor(L.wd, D, F, seed, k0 + 6, F, 0, 0, 0, st);
+            fill_bf16(L.g_attn, D, 1.0f, st);
+            fill_bf16(L.g_mlp, D, 1.0f, st);
+            m->layers.push_back(L);
+        }
+        if (!d.tied_embeddings) init_tensor(m->lm, V, D, seed, 1 + 7 * d.n_layers, D, 0, 0, 0, st);
+        std::vector<float> inv(hd / 2);
+        for (int i = 0; i < hd / 2; ++i)
+            inv[i] = static_cast<float>(1.0 / std::pow(static_cast<double>(d.rope_theta), 2.0 * i / hd));
+        m->inv_freq = dalloc<float>(hd / 2);
+        SW_CUDA(cudaMemcpy(m->inv_freq, inv.data(), inv.size() * 4, cudaMemcpyHostToDevice));
+        ws_alloc(m->pre, d, d.max_prefill_tokens, false, 1);
+        ws_alloc(m->dec, d, std::min(d.max_decode_batch, kMaxDecodeRows), true, 16);
+        ring_init(m->pre_ring, 4, m->pre.pmeta_bytes);
+        ring_init(m->dec_ring, 8, sizeof(StepMeta));
+        m->scratch_u64 = dalloc<unsigned long long>(1);
+        SW_CUDA(cudaDeviceSynchronize());
+        *out = m.release();
+    });
+}
+
+extern "C" int sw_model_destroy(sw_model* m) {
+    return guarded([&] {
+        if (!m) return;
+        cudaDeviceSynchronize();
+        for (auto& [k, g] : m->graphs)
+            if (g.exec) cudaGraphExecDestroy(g.exec);
+        for (Workspace* w : {&m->pre, &m->dec}) {
+            for (void* p : {(void*)w->x, (void*)w->xn, (void*)w->qkv, (void*)w->q, (void*)w->attn, (void*)w->act,
+                            (void*)w->xlast, (void*)w->keys, (void*)w->meta, (void*)w->part_o, (void*)w->part_ml,
+                            (void*)w->pmeta})
+                if (p) cudaFree(p);
+        }
+        for (PinnedRing* r : {&m->pre_ring, &m->dec_ring}) {
+            for (void* p : r->slots) cudaFreeHost(p);
+            for (cudaEvent_t e : r->done) cudaEventDestroy(e);
+        }
+        cudaFree(m->inv_freq);
+        cudaFree(m->scratch_u64);
+        cudaFree(m->weight_arena);
+        delete m;
+    });
+}
+
+extern "C" int sw_model_weight_checksum(sw_model* m, uint64_t* out) {
+    return guarded([&] {
+        SW_CUDA(cudaMemset(m->scratch_u64, 0, 8));
+        checksum_bf16(m->weight_arena, static_cast<int64_t>(m->weight_bytes / 2), m->scratch_u64, nullptr);
+        unsigned long long v = 0;
+        SW_CUDA(cudaMemcpy(&v, m->scratch_u64, 8, cudaMemcpyDeviceToHost));
+        *out = v;
+    });
+}
+
+extern "C" int sw_model_tensor(sw_model* m, const char* name, void** ptr, int64_t* numel) {
+    return guarded([&] {
+        auto it = m->tensors.find(name);
+        if (it == m->tensors.end()) throw ConfigError(std::string("model: no tensor '") + name + "'");
+        *ptr = it->second.first;
+        *numel = it->second.second;
+    });
+}
+
+extern "C" int sw_kv_arena_create(sw_model* m, int64_t n_pages, int32_t n_slots, int32_t max_pages_per_slot,
+                                  int32_t max_out_tokens, sw_kv** out) {
+    return guarded([&] {
+        if (!m || !out || n_pages < 1 || n_slots < 1 || max_pages_per_slot < 1 || max_out_tokens < 1)
+            throw ConfigError("sw_kv_arena_create: bad arguments");
+        const sw_model_desc& d = m->desc;
+        auto kv = std::make_unique<sw_kv>();
+        kv->model = m;
+        kv->n_pages = n_pages;
+        kv->n_slots = n_slots;
+        kv->max_pages = max_pages_per_slot;
+        kv->max_out = max_out_tokens;
+        kv->page_tokens = 16;
+        kv->page_stride = 2LL * d.n_kv_heads * kv->page_tokens * d.head_dim;
+        kv->layer_stride = kv->page_stride * n_pages;
+        const size_t bytes = static_cast<size_t>(kv->layer_stride) * d.n_layers * 2;
+        SW_CUDA(cudaMalloc(&kv->pages, bytes));
+        kv->page_table = dalloc<int32_t>(static_cast<size_t>(n_slots) * max_pages_per_slot);
+        SW_CUDA(cudaMemset(kv->page_table, 0, static_cast<size_t>(n_slots) * max_pages_per_slot * 4));
+        kv->last_token = dalloc<int32_t>(n_slots);
+        SW_CUDA(cudaMemset(kv->last_token, 0, static_cast<size_t>(n_slots) * 4));
+        kv->out_tokens = dalloc<int32_t>(static_cast<size_t>(n_slots) * max_out_tokens);
+        SW_CUDA(cudaMemset(kv->out_tokens, 0xff, static_cast<size_t>(n_slots) * max_out_tokens * 4));
+        // split-KV geometry: at most 16 splits of >= 256 keys (multiple of 64)
+        const int max_ctx = max_pages_per_slot * kv->page_tokens;
+        kv->chunk = std::max(256, (cdiv(max_ctx, 16) + 63) / 64 * 64);
+        kv->max_splits = cdiv(max_ctx, kv->chunk);
+        *out = kv.release();
+    });
+}
+
+extern "C" int sw_kv_arena_destroy(sw_kv* kv) {
+    return guarded([&] {
+        if (!kv) return;
+        cudaDeviceSynchronize();
+        for (auto it = kv->model->graphs.begin(); it != kv->model->graphs.end();) {
+            if (it->first.first == kv) {
+                if (it->second.exec) cudaGraphExecDestroy(it->second.exec);
+                it = kv->model->graphs.erase(it);
+            } else {
+                ++it;
+            }
+        }
+        cudaFree(kv->pages);
+        cudaFree(kv->page_table);
+        cudaFree(kv->last_token);
+        cudaFree(kv->out_tokens);
+        delete kv;
+    });
+}
+
+extern "C" int sw_kv_arena_views(sw_kv* kv, int32_t** page_table, int32_t** last_token, int32_t** out_tokens,
+                                 void** pages) {
+    return guarded([&] {
+        if (page_table) *page_table = kv->page_table;
+        if (last_token) *last_token = kv->last_token;
+        if (out_tokens) *out_tokens = kv->out_tokens;
+        if (pages) *pages = kv->pages;
+    });
+}
+
+extern "C" int sw_prefill_enqueue(sw_model* m, sw_kv* kv, const sw_batch* b, void* stream) {
+    return guarded([&] {
+        if (!m || !kv || !b || !b->slots || !b->n_tokens || !b->tokens || !b->page_rows)
+            throw ConfigError("sw_prefill_enqueue: null argument");
+        prefill_forward(m, kv, *b, static_cast<cudaStream_t>(stream));
+    });
+}
+
+extern "C" int sw_decode_enqueue(sw_model* m, sw_kv* kv, const sw_batch* b, void* stream) {
+    return guarded([&] {
+        if (!m || !kv || !b || !b->slots || !b->positions) throw ConfigError("sw_decode_enqueue: null argument");
+        decode_forward(m, kv, *b, static_cast<cudaStream_t>(stream), /*use_graph=*/b->logits_out == nullptr);
+    });
+}
+
+// ---- op level (kernel unit tests)
+extern "C" int sw_op_gemm(const void* A, const void* B, void* C, int32_t M, int32_t N, int32_t K, int32_t epilogue,
+                          void* stream) {
+    return guarded([&] {
+        // A = activations [M, K], B = weights [N, K]; swap-AB when M <= 256
+        const bool swap = M <= 256;
+        GemmProblem p = gp(A, M, B, N, M, N, K, epilogue, swap, C, epilogue == EPI_SWIGLU ? N / 2 : N);
+        gemm_run(p, static_cast<cudaStream_t>(stream));
+    });
+}
+
+extern "C" int sw_op_rmsnorm(const float* x, const void* gain, void* y, int32_t rows, int32_t dim, float eps,
+                             void* stream) {
+    return guarded([&] {
+        rmsnorm(x, static_cast<const __nv_bfloat16*>(gain), static_cast<__nv_bfloat16*>(y), rows, dim, eps, nullptr,
+                nullptr, static_cast<cudaStream_t>(stream));
+    });
+}

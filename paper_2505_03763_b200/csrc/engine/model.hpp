@@ -1,0 +1,99 @@
+// Model + KV arena objects behind the kernel-level C-ABI (sw_model / sw_kv).
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../../include/splitwise.h"
+#include "../kernels/attention.cuh"
+#include "../kernels/elementwise.cuh"
+
+namespace sw {
+
+struct LayerWeights {
+    __nv_bfloat16* wqkv;  // [(H + 2Hkv) hd, d]  rows: q heads | k heads | v heads
+    __nv_bfloat16* wo;    // [d, H hd]
+    __nv_bfloat16* wgu;   // [2 ffn, d]  blocks of 128 rows: [gate 64 | up 64]
+    __nv_bfloat16* wd;    // [d, ffn]
+    __nv_bfloat16* g_attn;
+    __nv_bfloat16* g_mlp;
+};
+
+// Per-phase activation workspace (one per stream: prefill and decode never
+// share buffers, so the two phases can run concurrently).
+struct Workspace {
+    int rows = 0;
+    float* x = nullptr;              // [rows, d] residual stream, fp32
+    __nv_bfloat16* xn = nullptr;     // [rows, d]
+    __nv_bfloat16* qkv = nullptr;    // [rows, (H + 2Hkv) hd]
+    __nv_bfloat16* q = nullptr;      // [rows, H hd] roped
+    __nv_bfloat16* attn = nullptr;   // [rows, H hd]
+    __nv_bfloat16* act = nullptr;    // [rows, ffn]
+    __nv_bfloat16* xlast = nullptr;  // [256, d] rows feeding the LM head
+    unsigned long long* keys = nullptr;  // [256] packed argmax
+    // decode only
+    StepMeta* meta = nullptr;
+    float* part_o = nullptr;
+    float* part_ml = nullptr;
+    // prefill only: device metadata block
+    int32_t* pmeta = nullptr;
+    size_t pmeta_bytes = 0;
+};
+
+struct PinnedRing {
+    std::vector<void*> slots;
+    std::vector<cudaEvent_t> done;
+    size_t bytes = 0;
+    int next = 0;
+};
+
+struct DecodeGraph {
+    cudaGraphExec_t exec = nullptr;
+    int eager_runs = 0;
+};
+
+}  // namespace sw
+
+struct sw_model {
+    sw_model_desc desc{};
+    int device = 0;
+    void* weight_arena = nullptr;
+    size_t weight_bytes = 0;
+    __nv_bfloat16* emb = nullptr;
+    __nv_bfloat16* lm = nullptr;
+    __nv_bfloat16* g_final = nullptr;
+    std::vector<sw::LayerWeights> layers;
+    std::map<std::string, std::pair<void*, int64_t>> tensors;
+    float* inv_freq = nullptr;
+    sw::Workspace pre, dec;
+    sw::PinnedRing pre_ring, dec_ring;
+    std::map<std::pair<const sw_kv*, int>, sw::DecodeGraph> graphs;  // (arena, row bucket)
+    unsigned long long* scratch_u64 = nullptr;
+};
+
+struct sw_kv {
+    sw_model* model = nullptr;
+    int64_t n_pages = 0;
+    int32_t n_slots = 0, max_pages = 0, max_out = 0;
+    int page_tokens = 16;
+    __nv_bfloat16* pages = nullptr;  // [L][n_pages][2][Hkv][B][hd]
+    int32_t* page_table = nullptr;   // [n_slots][max_pages]
+    int32_t* last_token = nullptr;   // [n_slots]
+    int32_t* out_tokens = nullptr;   // [n_slots][max_out]
+    int64_t layer_stride = 0;        // elements per layer
+    int64_t page_stride = 0;         // elements per page (one layer)
+    int chunk = 256;
+    int max_splits = 1;
+};
+
+namespace sw {
+// Forward passes (stream-ordered; host arrays staged internally).
+void prefill_forward(sw_model* m, sw_kv* kv, const sw_batch& b, cudaStream_t st);
+void decode_forward(sw_model* m, sw_kv* kv, const sw_batch& b, cudaStream_t st, bool use_graph);
+int decode_bucket(int n);
+}  // namespace sw

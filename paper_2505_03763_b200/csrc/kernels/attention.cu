@@ -1,0 +1,439 @@
+// Attention over the paged KV cache.
+//
+// Prefill: causal flash attention (online softmax, fp32 statistics) for a
+//   varlen batch of prompts, GQA.  One CTA = 64 query rows of one head of one
+//   prompt (4 warps x 16 rows); K/V stream through smem in 64-key blocks read
+//   straight from the 16-token pages just written by rope_kv (double-buffered
+//   cp.async, XOR-swizzled 16 B chunks for conflict-free ldmatrix); QK^T and
+//   PV on the tensor cores with mma.m16n8k16 bf16 -> fp32.
+// Decode: split-KV paged attention.  One CTA = one (row, kv head, split of
+//   the context); the G = H/Hkv query heads sharing the kv head are packed so
+//   every K/V byte is read once per step.  64-key steps double-buffered in
+//   smem; partial (max, sum, unnormalised O) per split, merged by
+//   attn_decode_combine.  HBM-bound by design.
+#include "attention.cuh"
+#include "common.cuh"
+
+namespace sw {
+
+namespace {
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
+    const int sz = valid ? 16 : 0;  // zero-fill when invalid
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_addr(smem)), "l"(gmem), "r"(sz)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+__device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], const void* p) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"(smem_addr(p)));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t (&r)[4], const void* p) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"(smem_addr(p)));
+}
+__device__ __forceinline__ void mma_bf16(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};"
+        : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+// [rows][HD] bf16 tile, 16 B chunks XOR-swizzled by row.
+template <int HD>
+__device__ __forceinline__ int swz(int row, int chunk) {
+    return row * HD + ((chunk ^ (row & 7)) << 3);
+}
+
+constexpr int kQRows = 64;
+constexpr int kKeys = 64;
+
+template <int HD>
+__global__ void __launch_bounds__(128) attn_prefill_kernel(const __nv_bfloat16* __restrict__ q,
+                                                           const __nv_bfloat16* __restrict__ kv_layer,
+                                                           __nv_bfloat16* __restrict__ out, PrefillAttnArgs a) {
+    extern __shared__ __align__(128) uint8_t smem_raw[];
+    __nv_bfloat16* sQ = reinterpret_cast<__nv_bfloat16*>(smem_raw);
+    __nv_bfloat16* sK = sQ + kQRows * HD;       // [2][64][HD]
+    __nv_bfloat16* sV = sK + 2 * kKeys * HD;    // [2][64][HD]
+    constexpr int CH = HD / 8;                  // 16 B chunks per row
+
+    const int tile = blockIdx.x;
+    if (tile >= *a.n_tiles) return;
+    const int h = blockIdx.y;
+    const int hk = h / (a.H / a.Hkv);
+    const int s = a.tile_seq[tile];
+    const int q0 = a.tile_q0[tile];
+    const int start = a.cu_seqlens[s];
+    const int len = a.cu_seqlens[s + 1] - start;
+    const int slot = a.seq_slot[s];
+    const int32_t* ptab = a.page_table + static_cast<int64_t>(slot) * a.max_pages;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int64_t qstride = static_cast<int64_t>(a.H) * HD;
+
+    // Q tile -> smem (zero rows past the prompt)
+    for (int i = tid; i < kQRows * CH; i += 128) {
+        const int r = i / CH, c = i % CH;
+        const bool ok = q0 + r < len;
+        const __nv_bfloat16* src = q + (start + (ok ? q0 + r : 0)) * qstride + h * HD + c * 8;
+        cp_async16(sQ + swz<HD>(r, c), src, ok);
+    }
+    auto load_kv = [&](int blk, int buf) {
+        for (int i = tid; i < kKeys * CH; i += 128) {
+            const int r = i / CH, c = i % CH;
+            const int key = blk * kKeys + r;
+            const bool ok = key < len;
+            const int page = ok ? ptab[key / a.page_tokens] : 0;
+            const __nv_bfloat16* base = kv_layer + static_cast<int64_t>(page) * a.page_stride +
+                                        static_cast<int64_t>(hk) * a.page_tokens * HD +
+                                        static_cast<int64_t>(key % a.page_tokens) * HD + c * 8;
+            cp_async16(sK + buf * kKeys * HD + swz<HD>(r, c), base, ok);
+            cp_async16(sV + buf * kKeys * HD + swz<HD>(r, c), base + a.kv_stride, ok);
+        }
+    };
+    const int last_blk = min((q0 + kQRows - 1) / kKeys, (len - 1) / kKeys);
+    load_kv(0, 0);
+    cp_async_commit();
+
+    uint32_t qf[HD / 16][4];
+    float o[HD / 8][4];
+#pragma unroll
+    for (int i = 0; i < HD / 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+    float m_run[2] = {-INFINITY, -INFINITY}, l_run[2] = {0.f, 0.f};
+    const int row_a = q0 + warp * 16 + (lane >> 2);  // query position of c0/c1; +8 for c2/c3
+
+    for (int blk = 0; blk <= last_blk; ++blk) {
+        const int buf = blk & 1;
+        if (blk < last_blk) {
+            load_kv(blk + 1, buf ^ 1);
+            cp_async_commit();
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncthreads();
+        if (blk == 0) {
+#pragma unroll
+            for (int ks = 0; ks < HD / 16; ++ks) {
+                const int r = warp * 16 + (lane & 15);
+                const int c = ks * 2 + (lane >> 4);
+                ldsm_x4(qf[ks], sQ + swz<HD>(r, c));
+            }
+        }
+        const __nv_bfloat16* K = sK + buf * kKeys * HD;
+        const __nv_bfloat16* V = sV + buf * kKeys * HD;
+        float sc[8][4];
+#pragma unroll
+        for (int nb = 0; nb < 8; ++nb) sc[nb][0] = sc[nb][1] = sc[nb][2] = sc[nb][3] = 0.f;
+#pragma unroll
+        for (int ks = 0; ks < HD / 16; ++ks) {
+#pragma unroll
+            for (int np = 0; np < 4; ++np) {
+                uint32_t b[4];
+                const int key = np * 16 + (lane & 7) + ((lane >> 4) << 3);
+                const int c = ks * 2 + ((lane >> 3) & 1);
+                ldsm_x4(b, K + swz<HD>(key, c));
+                mma_bf16(sc[2 * np], qf[ks], b[0], b[1]);
+                mma_bf16(sc[2 * np + 1], qf[ks], b[2], b[3]);
+            }
+        }
+        // mask + online softmax (log2 domain)
+        const bool edge = (blk + 1) * kKeys > q0 || (blk + 1) * kKeys > len;
+        float mx[2] = {-INFINITY, -INFINITY};
+#pragma unroll
+        for (int nb = 0; nb < 8; ++nb) {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                float v = sc[nb][e] * a.scale_log2;
+                if (edge) {
+                    const int key = blk * kKeys + nb * 8 + (lane & 3) * 2 + (e & 1);
+                    const int qp = row_a + ((e >> 1) << 3);
+                    if (key > qp || key >= len) v = -INFINITY;
+                }
+                sc[nb][e] = v;
+                mx[e >> 1] = fmaxf(mx[e >> 1], v);
+            }
+        }
+        float alpha[2];
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+            mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 1));
+            mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 2));
+            const float m_new = fmaxf(m_run[r], mx[r]);
+            const float m_use = m_new == -INFINITY ? 0.f : m_new;
+            alpha[r] = exp2f(m_run[r] - m_use);
+            m_run[r] = m_new;
+            mx[r] = m_use;
+        }
+        float rs[2] = {0.f, 0.f};
+#pragma unroll
+        for (int nb = 0; nb < 8; ++nb) {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const float p = exp2f(sc[nb][e] - mx[e >> 1]);
+                sc[nb][e] = p;
+                rs[e >> 1] += p;
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < 2; ++r) l_run[r] = l_run[r] * alpha[r] + rs[r];
+#pragma unroll
+        for (int i = 0; i < HD / 8; ++i) {
+            o[i][0] *= alpha[0];
+            o[i][1] *= alpha[0];
+            o[i][2] *= alpha[1];
+            o[i][3] *= alpha[1];
+        }
+        // O += P V
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+            uint32_t pa[4];
+            pa[0] = pack_bf2(sc[2 * kk][0], sc[2 * kk][1]);
+            pa[1] = pack_bf2(sc[2 * kk][2], sc[2 * kk][3]);
+            pa[2] = pack_bf2(sc[2 * kk + 1][0], sc[2 * kk + 1][1]);
+            pa[3] = pack_bf2(sc[2 * kk + 1][2], sc[2 * kk + 1][3]);
+#pragma unroll
+            for (int dp = 0; dp < HD / 16; ++dp) {
+                uint32_t b[4];
+                const int key = kk * 16 + (lane & 7) + (((lane >> 3) & 1) << 3);
+                const int c = dp * 2 + (lane >> 4);
+                ldsm_x4_t(b, V + swz<HD>(key, c));
+                mma_bf16(o[2 * dp], pa, b[0], b[1]);
+                mma_bf16(o[2 * dp + 1], pa, b[2], b[3]);
+            }
+        }
+        __syncthreads();
+    }
+    // normalise + store (row sums were kept per thread: reduce over the quad)
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+        l_run[r] += __shfl_xor_sync(0xffffffffu, l_run[r], 1);
+        l_run[r] += __shfl_xor_sync(0xffffffffu, l_run[r], 2);
+    }
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+        const int qp = row_a + r * 8;
+        if (qp >= len) continue;
+        const float inv = 1.f / l_run[r];
+        __nv_bfloat16* dst = out + (start + qp) * qstride + h * HD + (lane & 3) * 2;
+#pragma unroll
+        for (int i = 0; i < HD / 8; ++i)
+            *reinterpret_cast<uint32_t*>(dst + i * 8) = pack_bf2(o[i][2 * r] * inv, o[i][2 * r + 1] * inv);
+    }
+}
+
+// ------------------------------------------------------------------ decode
+constexpr int kDecKeys = 64;  // keys per smem step
+constexpr int kPad = 8;       // row padding (bf16) against bank conflicts
+
+template <int HD, int G>
+__global__ void __launch_bounds__(128) attn_decode_kernel(const __nv_bfloat16* __restrict__ q,
+                                                          const __nv_bfloat16* __restrict__ kv_layer,
+                                                          DecodeAttnArgs a) {
+    constexpr int LD = HD + kPad;
+    extern __shared__ __align__(16) uint8_t dsmem[];
+    auto sK = reinterpret_cast<__nv_bfloat16(*)[kDecKeys * LD]>(dsmem);                  // [2]
+    auto sV = reinterpret_cast<__nv_bfloat16(*)[kDecKeys * LD]>(dsmem + 2 * kDecKeys * LD * 2);  // [2]
+    float* sQ = reinterpret_cast<float*>(dsmem + 4 * kDecKeys * LD * 2);                 // [G*HD]
+    auto sS = reinterpret_cast<float(*)[kDecKeys]>(sQ + G * HD);                         // [G]
+    float* sAlpha = reinterpret_cast<float*>(sS + G);
+
+    const int row = blockIdx.z;
+    if (row >= a.meta->n) return;
+    const int ctx = a.meta->pos[row] + 1;
+    const int k_begin = blockIdx.x * a.chunk;
+    if (k_begin >= ctx) return;
+    const int k_end = min(ctx, k_begin + a.chunk);
+    const int hk = blockIdx.y;
+    const int slot = a.meta->slot[row];
+    const int32_t* ptab = a.page_table + static_cast<int64_t>(slot) * a.max_pages;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+    for (int i = tid; i < G * HD; i += 128)
+        sQ[i] = bf2f(q[static_cast<int64_t>(row) * a.H * HD + (hk * G) * HD + i]) * a.scale_log2;
+
+    constexpr int CH = HD / 8;
+    auto load = [&](int k0, int buf) {
+        for (int i = tid; i < kDecKeys * CH; i += 128) {
+            const int r = i / CH, c = i % CH;
+            const int key = k0 + r;
+            const bool ok = key < k_end;
+            const int page = ok ? ptab[key / a.page_tokens] : 0;
+            const __nv_bfloat16* base = kv_layer + static_cast<int64_t>(page) * a.page_stride +
+                                        static_cast<int64_t>(hk) * a.page_tokens * HD +
+                                        static_cast<int64_t>(key % a.page_tokens) * HD + c * 8;
+            cp_async16(&sK[buf][r * LD + c * 8], base, ok);
+            cp_async16(&sV[buf][r * LD + c * 8], base + a.kv_stride, ok);
+        }
+    };
+
+    // thread roles: scores -> key = tid % 64, heads [hq0, hq0 + G/2) (G even) ;
+    // output -> (g, d) pairs strided over the block.
+    constexpr int HPT = G >= 2 ? G / 2 : 1;
+    const int skey = tid & 63;
+    const int hq0 = (tid >> 6) * HPT;
+    constexpr int OUT_PER_T = (G * HD) / 128;
+    float acc[OUT_PER_T];
+#pragma unroll
+    for (int j = 0; j < OUT_PER_T; ++j) acc[j] = 0.f;
+    float m_run = -INFINITY, l_run = 0.f;  // owned by warp g < G (lane 0 copy kept by every lane)
+
+    const int n_steps = cdiv(k_end - k_begin, kDecKeys);
+    load(k_begin, 0);
+    cp_async_commit();
+    __syncthreads();  // sQ ready
+    for (int st = 0; st < n_steps; ++st) {
+        const int buf = st & 1;
+        if (st + 1 < n_steps) {
+            load(k_begin + (st + 1) * kDecKeys, buf ^ 1);
+            cp_async_commit();
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncthreads();
+        const int kbase = k_begin + st * kDecKeys;
+        // scores
+        if (tid < 64 * (G / HPT)) {
+            float dot[HPT];
+#pragma unroll
+            for (int j = 0; j < HPT; ++j) dot[j] = 0.f;
+            const uint4* kr = reinterpret_cast<const uint4*>(&sK[buf][skey * LD]);
+#pragma unroll 4
+            for (int c = 0; c < CH; ++c) {
+                const uint4 kv = kr[c];
+                const float k8[8] = {bf_lo(kv.x), bf_hi(kv.x), bf_lo(kv.y), bf_hi(kv.y),
+                                     bf_lo(kv.z), bf_hi(kv.z), bf_lo(kv.w), bf_hi(kv.w)};
+#pragma unroll
+                for (int j = 0; j < HPT; ++j) {
+                    const float4 qa = *reinterpret_cast<const float4*>(&sQ[(hq0 + j) * HD + c * 8]);
+                    const float4 qb = *reinterpret_cast<const float4*>(&sQ[(hq0 + j) * HD + c * 8 + 4]);
+                    dot[j] += qa.x * k8[0] + qa.y * k8[1] + qa.z * k8[2] + qa.w * k8[3] + qb.x * k8[4] +
+                              qb.y * k8[5] + qb.z * k8[6] + qb.w * k8[7];
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < HPT; ++j) sS[hq0 + j][skey] = kbase + skey < k_end ? dot[j] : -INFINITY;
+        }
+        __syncthreads();
+        // softmax bookkeeping: warp g owns head g
+        if (warp < G) {
+            const float s0 = sS[warp][lane], s1 = sS[warp][lane + 32];
+            const float mx = warp_max(fmaxf(s0, s1));
+            const float m_new = fmaxf(m_run, mx);
+            const float alpha = exp2f(m_run - m_new);  // m_new finite: key k_begin is always valid
+            const float p0 = exp2f(s0 - m_new), p1 = exp2f(s1 - m_new);
+            sS[warp][lane] = p0;
+            sS[warp][lane + 32] = p1;
+            l_run = l_run * alpha + warp_sum(p0 + p1);
+            m_run = m_new;
+            if (lane == 0) sAlpha[warp] = alpha;
+        }
+        __syncthreads();
+        // O += P V
+#pragma unroll
+        for (int j = 0; j < OUT_PER_T; ++j) {
+            const int idx = j * 128 + tid;
+            const int g = idx / HD, d = idx % HD;
+            float v = acc[j] * sAlpha[g];
+            const float* p = sS[g];
+#pragma unroll 8
+            for (int k = 0; k < kDecKeys; ++k) v += p[k] * bf2f(sV[buf][k * LD + d]);
+            acc[j] = v;
+        }
+        __syncthreads();
+    }
+    // partials: [row][hk][split][G][HD] and (m, l)
+    const int64_t pidx = (static_cast<int64_t>(row) * a.Hkv + hk) * a.max_splits + blockIdx.x;
+    float* po = a.part_o + pidx * G * HD;
+#pragma unroll
+    for (int j = 0; j < OUT_PER_T; ++j) po[j * 128 + tid] = acc[j];
+    if (warp < G && lane == 0) {
+        a.part_ml[(pidx * G + warp) * 2 + 0] = m_run;
+        a.part_ml[(pidx * G + warp) * 2 + 1] = l_run;
+    }
+}
+
+template <int HD>
+__global__ void attn_decode_combine_kernel(DecodeAttnArgs a, __nv_bfloat16* __restrict__ out, int G) {
+    const int row = blockIdx.y;
+    if (row >= a.meta->n) return;
+    const int h = blockIdx.x;
+    const int hk = h / G, g = h % G;
+    const int ctx = a.meta->pos[row] + 1;
+    const int splits = cdiv(ctx, a.chunk);
+    const int64_t base = (static_cast<int64_t>(row) * a.Hkv + hk) * a.max_splits;
+    float m = -INFINITY;
+    for (int s = 0; s < splits; ++s) m = fmaxf(m, a.part_ml[((base + s) * G + g) * 2]);
+    float l = 0.f;
+    for (int s = 0; s < splits; ++s) l += a.part_ml[((base + s) * G + g) * 2 + 1] * exp2f(a.part_ml[((base + s) * G + g) * 2] - m);
+    const float inv = 1.f / l;
+    for (int d = threadIdx.x; d < HD; d += blockDim.x) {
+        float v = 0.f;
+        for (int s = 0; s < splits; ++s)
+            v += a.part_o[((base + s) * G + g) * HD + d] * exp2f(a.part_ml[((base + s) * G + g) * 2] - m);
+        out[static_cast<int64_t>(row) * a.H * HD + h * HD + d] = __float2bfloat16_rn(v * inv);
+    }
+}
+
+template <int HD, int G>
+void decode_launch(const __nv_bfloat16* q, const __nv_bfloat16* kv_layer, __nv_bfloat16* out, const DecodeAttnArgs& a,
+                   int max_rows, cudaStream_t st) {
+    dim3 grid(a.max_splits, a.Hkv, max_rows);
+    constexpr int smem = 4 * kDecKeys * (HD + kPad) * 2 + (G * HD + G * kDecKeys + G) * 4;
+    static bool cfg = false;
+    if (!cfg) {
+        SW_CUDA(cudaFuncSetAttribute(attn_decode_kernel<HD, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        cfg = true;
+    }
+    attn_decode_kernel<HD, G><<<grid, 128, smem, st>>>(q, kv_layer, a);
+    SW_LAUNCH_CHECK();
+    attn_decode_combine_kernel<HD><<<dim3(a.H, max_rows), HD, 0, st>>>(a, out, G);
+    SW_LAUNCH_CHECK();
+}
+
+}  // namespace
+
+void attn_prefill(const __nv_bfloat16* q, const __nv_bfloat16* kv_layer, __nv_bfloat16* out, const PrefillAttnArgs& a,
+                  int max_tiles, int hd, cudaStream_t st) {
+    dim3 grid(max_tiles, a.H);
+    if (hd == 64) {
+        const int smem = (kQRows + 4 * kKeys) * 64 * 2;
+        static bool cfg = false;
+        if (!cfg) {
+            SW_CUDA(cudaFuncSetAttribute(attn_prefill_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+            cfg = true;
+        }
+        attn_prefill_kernel<64><<<grid, 128, smem, st>>>(q, kv_layer, out, a);
+    } else if (hd == 128) {
+        const int smem = (kQRows + 4 * kKeys) * 128 * 2;
+        static bool cfg = false;
+        if (!cfg) {
+            SW_CUDA(cudaFuncSetAttribute(attn_prefill_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+            cfg = true;
+        }
+        attn_prefill_kernel<128><<<grid, 128, smem, st>>>(q, kv_layer, out, a);
+    } else {
+        throw_cuda("attn_prefill: head_dim must be 64 or 128", cudaErrorInvalidValue, __FILE__, __LINE__);
+    }
+    SW_LAUNCH_CHECK();
+}
+
+void attn_decode(const __nv_bfloat16* q, const __nv_bfloat16* kv_layer, __nv_bfloat16* out, const DecodeAttnArgs& a,
+                 int max_rows, int hd, cudaStream_t st) {
+    const int G = a.H / a.Hkv;
+    if (hd == 64 && G == 4) decode_launch<64, 4>(q, kv_layer, out, a, max_rows, st);
+    else if (hd == 64 && G == 2) decode_launch<64, 2>(q, kv_layer, out, a, max_rows, st);
+    else if (hd == 128 && G == 4) decode_launch<128, 4>(q, kv_layer, out, a, max_rows, st);
+    else throw_cuda("attn_decode: unsupported (head_dim, group)", cudaErrorInvalidValue, __FILE__, __LINE__);
+}
+
+}  // namespace sw

@@ -1,0 +1,48 @@
+// Host-facing interface of the attention kernels (attention.cu).
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "elementwise.cuh"
+
+namespace sw {
+
+// Prefill: 64-row query tiles over a varlen batch (host-built tile list).
+struct PrefillAttnArgs {
+    const int* n_tiles;        // device
+    const int32_t* tile_seq;   // device [tiles]
+    const int32_t* tile_q0;    // device [tiles]
+    const int32_t* cu_seqlens; // device [seqs + 1]
+    const int32_t* seq_slot;   // device [seqs]
+    const int32_t* page_table; // device [slots][max_pages]
+    int max_pages;
+    int page_tokens;
+    int64_t page_stride;  // elements per page (one layer)
+    int64_t kv_stride;    // elements from K to V inside a page
+    int H, Hkv;
+    float scale_log2;     // log2(e) / sqrt(head_dim)
+};
+
+struct DecodeAttnArgs {
+    const StepMeta* meta;
+    const int32_t* page_table;
+    int max_pages;
+    int page_tokens;
+    int64_t page_stride;
+    int64_t kv_stride;
+    int H, Hkv;
+    float scale_log2;
+    int chunk;       // keys per split
+    int max_splits;  // grid x; splits past the context exit
+    float* part_o;   // [rows][Hkv][max_splits][G][hd]
+    float* part_ml;  // [rows][Hkv][max_splits][G][2]
+};
+
+void attn_prefill(const __nv_bfloat16* q, const __nv_bfloat16* kv_layer, __nv_bfloat16* out, const PrefillAttnArgs& a,
+                  int max_tiles, int hd, cudaStream_t st);
+void attn_decode(const __nv_bfloat16* q, const __nv_bfloat16* kv_layer, __nv_bfloat16* out, const DecodeAttnArgs& a,
+                 int max_rows, int hd, cudaStream_t st);
+
+}  // namespace sw

@@ -1,0 +1,225 @@
+// HBM-bound helper kernels of both phases: synthetic weight init, embedding
+// gather (+ page-table install for decode), RMSNorm, RoPE + paged-KV scatter,
+// and the greedy-token finalize that follows the LM-head argmax GEMM.
+#include "common.cuh"
+#include "elementwise.cuh"
+
+namespace sw {
+
+// ---------------------------------------------------------------- weights
+// dst row for logical row r: (r / blk) * blk_stride + blk_off + r % blk.
+__global__ void init_tensor_kernel(__nv_bfloat16* __restrict__ dst, int64_t rows, int cols, uint64_t tseed,
+                                   double scale, int blk, int blk_stride, int blk_off) {
+    const int64_t n = rows * cols;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t z = smx_mix(tseed + static_cast<uint64_t>(i + 1) * 0x9e3779b97f4a7c15ULL);
+        const double u = static_cast<double>(z >> 11) * 0x1.0p-53;
+        const float w = __double2float_rn((2.0 * u - 1.0) * scale);
+        const int64_t r = i / cols, c = i % cols;
+        const int64_t dr = (r / blk) * blk_stride + blk_off + r % blk;
+        dst[dr * cols + c] = __float2bfloat16_rn(w);
+    }
+}
+
+void init_tensor(__nv_bfloat16* dst, int64_t rows, int cols, uint64_t seed, int k, int fan_in, int blk,
+                 int blk_stride, int blk_off, cudaStream_t st) {
+    const uint64_t tseed = seed ^ (static_cast<uint64_t>(k) * 0x9e3779b97f4a7c15ULL);
+    const double scale = sqrt(3.0 / static_cast<double>(fan_in));
+    init_tensor_kernel<<<148 * 16, 256, 0, st>>>(dst, rows, cols, tseed, scale, blk <= 0 ? (int)rows : blk,
+                                                 blk <= 0 ? (int)rows : blk_stride, blk_off);
+    SW_LAUNCH_CHECK();
+}
+
+__global__ void fill_bf16_kernel(__nv_bfloat16* dst, int64_t n, float v) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = __float2bfloat16_rn(v);
+}
+void fill_bf16(__nv_bfloat16* dst, int64_t n, float v, cudaStream_t st) {
+    fill_bf16_kernel<<<148, 256, 0, st>>>(dst, n, v);
+    SW_LAUNCH_CHECK();
+}
+
+// FNV-style order-dependent checksum of a bf16 buffer (weight parity tests).
+__global__ void checksum_kernel(const uint16_t* __restrict__ p, int64_t n, unsigned long long* out) {
+    unsigned long long acc = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        acc += smx_mix(static_cast<uint64_t>(p[i]) ^ (static_cast<uint64_t>(i) << 16));
+    atomicAdd(out, acc);
+}
+void checksum_bf16(const void* p, int64_t n, unsigned long long* out_dev, cudaStream_t st) {
+    checksum_kernel<<<148 * 4, 256, 0, st>>>(static_cast<const uint16_t*>(p), n, out_dev);
+    SW_LAUNCH_CHECK();
+}
+
+// ---------------------------------------------------------------- embedding
+// One CTA per row: x[row] = fp32(emb[token]).  Decode rows take the token from
+// the slot's device-resident last generated token (no host round trip) unless
+// explicit tokens are given, and install the step's new page first.
+__global__ void embed_kernel(const StepMeta* __restrict__ meta, const __nv_bfloat16* __restrict__ emb,
+                             float* __restrict__ x, int d, const int32_t* __restrict__ last_token,
+                             int32_t* __restrict__ page_table, int max_pages, int page_tokens) {
+    const int row = blockIdx.x;
+    const int n_rows = meta->n;
+    if (row >= n_rows) return;
+    const int slot = meta->slot[row];
+    int tok = meta->token[row];
+    if (tok < 0) tok = last_token[slot];
+    if (threadIdx.x == 0 && meta->new_page[row] >= 0)
+        page_table[static_cast<int64_t>(slot) * max_pages + meta->pos[row] / page_tokens] = meta->new_page[row];
+    const uint4* src = reinterpret_cast<const uint4*>(emb + static_cast<int64_t>(tok) * d);
+    float4* dst = reinterpret_cast<float4*>(x + static_cast<int64_t>(row) * d);
+    for (int i = threadIdx.x; i < d / 8; i += blockDim.x) {
+        const uint4 v = src[i];
+        dst[2 * i] = make_float4(bf_lo(v.x), bf_hi(v.x), bf_lo(v.y), bf_hi(v.y));
+        dst[2 * i + 1] = make_float4(bf_lo(v.z), bf_hi(v.z), bf_lo(v.w), bf_hi(v.w));
+    }
+}
+
+void embed(const StepMeta* meta, int max_rows, const __nv_bfloat16* emb, float* x, int d, const int32_t* last_token,
+           int32_t* page_table, int max_pages, int page_tokens, cudaStream_t st) {
+    embed_kernel<<<max_rows, 128, 0, st>>>(meta, emb, x, d, last_token, page_table, max_pages, page_tokens);
+    SW_LAUNCH_CHECK();
+}
+
+// Prefill: token ids come staged per token.
+__global__ void embed_tokens_kernel(const int32_t* __restrict__ tokens, const int* __restrict__ n_tokens,
+                                    const __nv_bfloat16* __restrict__ emb, float* __restrict__ x, int d) {
+    const int row = blockIdx.x;
+    if (row >= *n_tokens) return;
+    const int tok = tokens[row];
+    const uint4* src = reinterpret_cast<const uint4*>(emb + static_cast<int64_t>(tok) * d);
+    float4* dst = reinterpret_cast<float4*>(x + static_cast<int64_t>(row) * d);
+    for (int i = threadIdx.x; i < d / 8; i += blockDim.x) {
+        const uint4 v = src[i];
+        dst[2 * i] = make_float4(bf_lo(v.x), bf_hi(v.x), bf_lo(v.y), bf_hi(v.y));
+        dst[2 * i + 1] = make_float4(bf_lo(v.z), bf_hi(v.z), bf_lo(v.w), bf_hi(v.w));
+    }
+}
+void embed_tokens(const int32_t* tokens, const int* n_tokens_dev, int rows, const __nv_bfloat16* emb, float* x, int d,
+                  cudaStream_t st) {
+    embed_tokens_kernel<<<rows, 128, 0, st>>>(tokens, n_tokens_dev, emb, x, d);
+    SW_LAUNCH_CHECK();
+}
+
+// ---------------------------------------------------------------- RMSNorm
+// One warp per row; fp32 statistics, bf16 output feeding the next GEMM.
+// `rows_dev` (optional) bounds the live rows at run time (graph-safe);
+// `row_index` (optional) gathers rows (LM head on the last prompt position).
+__global__ void rmsnorm_kernel(const float* __restrict__ x, const __nv_bfloat16* __restrict__ g,
+                               __nv_bfloat16* __restrict__ y, int rows, int d, float eps, const int* rows_dev,
+                               const int32_t* __restrict__ row_index) {
+    const int warps = blockDim.x >> 5;
+    const int row = blockIdx.x * warps + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    const int live = rows_dev ? *rows_dev : rows;
+    if (row >= rows || row >= live) return;
+    const int src_row = row_index ? row_index[row] : row;
+    const float4* xr = reinterpret_cast<const float4*>(x + static_cast<int64_t>(src_row) * d);
+    float ss = 0.f;
+    for (int i = lane; i < d / 4; i += 32) {
+        const float4 v = xr[i];
+        ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+    }
+    ss = warp_sum(ss);
+    const float inv = rsqrtf(ss / static_cast<float>(d) + eps);
+    const uint2* g2 = reinterpret_cast<const uint2*>(g);
+    uint2* y2 = reinterpret_cast<uint2*>(y + static_cast<int64_t>(row) * d);
+    for (int i = lane; i < d / 4; i += 32) {
+        const float4 v = xr[i];
+        const uint2 gg = g2[i];
+        uint2 o;
+        o.x = pack_bf2(v.x * inv * bf_lo(gg.x), v.y * inv * bf_hi(gg.x));
+        o.y = pack_bf2(v.z * inv * bf_lo(gg.y), v.w * inv * bf_hi(gg.y));
+        y2[i] = o;
+    }
+}
+
+void rmsnorm(const float* x, const __nv_bfloat16* g, __nv_bfloat16* y, int rows, int d, float eps, const int* rows_dev,
+             const int32_t* row_index, cudaStream_t st) {
+    rmsnorm_kernel<<<cdiv(rows, 8), 256, 0, st>>>(x, g, y, rows, d, eps, rows_dev, row_index);
+    SW_LAUNCH_CHECK();
+}
+
+// ---------------------------------------------------------------- RoPE + KV
+// qkv [T, (H + 2 Hkv) * hd] (GEMM output) -> q [T, H*hd] roped, and K (roped)
+// / V scattered into the paged cache of layer `layer`:
+//   pages[layer][page][kv][head][page_tokens][hd],  page = table[slot][pos / B].
+__global__ void rope_kv_kernel(const __nv_bfloat16* __restrict__ qkv, __nv_bfloat16* __restrict__ q_out,
+                               __nv_bfloat16* __restrict__ kv_layer, const int32_t* __restrict__ tok_pos,
+                               const int32_t* __restrict__ tok_slot, const int32_t* __restrict__ page_table,
+                               const float* __restrict__ inv_freq, int rows, const int* rows_dev, int H, int Hkv,
+                               int hd, int max_pages, int page_tokens, int64_t page_stride) {
+    const int t = blockIdx.x;
+    const int live = rows_dev ? *rows_dev : rows;
+    if (t >= live) return;
+    const int half = hd / 2;
+    const int pos = tok_pos[t];
+    const int slot = tok_slot[t];
+    const int page = page_table[static_cast<int64_t>(slot) * max_pages + pos / page_tokens];
+    const int off = pos % page_tokens;
+    const int width = (H + 2 * Hkv) * hd;
+    const __nv_bfloat16* src = qkv + static_cast<int64_t>(t) * width;
+    __nv_bfloat16* kbase = kv_layer + static_cast<int64_t>(page) * page_stride;
+    const int64_t head_stride = static_cast<int64_t>(page_tokens) * hd;
+    const int64_t kv_stride = static_cast<int64_t>(Hkv) * head_stride;
+    // (head, i) pairs over q and k heads: rotate; v heads: copy.
+    for (int idx = threadIdx.x; idx < (H + Hkv) * half; idx += blockDim.x) {
+        const int h = idx / half, i = idx % half;
+        float s, c;
+        sincosf(static_cast<float>(pos) * inv_freq[i], &s, &c);
+        const float a = bf2f(src[h * hd + i]), b = bf2f(src[h * hd + i + half]);
+        const __nv_bfloat16 ra = __float2bfloat16_rn(a * c - b * s);
+        const __nv_bfloat16 rb = __float2bfloat16_rn(b * c + a * s);
+        if (h < H) {
+            __nv_bfloat16* qd = q_out + static_cast<int64_t>(t) * H * hd + h * hd;
+            qd[i] = ra;
+            qd[i + half] = rb;
+        } else {
+            __nv_bfloat16* kd = kbase + (h - H) * head_stride + off * hd;
+            kd[i] = ra;
+            kd[i + half] = rb;
+        }
+    }
+    for (int idx = threadIdx.x; idx < Hkv * hd; idx += blockDim.x) {
+        const int h = idx / hd, i = idx % hd;
+        kbase[kv_stride + h * head_stride + off * hd + i] = src[(H + Hkv + h) * hd + i];
+    }
+}
+
+void rope_kv(const __nv_bfloat16* qkv, __nv_bfloat16* q_out, __nv_bfloat16* kv_layer, const int32_t* tok_pos,
+             const int32_t* tok_slot, const int32_t* page_table, const float* inv_freq, int rows, const int* rows_dev,
+             int H, int Hkv, int hd, int max_pages, int page_tokens, cudaStream_t st) {
+    const int64_t page_stride = 2LL * Hkv * page_tokens * hd;
+    rope_kv_kernel<<<rows, 256, 0, st>>>(qkv, q_out, kv_layer, tok_pos, tok_slot, page_table, inv_freq, rows,
+                                         rows_dev, H, Hkv, hd, max_pages, page_tokens, page_stride);
+    SW_LAUNCH_CHECK();
+}
+
+// ---------------------------------------------------------------- tokens
+// Decode the packed argmax keys of `rows` rows into the slots' last token and
+// output buffer, then reset the keys for the next launch.
+__global__ void finalize_tokens_kernel(unsigned long long* __restrict__ keys, const int32_t* __restrict__ slot,
+                                       const int32_t* __restrict__ out_index, int rows, const int* rows_dev,
+                                       int32_t* __restrict__ last_token, int32_t* __restrict__ out_tokens,
+                                       int max_out) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    const int live = rows_dev ? *rows_dev : rows;
+    if (r >= rows) return;
+    if (r < live) {
+        const int tok = static_cast<int>(argmax_index(keys[r]));
+        const int s = slot[r];
+        last_token[s] = tok;
+        const int oi = out_index[r];
+        if (oi >= 0 && oi < max_out) out_tokens[static_cast<int64_t>(s) * max_out + oi] = tok;
+    }
+    keys[r] = 0ull;
+}
+
+void finalize_tokens(unsigned long long* keys, const int32_t* slot, const int32_t* out_index, int rows,
+                     const int* rows_dev, int32_t* last_token, int32_t* out_tokens, int max_out, cudaStream_t st) {
+    finalize_tokens_kernel<<<cdiv(rows, 128), 128, 0, st>>>(keys, slot, out_index, rows, rows_dev, last_token,
+                                                             out_tokens, max_out);
+    SW_LAUNCH_CHECK();
+}
+
+}  // namespace sw

@@ -1,0 +1,384 @@
+// tcgen05/TMEM GEMM for sm_100a with fused epilogues -- the tensor-core core
+// of both phases.
+//
+//   Y[t, f] = sum_k X[t, k] * W[f, k]      X: activations bf16 [T, K]
+//                                          W: weights     bf16 [F, K]
+// Prefill ("normal"):  A = X (UMMA M = 128 tokens), B = W (UMMA N = BN features)
+// Decode  ("swap-AB"): A = W (UMMA M = 128 features), B = X (UMMA N = BN >= b
+//                      tokens, TMA pads).  The weight stream is the A operand,
+//                      so a batch of b <= 256 rows costs one pass over W.
+//
+// One CTA = one 128 x BN output tile, 6 warps:
+//   warp 0  TMA producer (one lane): A/B K-blocks of 64 into a STAGES-deep
+//           ring of 128B-swizzled smem, completion by mbarrier tx-count;
+//   warp 1  TMEM allocator + MMA issuer (one lane): 4 x tcgen05.mma
+//           (128 x BN x 16) per K-block, tcgen05.commit frees the ring slot;
+//   warps 2-5 epilogue: tcgen05.ld 32x32b.x32 (warp%4 picks its 32 TMEM
+//           lanes) -> registers -> fused epilogue -> global.
+// Epilogues: STORE (bf16), RESID (fp32 residual +=), SWIGLU over
+// [gate 64 | up 64] feature blocks (bf16 out, half width), ARGMAX (packed
+// 64-bit atomicMax per token: LM head + greedy sampling in one pass).
+#include <cuda.h>
+
+#include <map>
+#include <mutex>
+#include <tuple>
+
+#include "common.cuh"
+#include "gemm_sm100.cuh"
+
+namespace sw {
+
+namespace {
+
+constexpr int BM = 128;
+constexpr int BK = 64;
+constexpr int kThreads = 192;
+
+template <int BN>
+struct GemmCfg {
+    static constexpr int kABytes = BM * BK * 2;
+    static constexpr int kBBytes = BN * BK * 2;
+    static constexpr int kStageBytes = kABytes + kBBytes;
+    static constexpr int kStages = (200 * 1024) / kStageBytes > 8 ? 8 : (200 * 1024) / kStageBytes;
+    static constexpr int kTmemCols = BN < 32 ? 32 : BN;
+    static constexpr int kXchgBytes = 64 * 33 * 4;  // SwiGLU swap-mode exchange
+    static constexpr int kSmem = 1024 + kStages * kStageBytes + kXchgBytes + 256;
+};
+
+__device__ __forceinline__ float silu_mul(float g, float u) { return g / (1.0f + __expf(-g)) * u; }
+
+template <int BN, int MODE, bool SWAP>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmArgs args) {
+    using C = GemmCfg<BN>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sA = smem;
+    uint8_t* sB = smem + C::kStages * C::kABytes;
+    float* xchg = reinterpret_cast<float*>(sB + C::kStages * C::kBBytes);
+    uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(xchg) + C::kXchgBytes);
+    uint64_t* empty = full + C::kStages;
+    uint64_t* acc_ready = empty + C::kStages;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_ready + 1);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const int m0 = blockIdx.y * BM;
+    const int n0 = blockIdx.x * BN;
+    const int nk = args.K / BK;
+
+    if (warp == 0 && lane == 0) {
+        for (int s = 0; s < C::kStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        mbar_init(acc_ready, 1);
+        fence_mbar_init();
+    }
+    if (warp == 1) {
+        tmem_alloc(tmem_slot, C::kTmemCols);
+        tmem_relinquish();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            tma_prefetch_desc(&tmA);
+            tma_prefetch_desc(&tmB);
+            // Weights are streamed once per launch (evict-first); activations
+            // are re-read by every feature tile (evict-last).
+            const uint64_t pol_w = l2_policy_evict_first();
+            const uint64_t pol_x = l2_policy_evict_last();
+            const uint64_t pol_a = SWAP ? pol_w : pol_x;
+            const uint64_t pol_b = SWAP ? pol_x : pol_w;
+            for (int kb = 0; kb < nk; ++kb) {
+                const int s = kb % C::kStages;
+                const uint32_t ph = (kb / C::kStages) & 1;
+                mbar_wait(&empty[s], ph ^ 1);
+                mbar_expect_tx(&full[s], C::kStageBytes);
+                tma_load_2d(sA + s * C::kABytes, &tmA, &full[s], kb * BK, m0, pol_a);
+                tma_load_2d(sB + s * C::kBBytes, &tmB, &full[s], kb * BK, n0, pol_b);
+            }
+        }
+        __syncwarp();
+    } else if (warp == 1) {
+        if (lane == 0) {
+            constexpr uint32_t idesc = umma_idesc_bf16(BM, BN);
+            for (int kb = 0; kb < nk; ++kb) {
+                const int s = kb % C::kStages;
+                const uint32_t ph = (kb / C::kStages) & 1;
+                mbar_wait(&full[s], ph);
+                tc_fence_after();
+                const uint32_t a0 = smem_addr(sA + s * C::kABytes);
+                const uint32_t b0 = smem_addr(sB + s * C::kBBytes);
+#pragma unroll
+                for (int k = 0; k < BK / 16; ++k)
+                    umma_bf16(tmem, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32), idesc,
+                              (kb | k) != 0);
+                umma_commit(&empty[s]);
+            }
+            umma_commit(acc_ready);
+        }
+        __syncwarp();
+    } else {
+        // ------------------------------------------------------------ epilogue
+        const int quarter = warp & 3;  // TMEM lanes [32*quarter, 32*quarter+32)
+        const int row = quarter * 32 + lane;  // accumulator row inside the tile
+        mbar_wait(acc_ready, 0);
+        tc_fence_after();
+        const uint32_t tbase = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
+        uint32_t r[32];
+        const int n_live = args.live_tokens ? min(args.valid_tokens, *args.live_tokens) : args.valid_tokens;
+        if constexpr (!SWAP) {
+            // row = token, columns = features
+            const int t = m0 + row;
+            const bool live = t < n_live;
+            if constexpr (MODE == EPI_SWIGLU) {
+                for (int blk = 0; blk < BN / 128; ++blk) {
+#pragma unroll
+                    for (int half = 0; half < 64; half += 32) {
+                        uint32_t u[32];
+                        tmem_ld32(tbase + blk * 128 + half, r);
+                        tmem_ld32(tbase + blk * 128 + 64 + half, u);
+                        tmem_ld_wait();
+                        if (live) {
+                            __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(args.out) +
+                                                 static_cast<size_t>(t) * args.ldo + (n0 + blk * 128) / 2 + half;
+                            uint4* d4 = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+                            for (int q = 0; q < 4; ++q) {
+                                uint4 v;
+                                v.x = pack_bf2(silu_mul(__uint_as_float(r[8 * q + 0]), __uint_as_float(u[8 * q + 0])),
+                                               silu_mul(__uint_as_float(r[8 * q + 1]), __uint_as_float(u[8 * q + 1])));
+                                v.y = pack_bf2(silu_mul(__uint_as_float(r[8 * q + 2]), __uint_as_float(u[8 * q + 2])),
+                                               silu_mul(__uint_as_float(r[8 * q + 3]), __uint_as_float(u[8 * q + 3])));
+                                v.z = pack_bf2(silu_mul(__uint_as_float(r[8 * q + 4]), __uint_as_float(u[8 * q + 4])),
+                                               silu_mul(__uint_as_float(r[8 * q + 5]), __uint_as_float(u[8 * q + 5])));
+                                v.w = pack_bf2(silu_mul(__uint_as_float(r[8 * q + 6]), __uint_as_float(u[8 * q + 6])),
+                                               silu_mul(__uint_as_float(r[8 * q + 7]), __uint_as_float(u[8 * q + 7])));
+                                d4[q] = v;
+                            }
+                        }
+                    }
+                }
+            } else {
+                for (int c = 0; c < BN; c += 32) {
+                    tmem_ld32(tbase + c, r);
+                    tmem_ld_wait();
+                    if (!live) continue;
+                    if constexpr (MODE == EPI_STORE) {
+                        uint4* d4 = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(args.out) +
+                                                             static_cast<size_t>(t) * args.ldo + n0 + c);
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            uint4 v;
+                            v.x = pack_bf2(__uint_as_float(r[8 * q + 0]), __uint_as_float(r[8 * q + 1]));
+                            v.y = pack_bf2(__uint_as_float(r[8 * q + 2]), __uint_as_float(r[8 * q + 3]));
+                            v.z = pack_bf2(__uint_as_float(r[8 * q + 4]), __uint_as_float(r[8 * q + 5]));
+                            v.w = pack_bf2(__uint_as_float(r[8 * q + 6]), __uint_as_float(r[8 * q + 7]));
+                            d4[q] = v;
+                        }
+                    } else if constexpr (MODE == EPI_STORE_F32) {
+                        float4* d4 = reinterpret_cast<float4*>(static_cast<float*>(args.out) +
+                                                               static_cast<size_t>(t) * args.ldo + n0 + c);
+#pragma unroll
+                        for (int q = 0; q < 8; ++q)
+                            d4[q] = make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
+                                                __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]));
+                    } else if constexpr (MODE == EPI_RESID) {
+                        float4* d4 = reinterpret_cast<float4*>(static_cast<float*>(args.out) +
+                                                               static_cast<size_t>(t) * args.ldo + n0 + c);
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) {
+                            float4 v = d4[q];
+                            v.x += __uint_as_float(r[4 * q + 0]);
+                            v.y += __uint_as_float(r[4 * q + 1]);
+                            v.z += __uint_as_float(r[4 * q + 2]);
+                            v.w += __uint_as_float(r[4 * q + 3]);
+                            d4[q] = v;
+                        }
+                    }
+                }
+            }
+        } else {
+            // row = feature (weight row), columns = tokens
+            const int f = m0 + row;
+            for (int c = 0; c < BN; c += 32) {
+                tmem_ld32(tbase + c, r);
+                tmem_ld_wait();
+                const int tcount = min(32, n_live - (n0 + c));
+                if constexpr (MODE == EPI_STORE) {
+                    _Pragma("unroll") for (int j = 0; j < 32; ++j) if (j < tcount)
+                        static_cast<__nv_bfloat16*>(args.out)[static_cast<size_t>(n0 + c + j) * args.ldo + f] =
+                            __float2bfloat16_rn(__uint_as_float(r[j]));
+                } else if constexpr (MODE == EPI_STORE_F32) {
+                    _Pragma("unroll") for (int j = 0; j < 32; ++j) if (j < tcount)
+                        static_cast<float*>(args.out)[static_cast<size_t>(n0 + c + j) * args.ldo + f] =
+                            __uint_as_float(r[j]);
+                } else if constexpr (MODE == EPI_RESID) {
+                    _Pragma("unroll") for (int j = 0; j < 32; ++j) if (j < tcount)
+                        static_cast<float*>(args.out)[static_cast<size_t>(n0 + c + j) * args.ldo + f] +=
+                            __uint_as_float(r[j]);
+                } else if constexpr (MODE == EPI_SWIGLU) {
+                    // lanes 0-63 of the tile hold gate rows, 64-127 the matching up rows
+                    const int ew = threadIdx.x - 64;  // 0..127 over the epilogue warps
+                    (void)ew;
+                    if (row >= 64) {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) xchg[(row - 64) * 33 + j] = __uint_as_float(r[j]);
+                    }
+                    asm volatile("bar.sync 1, 128;" ::: "memory");
+                    if (row < 64) {
+                        const int g = m0 / 2 + row;
+                        _Pragma("unroll") for (int j = 0; j < 32; ++j) if (j < tcount)
+                            static_cast<__nv_bfloat16*>(args.out)[static_cast<size_t>(n0 + c + j) * args.ldo + g] =
+                                __float2bfloat16_rn(silu_mul(__uint_as_float(r[j]), xchg[row * 33 + j]));
+                    }
+                    asm volatile("bar.sync 1, 128;" ::: "memory");
+                } else if constexpr (MODE == EPI_ARGMAX) {
+                    _Pragma("unroll") for (int j = 0; j < 32; ++j) if (j < tcount) {
+                        unsigned long long key = argmax_key(__uint_as_float(r[j]),
+                                                            static_cast<uint32_t>(args.feature_offset + f));
+#pragma unroll
+                        for (int o = 16; o > 0; o >>= 1) {
+                            const unsigned long long other = __shfl_xor_sync(0xffffffffu, key, o);
+                            key = other > key ? other : key;
+                        }
+                        if (lane == 0) atomicMax(args.argmax + n0 + c + j, key);
+                    }
+                }
+            }
+        }
+        tc_fence_before();
+    }
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc(tmem, C::kTmemCols);
+    }
+}
+
+// ---------------------------------------------------------------- host side
+using EncodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                 const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                 CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiled encode_fn() {
+    static EncodeTiled fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        SW_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+        if (q != cudaDriverEntryPointSuccess || !p) throw_cuda("cuTensorMapEncodeTiled lookup", cudaErrorUnknown, __FILE__, __LINE__);
+        return reinterpret_cast<EncodeTiled>(p);
+    }();
+    return fn;
+}
+
+template <int BN, int MODE, bool SWAP>
+void launch_one(const CUtensorMap& a, const CUtensorMap& b, const GemmArgs& args, cudaStream_t st) {
+    using C = GemmCfg<BN>;
+    static bool configured = false;  // per instantiation
+    if (!configured) {
+        SW_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<BN, MODE, SWAP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     C::kSmem));
+        configured = true;
+    }
+    dim3 grid(args.N / BN, cdiv(args.M, BM));
+    gemm_tc_kernel<BN, MODE, SWAP><<<grid, kThreads, C::kSmem, st>>>(a, b, args);
+    SW_LAUNCH_CHECK();
+}
+
+template <bool SWAP, int MODE>
+void dispatch_bn(int bn, const CUtensorMap& a, const CUtensorMap& b, const GemmArgs& args, cudaStream_t st) {
+    switch (bn) {
+        case 32: launch_one<32, MODE, SWAP>(a, b, args, st); break;
+        case 64: launch_one<64, MODE, SWAP>(a, b, args, st); break;
+        case 128: launch_one<128, MODE, SWAP>(a, b, args, st); break;
+        case 256: launch_one<256, MODE, SWAP>(a, b, args, st); break;
+        default: throw_cuda("gemm: unsupported BN", cudaErrorInvalidValue, __FILE__, __LINE__);
+    }
+}
+
+}  // namespace
+
+CUtensorMap make_tmap_bf16(const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+    CUtensorMap m;
+    const cuuint64_t dims[2] = {cols, rows};
+    const cuuint64_t strides[1] = {cols * 2};
+    const cuuint32_t box[2] = {BK, box_rows};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
+                                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw_cuda("cuTensorMapEncodeTiled", cudaErrorInvalidValue, __FILE__, __LINE__);
+    return m;
+}
+
+const CUtensorMap& tmap_cached(const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+    static std::mutex mu;
+    static std::map<std::tuple<const void*, uint64_t, uint64_t, uint32_t>, CUtensorMap> cache;
+    std::lock_guard<std::mutex> lk(mu);
+    const auto key = std::make_tuple(base, rows, cols, box_rows);
+    auto it = cache.find(key);
+    if (it == cache.end()) it = cache.emplace(key, make_tmap_bf16(base, rows, cols, box_rows)).first;
+    return it->second;
+}
+
+int gemm_pick_bn_swap(int tokens) {
+    if (tokens <= 32) return 32;
+    if (tokens <= 64) return 64;
+    if (tokens <= 128) return 128;
+    return 256;
+}
+
+void gemm_run(const GemmProblem& p, cudaStream_t st) {
+    if (p.K % BK != 0) throw_cuda("gemm: K must be a multiple of 64", cudaErrorInvalidValue, __FILE__, __LINE__);
+    GemmArgs a{};
+    a.K = p.K;
+    a.mode = p.mode;
+    a.out = p.out;
+    a.ldo = p.ldo;
+    a.argmax = p.argmax;
+    a.feature_offset = p.feature_offset;
+    a.valid_tokens = p.tokens;
+    a.live_tokens = p.live_tokens;
+    if (p.swap) {
+        if (p.features % BM != 0)
+            throw_cuda("gemm(swap): feature count must be a multiple of 128", cudaErrorInvalidValue, __FILE__, __LINE__);
+        if (p.tokens > 256) throw_cuda("gemm(swap): at most 256 tokens", cudaErrorInvalidValue, __FILE__, __LINE__);
+        const int bn = gemm_pick_bn_swap(p.tokens);
+        a.M = p.features;
+        a.N = bn;
+        const CUtensorMap& ta = tmap_cached(p.W, p.w_rows, p.K, BM);
+        const CUtensorMap& tb = tmap_cached(p.X, p.x_rows, p.K, bn);
+        switch (p.mode) {
+            case EPI_STORE: dispatch_bn<true, EPI_STORE>(bn, ta, tb, a, st); break;
+            case EPI_RESID: dispatch_bn<true, EPI_RESID>(bn, ta, tb, a, st); break;
+            case EPI_SWIGLU: dispatch_bn<true, EPI_SWIGLU>(bn, ta, tb, a, st); break;
+            case EPI_ARGMAX: dispatch_bn<true, EPI_ARGMAX>(bn, ta, tb, a, st); break;
+            case EPI_STORE_F32: dispatch_bn<true, EPI_STORE_F32>(bn, ta, tb, a, st); break;
+            default: throw_cuda("gemm: bad epilogue", cudaErrorInvalidValue, __FILE__, __LINE__);
+        }
+    } else {
+        const int bn = 256;
+        if (p.features % bn != 0)
+            throw_cuda("gemm: feature count must be a multiple of 256", cudaErrorInvalidValue, __FILE__, __LINE__);
+        a.M = p.tokens;
+        a.N = p.features;
+        const CUtensorMap& ta = tmap_cached(p.X, p.x_rows, p.K, BM);
+        const CUtensorMap& tb = tmap_cached(p.W, p.w_rows, p.K, bn);
+        switch (p.mode) {
+            case EPI_STORE: dispatch_bn<false, EPI_STORE>(bn, ta, tb, a, st); break;
+            case EPI_RESID: dispatch_bn<false, EPI_RESID>(bn, ta, tb, a, st); break;
+            case EPI_SWIGLU: dispatch_bn<false, EPI_SWIGLU>(bn, ta, tb, a, st); break;
+            case EPI_STORE_F32: dispatch_bn<false, EPI_STORE_F32>(bn, ta, tb, a, st); break;
+            default: throw_cuda("gemm: bad epilogue for normal mode", cudaErrorInvalidValue, __FILE__, __LINE__);
+        }
+    }
+}
+
+}  // namespace sw

@@ -1,0 +1,99 @@
+"""End-to-end GPU runs through sw_engine_run (the run-level C-ABI).
+
+Config 1 of BASELINE.json (tiny decoder, 8 prompts x 64 tokens, 32 greedy
+steps) under serial and split-phase policies:
+  * every policy/mode yields the same tokens (batch-invariant kernels), and
+    each token agrees with the fp32 oracle (teacher forced) wherever the
+    oracle's top-2 margin exceeds the 1e-2 tolerance;
+  * the device page table equals the host allocator's rows and an
+    independent replay of the alloc/free journal (bit exact);
+  * the event log obeys the reference contract (KV ledger replay, token
+    counts, one TTFT/TBT per request).
+"""
+import numpy as np
+import pytest
+
+pytest.importorskip("torch")
+
+from oracle import model as M
+from oracle import pages as P
+
+pytestmark = pytest.mark.gpu
+
+RUNS = {
+    "sequential_serial": "policy=sequential;max_batch=8;engine.split=0",
+    "cb_serial": "policy=continuous_batching;engine.split=0",
+    "pipelined_P2_split": "policy=pipelined_splitwiser;P=2;max_batch=4;engine.split=1",
+    "pipelined_P4_split_nocoalesce": "policy=pipelined_splitwiser;P=4;max_batch=2;engine.split=1;engine.coalesce=0",
+    "mixed_split_arrivals": "policy=mixed_batching;arrival=fixed:0.003;engine.split=1",
+    "multi_instance_split": "policy=multi_instance;n_instances=2;inner=mixed_batching;engine.split=1",
+}
+
+
+@pytest.fixture(scope="module")
+def eng():
+    from paper_2505_03763_b200 import runtime
+
+    e = runtime.Engine(M.TINY, max_prefill_tokens=1024, max_decode_batch=16, n_pages=512, n_slots=16,
+                       max_pages_per_slot=8, max_out=40)
+    yield e
+    e.close()
+
+
+@pytest.fixture(scope="module")
+def results(eng):
+    out = {}
+    for name, extra in RUNS.items():
+        out[name] = eng.run(f"n=8;input=64;output=32;seed=1;kv_capacity_blocks=480;{extra}")
+    return out
+
+
+def test_all_runs_complete(results):
+    for name, r in results.items():
+        assert r.report["n_requests"] == 8, name
+        assert r.report["total_output_tokens"] == 8 * 32, name
+        assert len(r.tokens) == 8 and all(len(t) == 32 for t in r.tokens.values()), name
+
+
+def test_tokens_identical_across_policies_and_modes(results):
+    base = results["sequential_serial"].tokens
+    for name, r in results.items():
+        assert r.tokens == base, name
+
+
+def test_tokens_match_oracle_teacher_forced(results):
+    d = M.TINY
+    o = M.OracleModel(d)
+    toks = results["pipelined_P2_split"].tokens
+    bad = []
+    for rid in range(8):
+        prompt = M.prompt_tokens(d.seed, rid, 64, d.vocab)
+        row = list(range(100 * rid, 100 * rid + 8))
+        lg = o.prefill([prompt], [row])[0]
+        seq = toks[rid]
+        for g in range(32):
+            tol = 1e-2 * float(np.max(np.abs(lg)))
+            if M.top2_margin(lg) > tol and int(np.argmax(lg)) != seq[g]:
+                bad.append((rid, g))
+            if g + 1 < 32:
+                lg = o.decode([seq[g]], [64 + g], [row])[0]
+        o.release(row)
+    assert not bad, bad
+
+
+def test_page_tables_bit_exact(results):
+    from paper_2505_03763_b200.runtime import parse_devpages
+
+    for name, r in results.items():
+        dev = parse_devpages(r)
+        assert dev == r.pages, name
+        assert P.page_replay(r.journal, 480) == r.pages, name
+        # each request held blocks_for(in + out) pages at its largest extent
+        assert all(len(v) == P.blocks_for(64 + 32) for v in r.pages.values()), name
+
+
+def test_event_log_contract(results):
+    for name, r in results.items():
+        for t, inst, logged, replayed in P.ledger_replay(r.event_log):
+            assert logged == replayed, (name, t)
+        assert all(q["ttft_s"] > 0 and q["e2e_s"] >= q["ttft_s"] for q in r.requests), name

@@ -1,0 +1,110 @@
+"""Model-level parity of the CUDA path (through the C-ABI) with the CPU oracle.
+
+Bars (north star): logits within 1e-2 relative (per-row L2) of the fp32
+oracle; greedy tokens identical wherever the oracle's top-2 margin exceeds the
+tolerance; page tables bit exact.
+"""
+import numpy as np
+import pytest
+
+pytest.importorskip("torch")
+
+from oracle import model as M
+
+pytestmark = pytest.mark.gpu
+
+LOGIT_RTOL = 1e-2
+
+
+def rel_rows(a, b):
+    return np.linalg.norm(a - b, axis=-1) / np.linalg.norm(b, axis=-1)
+
+
+def margin_tol(ref_row):
+    return LOGIT_RTOL * float(np.max(np.abs(ref_row)))
+
+
+@pytest.fixture(scope="module")
+def tiny():
+    from paper_2505_03763_b200 import runtime
+
+    eng = runtime.Engine(M.TINY, max_prefill_tokens=2048, max_decode_batch=32, n_pages=1024, n_slots=64,
+                         max_pages_per_slot=16, max_out=40)
+    yield eng
+    eng.close()
+
+
+@pytest.fixture(scope="module")
+def tiny_oracle():
+    return M.OracleModel(M.TINY)
+
+
+def test_weights_bit_exact(tiny, tiny_oracle):
+    d = M.TINY
+    o = tiny_oracle
+    H, Hk, hd, F = d.n_heads, d.n_kv_heads, d.head_dim, d.ffn_dim
+    assert np.array_equal(tiny.tensor_numpy("emb").reshape(d.vocab, d.d_model), o.emb)
+    for l in range(d.n_layers):
+        W = o.layers[l]
+        qkv = tiny.tensor_numpy(f"layer{l}.wqkv").reshape(-1, d.d_model)
+        assert np.array_equal(qkv[:H * hd], W["wq"])
+        assert np.array_equal(qkv[H * hd:(H + Hk) * hd], W["wk"])
+        assert np.array_equal(qkv[(H + Hk) * hd:], W["wv"])
+        gu = tiny.tensor_numpy(f"layer{l}.wgu").reshape(2 * F, d.d_model)
+        for j in range(F // 64):
+            assert np.array_equal(gu[128 * j:128 * j + 64], W["wg"][64 * j:64 * j + 64])
+            assert np.array_equal(gu[128 * j + 64:128 * j + 128], W["wu"][64 * j:64 * j + 64])
+        assert np.array_equal(tiny.tensor_numpy(f"layer{l}.wo").reshape(d.d_model, -1), W["wo"])
+        assert np.array_equal(tiny.tensor_numpy(f"layer{l}.wd").reshape(d.d_model, F), W["wd"])
+    assert np.array_equal(tiny.tensor_numpy("lm").reshape(d.vocab, d.d_model), o.lm)
+
+
+def test_prefill_then_decode_teacher_forced(tiny, tiny_oracle):
+    d = M.TINY
+    o = tiny_oracle
+    lens = [1, 15, 16, 17, 64, 100, 129]  # page-boundary edge cases, ragged batch
+    slots = list(range(10, 10 + len(lens)))
+    prompts = [M.prompt_tokens(d.seed, 100 + i, n, d.vocab) for i, n in enumerate(lens)]
+    # disjoint page rows, deliberately non-contiguous ids
+    rows = [[(i * 37 + j * 11) % 800 for j in range(16)] for i in range(len(lens))]
+    seen = set()
+    for r in rows:
+        for p in r:
+            assert p not in seen
+            seen.add(p)
+    lg = tiny.prefill(slots, prompts, [r[:(n + 15) // 16] for r, n in zip(rows, lens)])
+    ref = o.prefill(prompts, rows)
+    assert rel_rows(lg, ref).max() < LOGIT_RTOL
+    toks = [int(np.argmax(l)) for l in ref]
+    for i, l in enumerate(ref):
+        if M.top2_margin(l) > margin_tol(l):
+            assert int(np.argmax(lg[i])) == toks[i]
+    pos = list(lens)
+    for step in range(20):
+        newp = [rows[i][pos[i] // 16] if pos[i] % 16 == 0 else -1 for i in range(len(lens))]
+        lg = tiny.decode(slots, pos, tokens=toks, new_page=newp)
+        ref = o.decode(toks, pos, rows)
+        err = rel_rows(lg, ref)
+        assert err.max() < LOGIT_RTOL, (step, err)
+        nxt = []
+        for i, l in enumerate(ref):
+            if M.top2_margin(l) > margin_tol(l):
+                assert int(np.argmax(lg[i])) == int(np.argmax(l)), (step, i)
+            nxt.append(int(np.argmax(l)))  # teacher forcing with the oracle's token
+        toks = nxt
+        pos = [p + 1 for p in pos]
+
+
+def test_decode_uses_device_resident_token(tiny, tiny_oracle):
+    """tokens=NULL feeds last_token[slot] written by the previous launch."""
+    d = M.TINY
+    prompts = [M.prompt_tokens(d.seed, 300 + i, 30 + i, d.vocab) for i in range(3)]
+    slots = [40, 41, 42]
+    rows = [[900 + 16 * i + j for j in range(4)] for i in range(3)]
+    lg = tiny.prefill(slots, prompts, [r[:2] for r in rows])
+    tiny_oracle.prefill(prompts, rows)
+    t1 = [int(np.argmax(l)) for l in lg]
+    pos = [len(p) for p in prompts]
+    lg_dev = tiny.decode(slots, pos, tokens=None, new_page=[-1] * 3)
+    ref = tiny_oracle.decode(t1, pos, rows)
+    assert rel_rows(lg_dev, ref).max() < LOGIT_RTOL
