@@ -107,14 +107,30 @@ LLAMA_8B = Desc(n_layers=32, d_model=4096, n_heads=32, n_kv_heads=8, head_dim=12
 
 
 class OracleModel:
-    """fp32 Llama-style decoder over bf16-valued weights, paged KV cache."""
+    """fp32 Llama-style decoder over bf16-valued weights, paged KV cache.
 
-    def __init__(self, desc: Desc, page_tokens: int = 16):
+    emulate_bf16=False is THE reference: everything in fp32.  emulate_bf16=True
+    additionally rounds to bf16 exactly where the CUDA path stores bf16
+    (RMSNorm outputs, roped q/k and v -- the KV cache --, the prefill softmax
+    numerators fed to the P.V tensor-core product, attention output, SwiGLU
+    output), so the remaining difference is accumulation order only.
+    """
+
+    def __init__(self, desc: Desc, page_tokens: int = 16, emulate_bf16: bool = False, share_weights_with=None):
         self.d = desc
         self.B = page_tokens
+        self.emul = emulate_bf16
+        self._phase = "prefill"
         D, H, Hk, hd, F, V, L = (desc.d_model, desc.n_heads, desc.n_kv_heads, desc.head_dim, desc.ffn_dim,
                                  desc.vocab, desc.n_layers)
         s = desc.seed
+        self.pages: Dict[int, np.ndarray] = {}
+        half = hd // 2
+        self.inv_freq = (1.0 / (desc.rope_theta ** (np.arange(half, dtype=np.float64) * 2.0 / hd))).astype(np.float32)
+        if share_weights_with is not None:  # same weights, separate KV store
+            o = share_weights_with
+            self.emb, self.layers, self.lm = o.emb, o.layers, o.lm
+            return
         self.emb = tensor_values(s, 0, V, D, D)
         self.layers = []
         for l in range(L):
@@ -129,12 +145,11 @@ class OracleModel:
                 wd=tensor_values(s, b + 6, D, F, F),
             ))
         self.lm = self.emb if desc.tied_embeddings else tensor_values(s, 1 + 7 * L, V, D, D)
-        half = hd // 2
-        self.inv_freq = (1.0 / (desc.rope_theta ** (np.arange(half, dtype=np.float64) * 2.0 / hd))).astype(np.float32)
-        # paged KV store: page id -> [L, 2, Hk, B, hd]
-        self.pages: Dict[int, np.ndarray] = {}
 
     # -- pieces
+    def _r(self, x: np.ndarray) -> np.ndarray:
+        return bf16_round(x) if self.emul else x
+
     def rmsnorm(self, x: np.ndarray) -> np.ndarray:
         ms = np.mean(x.astype(np.float32) ** 2, axis=-1, keepdims=True)
         return (x / np.sqrt(ms + np.float32(self.d.norm_eps))).astype(np.float32)
@@ -180,20 +195,22 @@ class OracleModel:
             sc = np.where(mask, -np.inf, sc)
             sc = sc - sc.max(axis=1, keepdims=True)
             p = np.exp(sc)
-            p /= p.sum(axis=1, keepdims=True)
-            out[:, h, :] = p @ vh
+            l = p.sum(axis=1, keepdims=True)
+            if self.emul and self._phase == "prefill":
+                p = bf16_round(p)
+            out[:, h, :] = (p @ vh) / l
         return out
 
     def _block(self, l: int, x: np.ndarray, rows: List[Sequence[int]], spans: List[np.ndarray]) -> np.ndarray:
         """One decoder layer over the concatenation of per-request token spans."""
         W = self.layers[l]
         H, Hk, hd = self.d.n_heads, self.d.n_kv_heads, self.d.head_dim
-        h = self.rmsnorm(x)
+        h = self._r(self.rmsnorm(x))
         q = (h @ W["wq"].T).reshape(-1, H, hd)
         k = (h @ W["wk"].T).reshape(-1, Hk, hd)
-        v = (h @ W["wv"].T).reshape(-1, Hk, hd)
+        v = self._r((h @ W["wv"].T).reshape(-1, Hk, hd))
         pos_all = np.concatenate(spans)
-        q, k = self.rope(q, pos_all), self.rope(k, pos_all)
+        q, k = self._r(self.rope(q, pos_all)), self._r(self.rope(k, pos_all))
         o = np.empty_like(q)
         off = 0
         for row, pos in zip(rows, spans):
@@ -202,10 +219,10 @@ class OracleModel:
             ks, vs = self._read_kv(l, row, int(pos[-1]) + 1)
             o[off:off + t] = self._attend(q[off:off + t], ks, vs, pos)
             off += t
-        x = x + o.reshape(len(x), -1) @ W["wo"].T
-        h = self.rmsnorm(x)
+        x = x + self._r(o.reshape(len(x), -1)) @ W["wo"].T
+        h = self._r(self.rmsnorm(x))
         gate = h @ W["wg"].T
-        a = (gate / (1.0 + np.exp(-gate))) * (h @ W["wu"].T)
+        a = self._r((gate / (1.0 + np.exp(-gate))) * (h @ W["wu"].T))
         return (x + a.astype(np.float32) @ W["wd"].T).astype(np.float32)
 
     def forward(self, tokens: np.ndarray, rows: List[Sequence[int]], spans: List[np.ndarray],
@@ -216,16 +233,18 @@ class OracleModel:
             x = self._block(l, x, rows, spans)
         if want is None:
             want = np.cumsum([len(s) for s in spans]) - 1
-        return (self.rmsnorm(x[want]) @ self.lm.T).astype(np.float32)
+        return (self._r(self.rmsnorm(x[want])) @ self.lm.T).astype(np.float32)
 
     # -- phase entry points (same semantics as sw_prefill_enqueue / sw_decode_enqueue)
     def prefill(self, prompts: List[np.ndarray], page_rows: List[Sequence[int]]) -> np.ndarray:
         toks = np.concatenate(prompts)
         spans = [np.arange(len(p)) for p in prompts]
+        self._phase = "prefill"
         return self.forward(toks, page_rows, spans)
 
     def decode(self, tokens: Sequence[int], positions: Sequence[int], page_rows: List[Sequence[int]]) -> np.ndarray:
         spans = [np.array([p]) for p in positions]
+        self._phase = "decode"
         return self.forward(np.asarray(tokens, dtype=np.int64), page_rows, spans)
 
     def release(self, page_row: Sequence[int]):

@@ -76,7 +76,7 @@ void ws_alloc(Workspace& w, const sw_model_desc& d, int rows, bool decode, int m
     w.rows = rows;
     w.x = dalloc<float>(static_cast<size_t>(rows) * d.d_model);
     w.xn = dalloc<__nv_bfloat16>(static_cast<size_t>(rows) * d.d_model);
-    w.qkv = dalloc<__nv_bfloat16>(static_cast<size_t>(rows) * qkv_w);
+    w.qkv = dalloc<float>(static_cast<size_t>(rows) * qkv_w);
     w.q = dalloc<__nv_bfloat16>(static_cast<size_t>(rows) * d.n_heads * d.head_dim);
     w.attn = dalloc<__nv_bfloat16>(static_cast<size_t>(rows) * d.n_heads * d.head_dim);
     w.act = dalloc<__nv_bfloat16>(static_cast<size_t>(rows) * d.ffn_dim);
@@ -250,7 +250,7 @@ void prefill_forward(sw_model* m, sw_kv* kv, const sw_batch& b, cudaStream_t st)
             const LayerWeights& L = m->layers[l];
             __nv_bfloat16* kvl = kv->pages + l * kv->layer_stride;
             rmsnorm(w.x, L.g_attn, w.xn, T, d.d_model, d.norm_eps, nullptr, nullptr, st);
-            gemm_run(gp(w.xn, w.rows, L.wqkv, qkv_w, T, qkv_w, d.d_model, EPI_STORE, false, w.qkv, qkv_w), st);
+            gemm_run(gp(w.xn, w.rows, L.wqkv, qkv_w, T, qkv_w, d.d_model, EPI_STORE_F32, false, w.qkv, qkv_w), st);
             rope_kv(w.qkv, w.q, kvl, dev(tpos), dev(tslot), kv->page_table, m->inv_freq, T, nullptr, d.n_heads,
                     d.n_kv_heads, d.head_dim, kv->max_pages, B, st);
             attn_prefill(w.q, kvl, w.attn, aa, n_tiles, d.head_dim, st);
@@ -297,7 +297,7 @@ void decode_layers(sw_model* m, sw_kv* kv, int R, cudaStream_t st) {
         const LayerWeights& L = m->layers[l];
         __nv_bfloat16* kvl = kv->pages + l * kv->layer_stride;
         rmsnorm(w.x, L.g_attn, w.xn, R, d.d_model, d.norm_eps, live, nullptr, st);
-        gemm_run(gp(w.xn, w.rows, L.wqkv, qkv_w, R, qkv_w, d.d_model, EPI_STORE, true, w.qkv, qkv_w, live), st);
+        gemm_run(gp(w.xn, w.rows, L.wqkv, qkv_w, R, qkv_w, d.d_model, EPI_STORE_F32, true, w.qkv, qkv_w, live), st);
         rope_kv(w.qkv, w.q, kvl, w.meta->pos, w.meta->slot, kv->page_table, m->inv_freq, R, live, d.n_heads,
                 d.n_kv_heads, d.head_dim, kv->max_pages, kv->page_tokens, st);
         attn_decode(w.q, kvl, w.attn, aa, R, d.head_dim, st);

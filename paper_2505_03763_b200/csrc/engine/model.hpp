@@ -30,7 +30,7 @@ struct Workspace {
     int rows = 0;
     float* x = nullptr;              // [rows, d] residual stream, fp32
     __nv_bfloat16* xn = nullptr;     // [rows, d]
-    __nv_bfloat16* qkv = nullptr;    // [rows, (H + 2Hkv) hd]
+    float* qkv = nullptr;            // [rows, (H + 2Hkv) hd] fp32 (rounded once, after RoPE)
     __nv_bfloat16* q = nullptr;      // [rows, H hd] roped
     __nv_bfloat16* attn = nullptr;   // [rows, H hd]
     __nv_bfloat16* act = nullptr;    // [rows, ffn]

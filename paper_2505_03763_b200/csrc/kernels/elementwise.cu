@@ -141,10 +141,11 @@ void rmsnorm(const float* x, const __nv_bfloat16* g, __nv_bfloat16* y, int rows,
 }
 
 // ---------------------------------------------------------------- RoPE + KV
-// qkv [T, (H + 2 Hkv) * hd] (GEMM output) -> q [T, H*hd] roped, and K (roped)
+// qkv fp32 [T, (H + 2 Hkv) * hd] (GEMM output, kept fp32 so q/k are rounded to
+// bf16 once, after the rotation) -> q [T, H*hd] roped, and K (roped)
 // / V scattered into the paged cache of layer `layer`:
 //   pages[layer][page][kv][head][page_tokens][hd],  page = table[slot][pos / B].
-__global__ void rope_kv_kernel(const __nv_bfloat16* __restrict__ qkv, __nv_bfloat16* __restrict__ q_out,
+__global__ void rope_kv_kernel(const float* __restrict__ qkv, __nv_bfloat16* __restrict__ q_out,
                                __nv_bfloat16* __restrict__ kv_layer, const int32_t* __restrict__ tok_pos,
                                const int32_t* __restrict__ tok_slot, const int32_t* __restrict__ page_table,
                                const float* __restrict__ inv_freq, int rows, const int* rows_dev, int H, int Hkv,
@@ -158,7 +159,7 @@ __global__ void rope_kv_kernel(const __nv_bfloat16* __restrict__ qkv, __nv_bfloa
     const int page = page_table[static_cast<int64_t>(slot) * max_pages + pos / page_tokens];
     const int off = pos % page_tokens;
     const int width = (H + 2 * Hkv) * hd;
-    const __nv_bfloat16* src = qkv + static_cast<int64_t>(t) * width;
+    const float* src = qkv + static_cast<int64_t>(t) * width;
     __nv_bfloat16* kbase = kv_layer + static_cast<int64_t>(page) * page_stride;
     const int64_t head_stride = static_cast<int64_t>(page_tokens) * hd;
     const int64_t kv_stride = static_cast<int64_t>(Hkv) * head_stride;
@@ -167,7 +168,7 @@ __global__ void rope_kv_kernel(const __nv_bfloat16* __restrict__ qkv, __nv_bfloa
         const int h = idx / half, i = idx % half;
         float s, c;
         sincosf(static_cast<float>(pos) * inv_freq[i], &s, &c);
-        const float a = bf2f(src[h * hd + i]), b = bf2f(src[h * hd + i + half]);
+        const float a = src[h * hd + i], b = src[h * hd + i + half];
         const __nv_bfloat16 ra = __float2bfloat16_rn(a * c - b * s);
         const __nv_bfloat16 rb = __float2bfloat16_rn(b * c + a * s);
         if (h < H) {
@@ -182,11 +183,11 @@ __global__ void rope_kv_kernel(const __nv_bfloat16* __restrict__ qkv, __nv_bfloa
     }
     for (int idx = threadIdx.x; idx < Hkv * hd; idx += blockDim.x) {
         const int h = idx / hd, i = idx % hd;
-        kbase[kv_stride + h * head_stride + off * hd + i] = src[(H + Hkv + h) * hd + i];
+        kbase[kv_stride + h * head_stride + off * hd + i] = __float2bfloat16_rn(src[(H + Hkv + h) * hd + i]);
     }
 }
 
-void rope_kv(const __nv_bfloat16* qkv, __nv_bfloat16* q_out, __nv_bfloat16* kv_layer, const int32_t* tok_pos,
+void rope_kv(const float* qkv, __nv_bfloat16* q_out, __nv_bfloat16* kv_layer, const int32_t* tok_pos,
              const int32_t* tok_slot, const int32_t* page_table, const float* inv_freq, int rows, const int* rows_dev,
              int H, int Hkv, int hd, int max_pages, int page_tokens, cudaStream_t st) {
     const int64_t page_stride = 2LL * Hkv * page_tokens * hd;
