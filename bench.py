@@ -1,0 +1,393 @@
+"""Benchmark: split-phase vs serial tokens/s on one B200 (and request-sharded
+replicas on N GPUs), with p50 TTFT/TBT, a kernel roofline line and the CPU
+oracle timed beside it.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+A "step" is one complete engine run of the BASELINE workload (configs[1]:
+Llama-3.2-1B shape, bf16, random weights, 64 requests x prompt 512 / gen 128)
+through the C-ABI (sw_engine_run).  value = generated tokens / device makespan
+(CUDA events inside the engine) summed over the K timed runs; e2e = the same
+tokens over the wall time of the sw_engine_run calls (prompt H2D staging and
+token/page-table D2H inside).  Under torchrun every rank runs its own engine
+on its round-robin shard of an N x 64-request trace (weak scaling); results
+are gathered with NCCL (torch.distributed) and timed as the max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "tokens/s/GPU split vs serial prefill+decode; p50 TTFT and TBT; 1/2/4/8 GPU"
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+
+WORKLOADS = {
+    # configs[1] of BASELINE.json -- the bench line
+    "1b": dict(model="LLAMA_1B", n=64, input=512, output=128, arrival="zero", max_prefill=32768, max_decode=64,
+               split="policy=pipelined_splitwiser;P=4;max_batch=16;engine.split=1",
+               serial="policy=sequential;max_batch=64;engine.split=0"),
+    # configs[2]: 8B shape, Poisson arrivals of mixed prompts, mixed batching vs continuous batching
+    "8b-poisson": dict(model="LLAMA_8B", n=128, input="128..2048", output=256, arrival="poisson:32",
+                       max_prefill=32768, max_decode=128,
+                       split="policy=mixed_batching;max_batch=128;engine.split=1",
+                       serial="policy=continuous_batching;max_batch=128;engine.split=0"),
+    # configs[0] shape on the GPU (fast sanity run)
+    "tiny": dict(model="TINY", n=8, input=64, output=32, arrival="zero", max_prefill=1024, max_decode=16,
+                 split="policy=pipelined_splitwiser;P=2;max_batch=4;engine.split=1",
+                 serial="policy=sequential;max_batch=8;engine.split=0"),
+}
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d, "measured"
+    return PEAKS_FALLBACK, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+
+        def loop():
+            while not self._stop.is_set():
+                try:
+                    out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                         timeout=5).stdout.strip()
+                    if out:
+                        self.samples.append([x.strip() for x in out.split(",")])
+                except Exception:
+                    pass
+                self._stop.wait(0.2)
+
+        self._t = threading.Thread(target=loop, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if len(s) > 3 + i and
+                          s[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------- CPU oracle
+def cpu_sample(desc_name: str, n_req: int = 4, prompt: int = 512, gen: int = 8):
+    """Time the fp32 CPU oracle (oracle/model.py, numpy/BLAS on all host
+    threads) on a bounded sample of the workload: n_req requests of the same
+    prompt length, `gen` greedy tokens each (x_1 from the prompt pass, then
+    gen-1 batched decode steps).  Weight generation is excluded."""
+    import numpy as np
+    from oracle import model as M
+
+    desc = getattr(M, desc_name)
+    t_init = time.perf_counter()
+    o = M.OracleModel(desc)
+    t_init = time.perf_counter() - t_init
+    prompts = [M.prompt_tokens(desc.seed, r, prompt, desc.vocab) for r in range(n_req)]
+    rows = [list(range(64 * r, 64 * r + 64)) for r in range(n_req)]
+    t0 = time.perf_counter()
+    lg = o.prefill(prompts, rows)
+    toks = [int(np.argmax(l)) for l in lg]
+    for g in range(1, gen):
+        lg = o.decode(toks, [prompt + g - 1] * n_req, rows)
+        toks = [int(np.argmax(l)) for l in lg]
+    dt = time.perf_counter() - t0
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    return {"value": n_req * gen / dt, "unit": "tokens/s", "cores": cores, "kind": "port",
+            "sample": f"{desc_name} full depth fp32 numpy oracle: {n_req} requests x prompt {prompt}, {gen} greedy "
+                      f"tokens each (prompt pass + {gen - 1} batched decode steps); weight init {t_init:.1f}s excluded",
+            "seconds": dt}
+
+
+# ----------------------------------------------------------------- roofline
+def roofline_decode_gemm(eng, desc, rows: int, peaks, reps: int = 20):
+    """The dominant kernel: the decode step's gate/up projection (swap-AB
+    tcgen05 GEMM with fused SwiGLU), HBM-bound.  Timed with CUDA events on the
+    stream it is launched on, rotating over all layers' weights (> L2) so every
+    launch streams from HBM.  Algorithmic bytes per launch = weights 2*ffn*d*2 +
+    activations rows*d*2 in + rows*ffn*2 out."""
+    import ctypes
+    import torch
+    import paper_2505_03763_b200 as sw
+
+    d, F, L = desc.d_model, desc.ffn_dim, desc.n_layers
+    x = torch.randn(rows, d, device="cuda").bfloat16()
+    y = torch.empty(rows, F, device="cuda", dtype=torch.bfloat16)
+    ws = [eng.tensor(f"layer{l}.wgu")[0] for l in range(L)]
+    st = torch.cuda.current_stream()
+    sp = ctypes.c_void_p(st.cuda_stream)
+
+    def launch(i):
+        sw.check(sw.lib().sw_op_gemm(ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(ws[i % L]),
+                                     ctypes.c_void_p(y.data_ptr()), rows, 2 * F, d, 2, sp))
+
+    for i in range(L):
+        launch(i)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for i in range(reps):
+        launch(i)
+    e1.record(st)
+    torch.cuda.synchronize()
+    t = e0.elapsed_time(e1) / 1e3 / reps
+    nbytes = 2 * F * d * 2 + rows * d * 2 + rows * F * 2
+    achieved = nbytes / t / 1e9
+    peak = float(peaks["hbm_gbs"])
+    return {"kernel": "gemm_tc_kernel<BN,SWIGLU,swap> (decode gate/up, rows=%d)" % rows, "bound": "hbm",
+            "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
+            "bytes_per_launch": nbytes, "us_per_launch": round(t * 1e6, 2)}
+
+
+def roofline_prefill_gemm(eng, desc, tokens: int, peaks, reps: int = 10):
+    """Prefill gate/up projection (normal-mode tcgen05 GEMM + SwiGLU), tensor-bound."""
+    import ctypes
+    import torch
+    import paper_2505_03763_b200 as sw
+
+    d, F, L = desc.d_model, desc.ffn_dim, desc.n_layers
+    x = torch.randn(tokens, d, device="cuda").bfloat16()
+    y = torch.empty(tokens, F, device="cuda", dtype=torch.bfloat16)
+    ws = [eng.tensor(f"layer{l}.wgu")[0] for l in range(L)]
+    st = torch.cuda.current_stream()
+    sp = ctypes.c_void_p(st.cuda_stream)
+
+    def launch(i):
+        sw.check(sw.lib().sw_op_gemm(ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(ws[i % L]),
+                                     ctypes.c_void_p(y.data_ptr()), tokens, 2 * F, d, 2, sp))
+
+    launch(0)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for i in range(reps):
+        launch(i)
+    e1.record(st)
+    torch.cuda.synchronize()
+    t = e0.elapsed_time(e1) / 1e3 / reps
+    flops = 2.0 * tokens * 2 * F * d
+    achieved = flops / t / 1e12
+    peak = float(peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"]))
+    return {"kernel": "gemm_tc_kernel<256,SWIGLU,normal> (prefill gate/up, tokens=%d)" % tokens, "bound": "tensor",
+            "achieved": round(achieved, 1), "peak": peak, "unit": "TFLOP/s", "frac": round(achieved / peak, 4),
+            "us_per_launch": round(t * 1e6, 1)}
+
+
+# ----------------------------------------------------------------- engine runs
+def spec_for(w, extra: str, rank: int, world: int) -> str:
+    s = (f"n={w['n'] * world};input={w['input']};output={w['output']};seed=1;arrival={w['arrival']};"
+         f"kv_capacity_blocks={w['kv_pages']};{extra}")
+    if world > 1:
+        s += f";shard={rank}/{world}"
+    return s
+
+
+def run_many(eng, spec: str, k: int):
+    import paper_2505_03763_b200 as sw
+
+    tokens = 0
+    makespan = 0.0
+    wall = 0.0
+    ttft, tbt = [], []
+    l0 = sw.launch_count()
+    h0, d0 = sw.transfer_bytes()
+    last = None
+    for _ in range(k):
+        t0 = time.perf_counter()
+        r = eng.run(spec)
+        wall += time.perf_counter() - t0
+        tokens += int(r.report["total_output_tokens"])
+        makespan += r.report["makespan_s"]
+        ttft.append(r.report["p50_ttft_s"])
+        tbt.append(r.report["p50_tbt_s"])
+        last = r
+    h1, d1 = sw.transfer_bytes()
+    return dict(tokens=tokens, makespan=makespan, wall=wall, p50_ttft=statistics.median(ttft),
+                p50_tbt=statistics.median(tbt), launches=sw.launch_count() - l0, h2d=(h1 - h0) / max(k, 1),
+                d2h=(d1 - d0) / max(k, 1), last=last)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="1b")
+    ap.add_argument("--split", default=None, help="override the split-phase policy spec")
+    ap.add_argument("--serial", default=None, help="override the serial policy spec")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    w = dict(WORKLOADS[args.workload])
+    peaks, peaks_src = load_peaks()
+
+    if args.impl == "reference":
+        # The reference's own CPU implementation of the path: it has no model math
+        # (splitsim prices phases with a roofline law), so this arm times the fp32
+        # CPU oracle port on the host cores, rank 0 only.
+        if rank != 0:
+            return
+        samples = [cpu_sample(w["model"] if w["model"] != "LLAMA_8B" else "LLAMA_1B") for _ in range(max(args.steps, 1))]
+        v = statistics.median(s["value"] for s in samples)
+        line = {"impl": "reference", "metric": METRIC, "value": round(v, 3), "unit": "tokens/s", "n_gpus": args.gpus,
+                "steps": args.steps, "warmup": 0, "ms_per_step": round(1e3 * statistics.median(s["seconds"] for s in samples), 1),
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "config": {"workload": args.workload, "sample": samples[0]["sample"]},
+                "cpu_baseline": {k: samples[0][k] for k in ("unit", "cores", "kind", "sample")} | {"value": round(v, 3)},
+                "e2e": {"value": round(v, 3), "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+
+    import torch
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from oracle import model as M  # shapes only (Desc constants)
+    from paper_2505_03763_b200 import runtime
+
+    desc = getattr(M, w["model"])
+    n_local = w["n"]
+    in_max = int(str(w["input"]).split("..")[-1])
+    pages_per = (in_max + w["output"] + 15) // 16
+    w["kv_pages"] = n_local * pages_per + 64
+    t_init = time.perf_counter()
+    eng = runtime.Engine(desc, max_prefill_tokens=w["max_prefill"], max_decode_batch=w["max_decode"],
+                         n_pages=w["kv_pages"], n_slots=n_local + 8, max_pages_per_slot=pages_per + 1,
+                         max_out=w["output"] + 1, device=local)
+    t_init = time.perf_counter() - t_init
+    split_spec = spec_for(w, args.split or w["split"], rank, world)
+    serial_spec = spec_for(w, args.serial or w["serial"], rank, world)
+
+    for _ in range(args.warmup):
+        eng.run(split_spec)
+    for _ in range(max(1, args.warmup // 3)):
+        eng.run(serial_spec)
+
+    def timed(spec):
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        res = run_many(eng, spec, args.steps)
+        torch.cuda.synchronize()
+        if dist:
+            t = torch.tensor([res["makespan"], res["wall"], float(res["tokens"])], device="cuda", dtype=torch.float64)
+            g = [torch.zeros_like(t) for _ in range(world)]
+            dist.all_gather(g, t)  # NCCL result gathering (the only collective)
+            res["makespan"] = max(float(x[0]) for x in g)
+            res["wall"] = max(float(x[1]) for x in g)
+            res["tokens"] = sum(float(x[2]) for x in g)
+        return res
+
+    with ClockSampler(local) as clocks:
+        split = timed(split_spec)
+    serial = timed(serial_spec)
+
+    roof = roofline_decode_gemm(eng, desc, w["max_decode"], peaks) if rank == 0 else None
+    roof_prefill = roofline_prefill_gemm(eng, desc, 4096, peaks) if rank == 0 else None
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "roofline_traffic.json")
+    if os.path.exists(tpath) and roof:
+        with open(tpath) as f:
+            traffic = json.load(f).get(args.workload, {}).get("decode_gate_up_bytes")
+    if rank != 0:
+        if dist:
+            dist.barrier()
+            dist.destroy_process_group()
+        eng.close()
+        return
+
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_sample("LLAMA_1B" if w["model"] != "TINY" else "TINY")
+        except Exception as e:  # never fail the GPU line on the CPU sample
+            cpu = {"value": None, "unit": "tokens/s", "cores": os.cpu_count(), "kind": "port", "sample": f"failed: {e}"}
+
+    value = split["tokens"] / split["makespan"]
+    serial_v = serial["tokens"] / serial["makespan"]
+    line = {
+        "metric": METRIC,
+        "value": round(value, 1),
+        "unit": "tokens/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(1e3 * split["makespan"] / args.steps, 2),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "bf16",
+        "data": "synthetic (SplitMix64 random-init weights and prompts)",
+        "config": {"workload": args.workload, "model_shape": w["model"], "requests_per_gpu": n_local,
+                   "prompt": w["input"], "gen": w["output"], "arrival": w["arrival"],
+                   "split_policy": args.split or w["split"], "serial_policy": args.serial or w["serial"],
+                   "l2": "working set > L2: every decode step streams all weights (2.5-16 GB)",
+                   "parallelism": f"request-sharded replicas x{world}"},
+        "split": {"tokens_per_s": round(value, 1), "p50_ttft_s": split["p50_ttft"], "p50_tbt_s": split["p50_tbt"]},
+        "serial": {"tokens_per_s": round(serial_v, 1), "p50_ttft_s": serial["p50_ttft"],
+                   "p50_tbt_s": serial["p50_tbt"]},
+        "split_over_serial": round(value / serial_v, 4),
+        "e2e": {"value": round(split["tokens"] / split["wall"], 1), "unit": "tokens/s",
+                "h2d_bytes_per_step": int(split["h2d"]), "d2h_bytes_per_step": int(split["d2h"])},
+        "gpu_launches": int(split["launches"]),
+        "roofline": None,
+        "roofline_prefill": roof_prefill,
+        "cpu_baseline": cpu,
+        "clocks": clocks.summary(),
+        "peaks_source": peaks_src,
+        "init_s": round(t_init, 1),
+    }
+    if roof:
+        line["roofline"] = {"bound": roof["bound"], "achieved": roof["achieved"], "peak": roof["peak"],
+                            "unit": roof["unit"], "frac": roof["frac"], "traffic": traffic, "kernel": roof["kernel"],
+                            "us_per_launch": roof["us_per_launch"], "bytes_per_launch": roof["bytes_per_launch"]}
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+    eng.close()
+
+
+if __name__ == "__main__":
+    main()

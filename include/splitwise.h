@@ -85,6 +85,10 @@ typedef struct sw_batch {
 
 const char* sw_last_error(void);
 void sw_free(void* p);
+/* Kernels launched by this library so far (graph replays count their nodes). */
+unsigned long long sw_launch_count(void);
+/* Host->device and device->host bytes moved by the run path so far. */
+void sw_transfer_bytes(unsigned long long* h2d, unsigned long long* d2h);
 
 /* ---- run level ---- */
 /* spec: `key=value;...` (see csrc/host/spec.hpp).  *out receives a malloc'd

@@ -90,6 +90,9 @@ def lib() -> ctypes.CDLL:
         L.sw_free.argtypes = [c_void_p]
         L.sw_sim_run.argtypes = [c_char_p, ctypes.POINTER(c_void_p)]
         L.sw_sim_run.restype = c_int
+        L.sw_launch_count.restype = ctypes.c_ulonglong
+        L.sw_transfer_bytes.argtypes = [ctypes.POINTER(ctypes.c_ulonglong)] * 2
+        L.sw_transfer_bytes.restype = None
         for name, args in {
             "sw_engine_run": [c_void_p, c_void_p, c_char_p, ctypes.POINTER(c_void_p)],
             "sw_model_create": [ctypes.POINTER(ModelDesc), c_int, ctypes.POINTER(c_void_p)],
@@ -117,7 +120,7 @@ def lib() -> ctypes.CDLL:
 
 
 EXPORTED_SYMBOLS = [
-    "sw_last_error", "sw_free", "sw_sim_run", "sw_engine_run", "sw_model_create", "sw_model_destroy",
+    "sw_last_error", "sw_free", "sw_launch_count", "sw_transfer_bytes", "sw_sim_run", "sw_engine_run", "sw_model_create", "sw_model_destroy",
     "sw_model_weight_checksum", "sw_model_tensor", "sw_kv_arena_create", "sw_kv_arena_destroy",
     "sw_kv_arena_views", "sw_prefill_enqueue", "sw_decode_enqueue", "sw_op_gemm", "sw_op_rmsnorm",
 ]
@@ -194,3 +197,13 @@ def sim_run(spec) -> RunResult:
     out = ctypes.c_void_p()
     check(lib().sw_sim_run(s.encode(), ctypes.byref(out)))
     return parse_run_text(_take_text(out))
+
+
+def launch_count() -> int:
+    return int(lib().sw_launch_count())
+
+
+def transfer_bytes():
+    h, d = ctypes.c_ulonglong(), ctypes.c_ulonglong()
+    lib().sw_transfer_bytes(ctypes.byref(h), ctypes.byref(d))
+    return int(h.value), int(d.value)

@@ -183,6 +183,7 @@ public:
         SW_CUDA(cudaMemcpy(host.data(), kv_->out_tokens, host.size() * 4, cudaMemcpyDeviceToHost));
         std::vector<int32_t> table(static_cast<size_t>(kv_->n_slots) * kv_->max_pages);
         SW_CUDA(cudaMemcpy(table.data(), kv_->page_table, table.size() * 4, cudaMemcpyDeviceToHost));
+        count_transfer(0, (host.size() + table.size()) * 4);
         for (const Entry& e : entries_) {
             const int slot = slot_of_.at(e.req.id);
             s += "#tokens " + std::to_string(e.req.id) + ":";

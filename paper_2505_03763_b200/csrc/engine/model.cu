@@ -21,6 +21,7 @@
 // reads the live row count and per-row metadata from a device StepMeta the
 // host refreshes with a single H2D copy per step.
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstddef>
 #include <cstring>
@@ -34,6 +35,8 @@
 #include "model.hpp"
 
 namespace sw {
+
+extern std::atomic<unsigned long long> g_launches;
 
 namespace {
 
@@ -223,6 +226,7 @@ void prefill_forward(sw_model* m, sw_kv* kv, const sw_batch& b, cudaStream_t st)
         const size_t bytes = static_cast<size_t>(p - h) * sizeof(int32_t);
         if (bytes > w.pmeta_bytes || bytes > m->pre_ring.bytes) throw ContractViolation("prefill: metadata overflow");
         SW_CUDA(cudaMemcpyAsync(w.pmeta, h, bytes, cudaMemcpyHostToDevice, st));
+        count_transfer(bytes, 0);
         ring_release(m->pre_ring, idx, st);
         auto dev = [&](int32_t* hp) { return w.pmeta + (hp - h); };
 
@@ -336,11 +340,13 @@ void decode_forward(sw_model* m, sw_kv* kv, const sw_batch& b, cudaStream_t st, 
     }
     const size_t bytes = offsetof(StepMeta, slot) + sizeof(StepMeta::slot) * 5;
     SW_CUDA(cudaMemcpyAsync(m->dec.meta, h, bytes, cudaMemcpyHostToDevice, st));
+    count_transfer(bytes, 0);
     ring_release(m->dec_ring, idx, st);
     const int R = std::min(decode_bucket(b.n), m->dec.rows);
     DecodeGraph& g = m->graphs[{kv, R}];
     if (use_graph && g.exec) {
         SW_CUDA(cudaGraphLaunch(g.exec, st));
+        count_launches(g.kernels);
     } else {
         decode_layers(m, kv, R, st);
         if (use_graph && ++g.eager_runs >= 1) {
@@ -349,7 +355,10 @@ void decode_forward(sw_model* m, sw_kv* kv, const sw_batch& b, cudaStream_t st, 
             SW_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
             cudaGraph_t graph;
             SW_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+            const unsigned long long before = g_launches.load();
             decode_layers(m, kv, R, cs);
+            g.kernels = g_launches.load() - before;
+            g_launches.fetch_sub(g.kernels);  // captured, not launched
             SW_CUDA(cudaStreamEndCapture(cs, &graph));
             SW_CUDA(cudaGraphInstantiate(&g.exec, graph, 0));
             SW_CUDA(cudaGraphDestroy(graph));

@@ -55,6 +55,7 @@ struct PinnedRing {
 struct DecodeGraph {
     cudaGraphExec_t exec = nullptr;
     int eager_runs = 0;
+    unsigned long long kernels = 0;  // kernel nodes in the graph
 };
 
 }  // namespace sw

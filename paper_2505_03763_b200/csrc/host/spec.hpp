@@ -62,6 +62,7 @@ struct RunSpec {
     double mem_budget_units = 22016.0;
     double block_mem_unit = 1.0;
     long long kv_capacity_override = 0;  // 0 = derive
+    int shard_index = 0, shard_count = 1;  // request sharding across replicas (GPUs)
     SpecMap rest;                        // backend-specific keys (engine.*, model.*)
 };
 
@@ -147,13 +148,29 @@ inline RunSpec build_spec(const SpecMap& m) {
         else if (k == "cost.prompt_overhead_s") s.inputs.cost.prompt_overhead_s = num(k, v);
         else if (k == "cost.step_overhead_s") s.inputs.cost.step_overhead_s = num(k, v);
         else if (k == "cost.kv_handoff_s") s.inputs.cost.kv_handoff_s = num(k, v);
-        else if (k.rfind("engine.", 0) == 0 || k.rfind("model.", 0) == 0) s.rest[k] = v;
+        else if (k == "shard") {
+            const auto slash = v.find('/');
+            if (slash == std::string::npos) throw ConfigError("shard: expected <index>/<count>");
+            s.shard_index = static_cast<int>(integer(k, v.substr(0, slash)));
+            s.shard_count = static_cast<int>(integer(k, v.substr(slash + 1)));
+            if (s.shard_count < 1 || s.shard_index < 0 || s.shard_index >= s.shard_count)
+                throw ConfigError("shard: index must be in [0, count)");
+        } else if (k.rfind("engine.", 0) == 0 || k.rfind("model.", 0) == 0) s.rest[k] = v;
         else if (k == "trace") s.rest[k] = v;
         else throw ConfigError("spec: unknown key '" + k + "'");
         have_ws = have_ws || k == "n";
     }
     validate(s.scheduler);
     s.inputs.requests = generate(s.workload);
+    if (s.shard_count > 1) {
+        // one replica's share of the trace: round robin by arrival order, the
+        // reference's multi_instance_split rule (schedulers.hpp:86-92); ids stay global
+        std::vector<Request> mine;
+        for (std::size_t i = 0; i < s.inputs.requests.size(); ++i)
+            if (static_cast<int>(i % static_cast<std::size_t>(s.shard_count)) == s.shard_index)
+                mine.push_back(s.inputs.requests[i]);
+        s.inputs.requests.swap(mine);
+    }
     s.inputs.gpu.kv_capacity_blocks =
         derive_kv_capacity(s.mem_budget_units, s.inputs.gpu.weight_mem_units, s.block_mem_unit,
                            s.inputs.gpu.shared_weights, model_instances(s.scheduler), s.kv_capacity_override);

@@ -20,7 +20,15 @@ struct CudaError;  // capi_util.hpp
         if (e_ != cudaSuccess) ::sw::throw_cuda(#call, e_, __FILE__, __LINE__); \
     } while (0)
 
-#define SW_LAUNCH_CHECK() SW_CUDA(cudaGetLastError())
+// Every kernel launch site goes through SW_LAUNCH_CHECK, which also counts the
+// launch (sw_launch_count in the C-ABI; CUDA-graph replays add their node count).
+void count_launches(unsigned long long n);
+void count_transfer(unsigned long long h2d, unsigned long long d2h);  // host<->device bytes of the run path
+#define SW_LAUNCH_CHECK()                 \
+    do {                                  \
+        SW_CUDA(cudaGetLastError());      \
+        ::sw::count_launches(1);          \
+    } while (0)
 
 __host__ __device__ constexpr int cdiv(int a, int b) { return (a + b - 1) / b; }
 
