@@ -136,7 +136,7 @@ class OracleModel:
 
     emulate_bf16=False is THE reference: everything in fp32.  emulate_bf16=True
     additionally rounds to bf16 exactly where the CUDA path stores bf16
-    (RMSNorm outputs, roped q/k and v -- the KV cache --, the prefill softmax
+    (RMSNorm outputs, roped q/k and v -- the KV cache --, the softmax
     numerators fed to the P.V tensor-core product, attention output, SwiGLU
     output), so the remaining difference is accumulation order only.
     """
@@ -221,7 +221,7 @@ class OracleModel:
             sc = sc - sc.max(axis=1, keepdims=True)
             p = np.exp(sc)
             l = p.sum(axis=1, keepdims=True)
-            if self.emul and self._phase == "prefill":
+            if self.emul:  # both attention kernels feed bf16 P to the P.V tensor-core product
                 p = bf16_round(p)
             out[:, h, :] = (p @ vh) / l
         return out

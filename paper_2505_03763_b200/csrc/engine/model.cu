@@ -41,6 +41,8 @@ extern std::atomic<unsigned long long> g_launches;
 namespace {
 
 constexpr int kLmRowsMax = 256;  // LM-head rows per launch (swap-AB N <= 256)
+constexpr int kSplitTiles = 640;     // split-K scratch: (tiles x splits) capacity
+constexpr int kSplitCounters = 1024;
 
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
@@ -97,6 +99,12 @@ void ws_alloc(Workspace& w, const sw_model_desc& d, int rows, bool decode, int m
         const size_t parts = static_cast<size_t>(kMaxDecodeRows) * d.n_kv_heads * max_splits_cap * G;
         w.part_o = dalloc<float>(parts * d.head_dim);
         w.part_ml = dalloc<float>(parts * 2);
+        w.attn_cnt = dalloc<unsigned>(static_cast<size_t>(kMaxDecodeRows) * d.n_kv_heads);
+        SW_CUDA(cudaMemset(w.attn_cnt, 0, static_cast<size_t>(kMaxDecodeRows) * d.n_kv_heads * sizeof(unsigned)));
+        w.splitk_floats = static_cast<size_t>(kSplitTiles) * 256 * 128;
+        w.splitk_ws = dalloc<float>(w.splitk_floats);
+        w.splitk_cnt = dalloc<unsigned>(kSplitCounters);
+        SW_CUDA(cudaMemset(w.splitk_cnt, 0, kSplitCounters * sizeof(unsigned)));
     } else {
         // header + tokens/pos/slot per token + per-seq arrays + tiles + page rows
         const size_t T = static_cast<size_t>(rows);
@@ -106,8 +114,14 @@ void ws_alloc(Workspace& w, const sw_model_desc& d, int rows, bool decode, int m
 }
 
 GemmProblem gp(const void* X, int64_t x_rows, const void* W, int64_t w_rows, int tokens, int features, int K,
-               int mode, bool swap, void* out, int ldo, const int* live = nullptr) {
+               int mode, bool swap, void* out, int ldo, const int* live = nullptr, const Workspace* ws = nullptr) {
     GemmProblem p{};
+    if (ws && ws->splitk_ws) {
+        p.ws = ws->splitk_ws;
+        p.ws_floats = ws->splitk_floats;
+        p.counters = ws->splitk_cnt;
+        p.n_counters = kSplitCounters;
+    }
     p.X = X;
     p.x_rows = x_rows;
     p.W = W;
@@ -255,7 +269,7 @@ void prefill_forward(sw_model* m, sw_kv* kv, const sw_batch& b, cudaStream_t st)
             __nv_bfloat16* kvl = kv->pages + l * kv->layer_stride;
             rmsnorm(w.x, L.g_attn, w.xn, T, d.d_model, d.norm_eps, nullptr, nullptr, st);
             gemm_run(gp(w.xn, w.rows, L.wqkv, qkv_w, T, qkv_w, d.d_model, EPI_STORE_F32, false, w.qkv, qkv_w), st);
-            rope_kv(w.qkv, w.q, kvl, dev(tpos), dev(tslot), kv->page_table, m->inv_freq, T, nullptr, d.n_heads,
+            rope_kv(w.qkv, w.q, kvl, dev(tpos), dev(tslot), kv->page_table, m->rope_cs, T, nullptr, d.n_heads,
                     d.n_kv_heads, d.head_dim, kv->max_pages, B, st);
             attn_prefill(w.q, kvl, w.attn, aa, n_tiles, d.head_dim, st);
             gemm_run(gp(w.attn, w.rows, L.wo, d.d_model, T, d.d_model, hdH, EPI_RESID, false, w.x, d.d_model), st);
@@ -297,20 +311,21 @@ void decode_layers(sw_model* m, sw_kv* kv, int R, cudaStream_t st) {
     aa.max_splits = kv->max_splits;
     aa.part_o = w.part_o;
     aa.part_ml = w.part_ml;
+    aa.counters = w.attn_cnt;
     for (int l = 0; l < d.n_layers; ++l) {
         const LayerWeights& L = m->layers[l];
         __nv_bfloat16* kvl = kv->pages + l * kv->layer_stride;
         rmsnorm(w.x, L.g_attn, w.xn, R, d.d_model, d.norm_eps, live, nullptr, st);
-        gemm_run(gp(w.xn, w.rows, L.wqkv, qkv_w, R, qkv_w, d.d_model, EPI_STORE_F32, true, w.qkv, qkv_w, live), st);
-        rope_kv(w.qkv, w.q, kvl, w.meta->pos, w.meta->slot, kv->page_table, m->inv_freq, R, live, d.n_heads,
+        gemm_run(gp(w.xn, w.rows, L.wqkv, qkv_w, R, qkv_w, d.d_model, EPI_STORE_F32, true, w.qkv, qkv_w, live, &w), st);
+        rope_kv(w.qkv, w.q, kvl, w.meta->pos, w.meta->slot, kv->page_table, m->rope_cs, R, live, d.n_heads,
                 d.n_kv_heads, d.head_dim, kv->max_pages, kv->page_tokens, st);
         attn_decode(w.q, kvl, w.attn, aa, R, d.head_dim, st);
-        gemm_run(gp(w.attn, w.rows, L.wo, d.d_model, R, d.d_model, hdH, EPI_RESID, true, w.x, d.d_model, live), st);
+        gemm_run(gp(w.attn, w.rows, L.wo, d.d_model, R, d.d_model, hdH, EPI_RESID, true, w.x, d.d_model, live, &w), st);
         rmsnorm(w.x, L.g_mlp, w.xn, R, d.d_model, d.norm_eps, live, nullptr, st);
         gemm_run(gp(w.xn, w.rows, L.wgu, 2 * d.ffn_dim, R, 2 * d.ffn_dim, d.d_model, EPI_SWIGLU, true, w.act,
-                    d.ffn_dim, live),
+                    d.ffn_dim, live, &w),
                  st);
-        gemm_run(gp(w.act, w.rows, L.wd, d.d_model, R, d.d_model, d.ffn_dim, EPI_RESID, true, w.x, d.d_model, live),
+        gemm_run(gp(w.act, w.rows, L.wd, d.d_model, R, d.d_model, d.ffn_dim, EPI_RESID, true, w.x, d.d_model, live, &w),
                  st);
     }
     rmsnorm(w.x, m->g_final, w.xlast, R, d.d_model, d.norm_eps, live, nullptr, st);
@@ -455,6 +470,8 @@ extern "C" int sw_model_create(const sw_model_desc* desc, int device, sw_model**
             inv[i] = static_cast<float>(1.0 / std::pow(static_cast<double>(d.rope_theta), 2.0 * i / hd));
         m->inv_freq = dalloc<float>(hd / 2);
         SW_CUDA(cudaMemcpy(m->inv_freq, inv.data(), inv.size() * 4, cudaMemcpyHostToDevice));
+        m->rope_cs = dalloc<float2>(static_cast<size_t>(kMaxPositions) * (hd / 2));
+        rope_table(m->inv_freq, m->rope_cs, kMaxPositions, static_cast<int>(hd / 2), st);
         ws_alloc(m->pre, d, d.max_prefill_tokens, false, 1);
         ws_alloc(m->dec, d, std::min(d.max_decode_batch, kMaxDecodeRows), true, 16);
         ring_init(m->pre_ring, 4, m->pre.pmeta_bytes);
@@ -474,7 +491,7 @@ extern "C" int sw_model_destroy(sw_model* m) {
         for (Workspace* w : {&m->pre, &m->dec}) {
             for (void* p : {(void*)w->x, (void*)w->xn, (void*)w->qkv, (void*)w->q, (void*)w->attn, (void*)w->act,
                             (void*)w->xlast, (void*)w->keys, (void*)w->meta, (void*)w->part_o, (void*)w->part_ml,
-                            (void*)w->pmeta})
+                            (void*)w->pmeta, (void*)w->splitk_ws, (void*)w->splitk_cnt, (void*)w->attn_cnt})
                 if (p) cudaFree(p);
         }
         for (PinnedRing* r : {&m->pre_ring, &m->dec_ring}) {
@@ -482,6 +499,7 @@ extern "C" int sw_model_destroy(sw_model* m) {
             for (cudaEvent_t e : r->done) cudaEventDestroy(e);
         }
         cudaFree(m->inv_freq);
+        cudaFree(m->rope_cs);
         cudaFree(m->scratch_u64);
         cudaFree(m->weight_arena);
         delete m;
@@ -512,6 +530,8 @@ extern "C" int sw_kv_arena_create(sw_model* m, int64_t n_pages, int32_t n_slots,
     return guarded([&] {
         if (!m || !out || n_pages < 1 || n_slots < 1 || max_pages_per_slot < 1 || max_out_tokens < 1)
             throw ConfigError("sw_kv_arena_create: bad arguments");
+        if (static_cast<int64_t>(max_pages_per_slot) * 16 > kMaxPositions)
+            throw ConfigError("sw_kv_arena_create: context longer than " + std::to_string(kMaxPositions) + " tokens");
         const sw_model_desc& d = m->desc;
         auto kv = std::make_unique<sw_kv>();
         kv->model = m;
@@ -587,9 +607,17 @@ extern "C" int sw_decode_enqueue(sw_model* m, sw_kv* kv, const sw_batch* b, void
 extern "C" int sw_op_gemm(const void* A, const void* B, void* C, int32_t M, int32_t N, int32_t K, int32_t epilogue,
                           void* stream) {
     return guarded([&] {
-        // A = activations [M, K], B = weights [N, K]; swap-AB when M <= 256
+        // A = activations [M, K], B = weights [N, K]; swap-AB (+ split-K) when M <= 256
         const bool swap = M <= 256;
-        GemmProblem p = gp(A, M, B, N, M, N, K, epilogue, swap, C, epilogue == EPI_SWIGLU ? N / 2 : N);
+        static Workspace op_ws;  // split-K scratch for op-level calls
+        if (!op_ws.splitk_ws) {
+            op_ws.splitk_floats = static_cast<size_t>(kSplitTiles) * 256 * 128;
+            op_ws.splitk_ws = dalloc<float>(op_ws.splitk_floats);
+            op_ws.splitk_cnt = dalloc<unsigned>(kSplitCounters);
+            SW_CUDA(cudaMemset(op_ws.splitk_cnt, 0, kSplitCounters * sizeof(unsigned)));
+        }
+        GemmProblem p = gp(A, M, B, N, M, N, K, epilogue, swap, C, epilogue == EPI_SWIGLU ? N / 2 : N, nullptr,
+                           swap ? &op_ws : nullptr);
         gemm_run(p, static_cast<cudaStream_t>(stream));
     });
 }

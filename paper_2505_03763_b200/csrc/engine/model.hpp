@@ -38,8 +38,12 @@ struct Workspace {
     unsigned long long* keys = nullptr;  // [256] packed argmax
     // decode only
     StepMeta* meta = nullptr;
+    float* splitk_ws = nullptr;  // split-K partial tiles of the decode GEMMs
+    size_t splitk_floats = 0;
+    unsigned* splitk_cnt = nullptr;
     float* part_o = nullptr;
     float* part_ml = nullptr;
+    unsigned* attn_cnt = nullptr;  // split-KV arrival counters [rows][Hkv]
     // prefill only: device metadata block
     int32_t* pmeta = nullptr;
     size_t pmeta_bytes = 0;
@@ -71,6 +75,7 @@ struct sw_model {
     std::vector<sw::LayerWeights> layers;
     std::map<std::string, std::pair<void*, int64_t>> tensors;
     float* inv_freq = nullptr;
+    float2* rope_cs = nullptr;  // [kMaxPositions][hd/2] (cos, sin)
     sw::Workspace pre, dec;
     sw::PinnedRing pre_ring, dec_ring;
     std::map<std::pair<const sw_kv*, int>, sw::DecodeGraph> graphs;  // (arena, row bucket)
@@ -93,6 +98,7 @@ struct sw_kv {
 };
 
 namespace sw {
+constexpr int kMaxPositions = 32768;  // RoPE table extent (max context)
 // Forward passes (stream-ordered; host arrays staged internally).
 void prefill_forward(sw_model* m, sw_kv* kv, const sw_batch& b, cudaStream_t st);
 void decode_forward(sw_model* m, sw_kv* kv, const sw_batch& b, cudaStream_t st, bool use_graph);

@@ -6,11 +6,9 @@
 //   straight from the 16-token pages just written by rope_kv (double-buffered
 //   cp.async, XOR-swizzled 16 B chunks for conflict-free ldmatrix); QK^T and
 //   PV on the tensor cores with mma.m16n8k16 bf16 -> fp32.
-// Decode: split-KV paged attention.  One CTA = one (row, kv head, split of
-//   the context); the G = H/Hkv query heads sharing the kv head are packed so
-//   every K/V byte is read once per step.  64-key steps double-buffered in
-//   smem; partial (max, sum, unnormalised O) per split, merged by
-//   attn_decode_combine.  HBM-bound by design.
+// Decode: split-KV paged attention on the tensor cores (see below); the G =
+//   H/Hkv query heads sharing a kv head are packed into one mma tile so every
+//   K/V byte is read once per step.  HBM-bound by design.
 #include "attention.cuh"
 #include "common.cuh"
 
@@ -231,172 +229,233 @@ __global__ void __launch_bounds__(128) attn_prefill_kernel(const __nv_bfloat16* 
 }
 
 // ------------------------------------------------------------------ decode
-constexpr int kDecKeys = 64;  // keys per smem step
-constexpr int kPad = 8;       // row padding (bf16) against bank conflicts
-
-template <int HD, int G>
+// One CTA = (row, kv head, split of the context).  Its 4 warps stream
+// disjoint KB-key blocks of the split (warp w takes blocks w, w+4, ...)
+// through private double-buffered smem, each with its own online softmax;
+// the G query heads of the kv head are the rows of a 16-row mma tile
+// (rows >= G are zero), so Q.K^T and P.V run on the tensor cores and the
+// kernel is a pure HBM stream of K/V pages.  Warps merge in smem; splits
+// merge in the last-arriving CTA of the (row, kv head) (ordered, so results
+// do not depend on timing).
+template <int HD, int G, int KB>
 __global__ void __launch_bounds__(128) attn_decode_kernel(const __nv_bfloat16* __restrict__ q,
                                                           const __nv_bfloat16* __restrict__ kv_layer,
-                                                          DecodeAttnArgs a) {
-    constexpr int LD = HD + kPad;
-    extern __shared__ __align__(16) uint8_t dsmem[];
-    auto sK = reinterpret_cast<__nv_bfloat16(*)[kDecKeys * LD]>(dsmem);                  // [2]
-    auto sV = reinterpret_cast<__nv_bfloat16(*)[kDecKeys * LD]>(dsmem + 2 * kDecKeys * LD * 2);  // [2]
-    float* sQ = reinterpret_cast<float*>(dsmem + 4 * kDecKeys * LD * 2);                 // [G*HD]
-    auto sS = reinterpret_cast<float(*)[kDecKeys]>(sQ + G * HD);                         // [G]
-    float* sAlpha = reinterpret_cast<float*>(sS + G);
+                                                          __nv_bfloat16* __restrict__ out, DecodeAttnArgs a) {
+    static_assert(G <= 8, "query rows live in the first 8 mma rows");
+    constexpr int CH = HD / 8;
+    extern __shared__ __align__(128) uint8_t dsm[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    __nv_bfloat16* wK = reinterpret_cast<__nv_bfloat16*>(dsm) + warp * (4 * KB * HD);  // [2][KB][HD]
+    __nv_bfloat16* wV = wK + 2 * KB * HD;                                               // [2][KB][HD]
+    float* cm = reinterpret_cast<float*>(dsm + 4 * (4 * KB * HD) * 2);  // [4][G]
+    float* cl = cm + 4 * G;                                             // [4][G]
+    float* co = cl + 4 * G;                                             // [4][G][HD]
+    __shared__ uint32_t s_last;
 
     const int row = blockIdx.z;
     if (row >= a.meta->n) return;
     const int ctx = a.meta->pos[row] + 1;
-    const int k_begin = blockIdx.x * a.chunk;
-    if (k_begin >= ctx) return;
+    const int splits = cdiv(ctx, a.chunk);
+    const int split = blockIdx.x;
+    if (split >= splits) return;
+    const int k_begin = split * a.chunk;
     const int k_end = min(ctx, k_begin + a.chunk);
     const int hk = blockIdx.y;
-    const int slot = a.meta->slot[row];
-    const int32_t* ptab = a.page_table + static_cast<int64_t>(slot) * a.max_pages;
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int32_t* ptab = a.page_table + static_cast<int64_t>(a.meta->slot[row]) * a.max_pages;
+    const int n_blocks = cdiv(k_end - k_begin, KB);
 
-    for (int i = tid; i < G * HD; i += 128)
-        sQ[i] = bf2f(q[static_cast<int64_t>(row) * a.H * HD + (hk * G) * HD + i]) * a.scale_log2;
+    // Q fragment (A operand, rows = query heads of this kv head)
+    const int r = lane >> 2;
+    uint32_t qf[HD / 16][4];
+    const __nv_bfloat16* qrow = q + static_cast<int64_t>(row) * a.H * HD + static_cast<int64_t>(hk * G + r) * HD;
+#pragma unroll
+    for (int ks = 0; ks < HD / 16; ++ks) {
+        const int c = ks * 16 + (lane & 3) * 2;
+        qf[ks][0] = r < G ? *reinterpret_cast<const uint32_t*>(qrow + c) : 0u;
+        qf[ks][1] = 0u;
+        qf[ks][2] = r < G ? *reinterpret_cast<const uint32_t*>(qrow + c + 8) : 0u;
+        qf[ks][3] = 0u;
+    }
 
-    constexpr int CH = HD / 8;
-    auto load = [&](int k0, int buf) {
-        for (int i = tid; i < kDecKeys * CH; i += 128) {
-            const int r = i / CH, c = i % CH;
-            const int key = k0 + r;
+    auto load = [&](int blk, int buf) {
+        const int k0 = k_begin + blk * KB;
+        for (int i = lane; i < KB * CH; i += 32) {
+            const int kr = i / CH, c = i % CH;
+            const int key = k0 + kr;
             const bool ok = key < k_end;
             const int page = ok ? ptab[key / a.page_tokens] : 0;
-            const __nv_bfloat16* base = kv_layer + static_cast<int64_t>(page) * a.page_stride +
-                                        static_cast<int64_t>(hk) * a.page_tokens * HD +
-                                        static_cast<int64_t>(key % a.page_tokens) * HD + c * 8;
-            cp_async16(&sK[buf][r * LD + c * 8], base, ok);
-            cp_async16(&sV[buf][r * LD + c * 8], base + a.kv_stride, ok);
+            const __nv_bfloat16* src = kv_layer + static_cast<int64_t>(page) * a.page_stride +
+                                       static_cast<int64_t>(hk) * a.page_tokens * HD +
+                                       static_cast<int64_t>(key % a.page_tokens) * HD + c * 8;
+            cp_async16(wK + buf * KB * HD + swz<HD>(kr, c), src, ok);
+            cp_async16(wV + buf * KB * HD + swz<HD>(kr, c), src + a.kv_stride, ok);
         }
     };
 
-    // thread roles: scores -> key = tid % 64, heads [hq0, hq0 + G/2) (G even) ;
-    // output -> (g, d) pairs strided over the block.
-    constexpr int HPT = G >= 2 ? G / 2 : 1;
-    const int skey = tid & 63;
-    const int hq0 = (tid >> 6) * HPT;
-    constexpr int OUT_PER_T = (G * HD) / 128;
-    float acc[OUT_PER_T];
+    float o[HD / 8][4];
 #pragma unroll
-    for (int j = 0; j < OUT_PER_T; ++j) acc[j] = 0.f;
-    float m_run = -INFINITY, l_run = 0.f;  // owned by warp g < G (lane 0 copy kept by every lane)
+    for (int i = 0; i < HD / 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+    float m_run = -INFINITY, l_run = 0.f;  // row r (c0/c1); rows r+8 are padding
 
-    const int n_steps = cdiv(k_end - k_begin, kDecKeys);
-    load(k_begin, 0);
-    cp_async_commit();
-    __syncthreads();  // sQ ready
-    for (int st = 0; st < n_steps; ++st) {
-        const int buf = st & 1;
-        if (st + 1 < n_steps) {
-            load(k_begin + (st + 1) * kDecKeys, buf ^ 1);
+    int it = 0;
+    if (warp < n_blocks) {
+        load(warp, 0);
+        cp_async_commit();
+    }
+    for (int blk = warp; blk < n_blocks; blk += 4, ++it) {
+        const int buf = it & 1;
+        if (blk + 4 < n_blocks) {
+            load(blk + 4, buf ^ 1);
             cp_async_commit();
             cp_async_wait<1>();
         } else {
             cp_async_wait<0>();
         }
-        __syncthreads();
-        const int kbase = k_begin + st * kDecKeys;
-        // scores
-        if (tid < 64 * (G / HPT)) {
-            float dot[HPT];
+        __syncwarp();
+        const __nv_bfloat16* K = wK + buf * KB * HD;
+        const __nv_bfloat16* V = wV + buf * KB * HD;
+        float sc[KB / 8][4];
 #pragma unroll
-            for (int j = 0; j < HPT; ++j) dot[j] = 0.f;
-            const uint4* kr = reinterpret_cast<const uint4*>(&sK[buf][skey * LD]);
-#pragma unroll 4
-            for (int c = 0; c < CH; ++c) {
-                const uint4 kv = kr[c];
-                const float k8[8] = {bf_lo(kv.x), bf_hi(kv.x), bf_lo(kv.y), bf_hi(kv.y),
-                                     bf_lo(kv.z), bf_hi(kv.z), bf_lo(kv.w), bf_hi(kv.w)};
+        for (int nb = 0; nb < KB / 8; ++nb) sc[nb][0] = sc[nb][1] = sc[nb][2] = sc[nb][3] = 0.f;
 #pragma unroll
-                for (int j = 0; j < HPT; ++j) {
-                    const float4 qa = *reinterpret_cast<const float4*>(&sQ[(hq0 + j) * HD + c * 8]);
-                    const float4 qb = *reinterpret_cast<const float4*>(&sQ[(hq0 + j) * HD + c * 8 + 4]);
-                    dot[j] += qa.x * k8[0] + qa.y * k8[1] + qa.z * k8[2] + qa.w * k8[3] + qb.x * k8[4] +
-                              qb.y * k8[5] + qb.z * k8[6] + qb.w * k8[7];
-                }
+        for (int ks = 0; ks < HD / 16; ++ks) {
+#pragma unroll
+            for (int np = 0; np < KB / 16; ++np) {
+                uint32_t b[4];
+                const int key = np * 16 + (lane & 7) + ((lane >> 4) << 3);
+                const int c = ks * 2 + ((lane >> 3) & 1);
+                ldsm_x4(b, K + swz<HD>(key, c));
+                mma_bf16(sc[2 * np], qf[ks], b[0], b[1]);
+                mma_bf16(sc[2 * np + 1], qf[ks], b[2], b[3]);
             }
+        }
+        const int kbase = k_begin + blk * KB;
+        float mx = -INFINITY;
 #pragma unroll
-            for (int j = 0; j < HPT; ++j) sS[hq0 + j][skey] = kbase + skey < k_end ? dot[j] : -INFINITY;
-        }
-        __syncthreads();
-        // softmax bookkeeping: warp g owns head g
-        if (warp < G) {
-            const float s0 = sS[warp][lane], s1 = sS[warp][lane + 32];
-            const float mx = warp_max(fmaxf(s0, s1));
-            const float m_new = fmaxf(m_run, mx);
-            const float alpha = exp2f(m_run - m_new);  // m_new finite: key k_begin is always valid
-            const float p0 = exp2f(s0 - m_new), p1 = exp2f(s1 - m_new);
-            sS[warp][lane] = p0;
-            sS[warp][lane + 32] = p1;
-            l_run = l_run * alpha + warp_sum(p0 + p1);
-            m_run = m_new;
-            if (lane == 0) sAlpha[warp] = alpha;
-        }
-        __syncthreads();
-        // O += P V
+        for (int nb = 0; nb < KB / 8; ++nb)
 #pragma unroll
-        for (int j = 0; j < OUT_PER_T; ++j) {
-            const int idx = j * 128 + tid;
-            const int g = idx / HD, d = idx % HD;
-            float v = acc[j] * sAlpha[g];
-            const float* p = sS[g];
-#pragma unroll 8
-            for (int k = 0; k < kDecKeys; ++k) v += p[k] * bf2f(sV[buf][k * LD + d]);
-            acc[j] = v;
+            for (int e = 0; e < 2; ++e) {
+                const int key = kbase + nb * 8 + (lane & 3) * 2 + e;
+                const float v = key < k_end ? sc[nb][e] * a.scale_log2 : -INFINITY;
+                sc[nb][e] = v;
+                mx = fmaxf(mx, v);
+            }
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+        const float m_new = fmaxf(m_run, mx);  // finite: the block's first key is valid
+        const float alpha = exp2f(m_run - m_new);
+        m_run = m_new;
+        float rs = 0.f;
+#pragma unroll
+        for (int nb = 0; nb < KB / 8; ++nb) {
+            sc[nb][0] = exp2f(sc[nb][0] - m_new);
+            sc[nb][1] = exp2f(sc[nb][1] - m_new);
+            sc[nb][2] = sc[nb][3] = 0.f;  // padding rows
+            rs += sc[nb][0] + sc[nb][1];
         }
-        __syncthreads();
+        l_run = l_run * alpha + rs;
+#pragma unroll
+        for (int i = 0; i < HD / 8; ++i) {
+            o[i][0] *= alpha;
+            o[i][1] *= alpha;
+        }
+#pragma unroll
+        for (int kk = 0; kk < KB / 16; ++kk) {
+            uint32_t pa[4];
+            pa[0] = pack_bf2(sc[2 * kk][0], sc[2 * kk][1]);
+            pa[1] = 0u;
+            pa[2] = pack_bf2(sc[2 * kk + 1][0], sc[2 * kk + 1][1]);
+            pa[3] = 0u;
+#pragma unroll
+            for (int dp = 0; dp < HD / 16; ++dp) {
+                uint32_t b[4];
+                const int key = kk * 16 + (lane & 7) + (((lane >> 3) & 1) << 3);
+                const int c = dp * 2 + (lane >> 4);
+                ldsm_x4_t(b, V + swz<HD>(key, c));
+                mma_bf16(o[2 * dp], pa, b[0], b[1]);
+                mma_bf16(o[2 * dp + 1], pa, b[2], b[3]);
+            }
+        }
+        __syncwarp();
     }
-    // partials: [row][hk][split][G][HD] and (m, l)
-    const int64_t pidx = (static_cast<int64_t>(row) * a.Hkv + hk) * a.max_splits + blockIdx.x;
-    float* po = a.part_o + pidx * G * HD;
+    l_run += __shfl_xor_sync(0xffffffffu, l_run, 1);
+    l_run += __shfl_xor_sync(0xffffffffu, l_run, 2);
+    // ---- merge the 4 warps
+    if (r < G) {
+        if ((lane & 3) == 0) {
+            cm[warp * G + r] = m_run;
+            cl[warp * G + r] = l_run;
+        }
 #pragma unroll
-    for (int j = 0; j < OUT_PER_T; ++j) po[j * 128 + tid] = acc[j];
-    if (warp < G && lane == 0) {
-        a.part_ml[(pidx * G + warp) * 2 + 0] = m_run;
-        a.part_ml[(pidx * G + warp) * 2 + 1] = l_run;
+        for (int i = 0; i < HD / 8; ++i) {
+            float* dst = co + (warp * G + r) * HD + i * 8 + (lane & 3) * 2;
+            dst[0] = o[i][0];
+            dst[1] = o[i][1];
+        }
     }
-}
-
-template <int HD>
-__global__ void attn_decode_combine_kernel(DecodeAttnArgs a, __nv_bfloat16* __restrict__ out, int G) {
-    const int row = blockIdx.y;
-    if (row >= a.meta->n) return;
-    const int h = blockIdx.x;
-    const int hk = h / G, g = h % G;
-    const int ctx = a.meta->pos[row] + 1;
-    const int splits = cdiv(ctx, a.chunk);
+    __syncthreads();
+    const int64_t pidx = (static_cast<int64_t>(row) * a.Hkv + hk) * a.max_splits + split;
+    for (int idx = threadIdx.x; idx < G * HD; idx += 128) {
+        const int g = idx / HD, d = idx % HD;
+        float M = -INFINITY;
+#pragma unroll
+        for (int w = 0; w < 4; ++w) M = fmaxf(M, cm[w * G + g]);
+        float L = 0.f, O = 0.f;
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+            const float sc_w = cm[w * G + g] == -INFINITY ? 0.f : exp2f(cm[w * G + g] - M);
+            L += cl[w * G + g] * sc_w;
+            O += co[(w * G + g) * HD + d] * sc_w;
+        }
+        if (splits == 1) {
+            out[static_cast<int64_t>(row) * a.H * HD + (hk * G + g) * HD + d] = __float2bfloat16_rn(O / L);
+        } else {
+            __stcg(a.part_o + pidx * G * HD + idx, O);
+            if (d == 0) {
+                __stcg(a.part_ml + (pidx * G + g) * 2, M);
+                __stcg(a.part_ml + (pidx * G + g) * 2 + 1, L);
+            }
+        }
+    }
+    if (splits == 1) return;
+    // ---- last split to arrive merges all splits in order
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned* cnt = a.counters + static_cast<int64_t>(row) * a.Hkv + hk;
+        s_last = atomicAdd(cnt, 1u) == static_cast<unsigned>(splits - 1);
+        if (s_last) *cnt = 0u;
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
     const int64_t base = (static_cast<int64_t>(row) * a.Hkv + hk) * a.max_splits;
-    float m = -INFINITY;
-    for (int s = 0; s < splits; ++s) m = fmaxf(m, a.part_ml[((base + s) * G + g) * 2]);
-    float l = 0.f;
-    for (int s = 0; s < splits; ++s) l += a.part_ml[((base + s) * G + g) * 2 + 1] * exp2f(a.part_ml[((base + s) * G + g) * 2] - m);
-    const float inv = 1.f / l;
-    for (int d = threadIdx.x; d < HD; d += blockDim.x) {
-        float v = 0.f;
-        for (int s = 0; s < splits; ++s)
-            v += a.part_o[((base + s) * G + g) * HD + d] * exp2f(a.part_ml[((base + s) * G + g) * 2] - m);
-        out[static_cast<int64_t>(row) * a.H * HD + h * HD + d] = __float2bfloat16_rn(v * inv);
+    for (int idx = threadIdx.x; idx < G * HD; idx += 128) {
+        const int g = idx / HD;
+        float M = -INFINITY;
+        for (int sp = 0; sp < splits; ++sp) M = fmaxf(M, __ldcg(a.part_ml + ((base + sp) * G + g) * 2));
+        float L = 0.f, O = 0.f;
+        for (int sp = 0; sp < splits; ++sp) {
+            const float w = exp2f(__ldcg(a.part_ml + ((base + sp) * G + g) * 2) - M);
+            L += __ldcg(a.part_ml + ((base + sp) * G + g) * 2 + 1) * w;
+            O += __ldcg(a.part_o + (base + sp) * G * HD + idx) * w;
+        }
+        out[static_cast<int64_t>(row) * a.H * HD + (hk * G) * HD + idx] = __float2bfloat16_rn(O / L);
     }
 }
 
 template <int HD, int G>
 void decode_launch(const __nv_bfloat16* q, const __nv_bfloat16* kv_layer, __nv_bfloat16* out, const DecodeAttnArgs& a,
                    int max_rows, cudaStream_t st) {
-    dim3 grid(a.max_splits, a.Hkv, max_rows);
-    constexpr int smem = 4 * kDecKeys * (HD + kPad) * 2 + (G * HD + G * kDecKeys + G) * 4;
+    constexpr int KB = HD <= 64 ? 32 : 16;
+    constexpr int smem = 4 * (4 * KB * HD) * 2 + (8 * G + 4 * G * HD) * 4;
     static bool cfg = false;
     if (!cfg) {
-        SW_CUDA(cudaFuncSetAttribute(attn_decode_kernel<HD, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        SW_CUDA(cudaFuncSetAttribute(attn_decode_kernel<HD, G, KB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         cfg = true;
     }
-    attn_decode_kernel<HD, G><<<grid, 128, smem, st>>>(q, kv_layer, a);
-    SW_LAUNCH_CHECK();
-    attn_decode_combine_kernel<HD><<<dim3(a.H, max_rows), HD, 0, st>>>(a, out, G);
+    dim3 grid(a.max_splits, a.Hkv, max_rows);
+    attn_decode_kernel<HD, G, KB><<<grid, 128, smem, st>>>(q, kv_layer, out, a);
     SW_LAUNCH_CHECK();
 }
 

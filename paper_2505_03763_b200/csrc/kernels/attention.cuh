@@ -38,6 +38,7 @@ struct DecodeAttnArgs {
     int max_splits;  // grid x; splits past the context exit
     float* part_o;   // [rows][Hkv][max_splits][G][hd]
     float* part_ml;  // [rows][Hkv][max_splits][G][2]
+    unsigned* counters;  // [rows][Hkv] split arrivals, zero between launches
 };
 
 void attn_prefill(const __nv_bfloat16* q, const __nv_bfloat16* kv_layer, __nv_bfloat16* out, const PrefillAttnArgs& a,

@@ -1,6 +1,8 @@
 // HBM-bound helper kernels of both phases: synthetic weight init, embedding
 // gather (+ page-table install for decode), RMSNorm, RoPE + paged-KV scatter,
 // and the greedy-token finalize that follows the LM-head argmax GEMM.
+#include <algorithm>
+
 #include "common.cuh"
 #include "elementwise.cuh"
 
@@ -102,41 +104,60 @@ void embed_tokens(const int32_t* tokens, const int* n_tokens_dev, int rows, cons
 }
 
 // ---------------------------------------------------------------- RMSNorm
-// One warp per row; fp32 statistics, bf16 output feeding the next GEMM.
+// One CTA per row, the row held in registers (VPT float4 per thread): one HBM
+// read of x, fp32 statistics, bf16 output feeding the next GEMM.
 // `rows_dev` (optional) bounds the live rows at run time (graph-safe);
 // `row_index` (optional) gathers rows (LM head on the last prompt position).
+template <int VPT>
 __global__ void rmsnorm_kernel(const float* __restrict__ x, const __nv_bfloat16* __restrict__ g,
-                               __nv_bfloat16* __restrict__ y, int rows, int d, float eps, const int* rows_dev,
+                               __nv_bfloat16* __restrict__ y, int d, float eps, const int* rows_dev,
                                const int32_t* __restrict__ row_index) {
-    const int warps = blockDim.x >> 5;
-    const int row = blockIdx.x * warps + (threadIdx.x >> 5);
-    const int lane = threadIdx.x & 31;
-    const int live = rows_dev ? *rows_dev : rows;
-    if (row >= rows || row >= live) return;
+    const int row = blockIdx.x;
+    if (rows_dev && row >= *rows_dev) return;
     const int src_row = row_index ? row_index[row] : row;
     const float4* xr = reinterpret_cast<const float4*>(x + static_cast<int64_t>(src_row) * d);
+    float4 v[VPT];
     float ss = 0.f;
-    for (int i = lane; i < d / 4; i += 32) {
-        const float4 v = xr[i];
-        ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+#pragma unroll
+    for (int k = 0; k < VPT; ++k) {
+        const int i = threadIdx.x + k * blockDim.x;
+        v[k] = i < d / 4 ? xr[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+        ss += v[k].x * v[k].x + v[k].y * v[k].y + v[k].z * v[k].z + v[k].w * v[k].w;
     }
+    __shared__ float red[32];
     ss = warp_sum(ss);
-    const float inv = rsqrtf(ss / static_cast<float>(d) + eps);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        float t = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
+        t = warp_sum(t);
+        if (threadIdx.x == 0) red[0] = t;
+    }
+    __syncthreads();
+    const float inv = rsqrtf(red[0] / static_cast<float>(d) + eps);
     const uint2* g2 = reinterpret_cast<const uint2*>(g);
     uint2* y2 = reinterpret_cast<uint2*>(y + static_cast<int64_t>(row) * d);
-    for (int i = lane; i < d / 4; i += 32) {
-        const float4 v = xr[i];
+#pragma unroll
+    for (int k = 0; k < VPT; ++k) {
+        const int i = threadIdx.x + k * blockDim.x;
+        if (i >= d / 4) break;
         const uint2 gg = g2[i];
         uint2 o;
-        o.x = pack_bf2(v.x * inv * bf_lo(gg.x), v.y * inv * bf_hi(gg.x));
-        o.y = pack_bf2(v.z * inv * bf_lo(gg.y), v.w * inv * bf_hi(gg.y));
+        o.x = pack_bf2(v[k].x * inv * bf_lo(gg.x), v[k].y * inv * bf_hi(gg.x));
+        o.y = pack_bf2(v[k].z * inv * bf_lo(gg.y), v[k].w * inv * bf_hi(gg.y));
         y2[i] = o;
     }
 }
 
 void rmsnorm(const float* x, const __nv_bfloat16* g, __nv_bfloat16* y, int rows, int d, float eps, const int* rows_dev,
              const int32_t* row_index, cudaStream_t st) {
-    rmsnorm_kernel<<<cdiv(rows, 8), 256, 0, st>>>(x, g, y, rows, d, eps, rows_dev, row_index);
+    const int threads = std::min(256, std::max(32, d / 4));
+    const int vpt = cdiv(d / 4, threads);
+    if (vpt <= 1) rmsnorm_kernel<1><<<rows, threads, 0, st>>>(x, g, y, d, eps, rows_dev, row_index);
+    else if (vpt <= 2) rmsnorm_kernel<2><<<rows, threads, 0, st>>>(x, g, y, d, eps, rows_dev, row_index);
+    else if (vpt <= 4) rmsnorm_kernel<4><<<rows, threads, 0, st>>>(x, g, y, d, eps, rows_dev, row_index);
+    else if (vpt <= 8) rmsnorm_kernel<8><<<rows, threads, 0, st>>>(x, g, y, d, eps, rows_dev, row_index);
+    else throw_cuda("rmsnorm: d_model too large", cudaErrorInvalidValue, __FILE__, __LINE__);
     SW_LAUNCH_CHECK();
 }
 
@@ -145,10 +166,27 @@ void rmsnorm(const float* x, const __nv_bfloat16* g, __nv_bfloat16* y, int rows,
 // bf16 once, after the rotation) -> q [T, H*hd] roped, and K (roped)
 // / V scattered into the paged cache of layer `layer`:
 //   pages[layer][page][kv][head][page_tokens][hd],  page = table[slot][pos / B].
+// cos/sin of pos * inv_freq[i] for every position < max_pos: the same fp32
+// angle and sincosf as computing it inline, evaluated once per model.
+__global__ void rope_table_kernel(const float* __restrict__ inv_freq, float2* __restrict__ table, int max_pos,
+                                  int half) {
+    const int64_t n = static_cast<int64_t>(max_pos) * half;
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+        const int pos = static_cast<int>(k / half), i = static_cast<int>(k % half);
+        float s, c;
+        sincosf(static_cast<float>(pos) * inv_freq[i], &s, &c);
+        table[k] = make_float2(c, s);
+    }
+}
+void rope_table(const float* inv_freq, float2* table, int max_pos, int half, cudaStream_t st) {
+    rope_table_kernel<<<148 * 4, 256, 0, st>>>(inv_freq, table, max_pos, half);
+    SW_LAUNCH_CHECK();
+}
+
 __global__ void rope_kv_kernel(const float* __restrict__ qkv, __nv_bfloat16* __restrict__ q_out,
                                __nv_bfloat16* __restrict__ kv_layer, const int32_t* __restrict__ tok_pos,
                                const int32_t* __restrict__ tok_slot, const int32_t* __restrict__ page_table,
-                               const float* __restrict__ inv_freq, int rows, const int* rows_dev, int H, int Hkv,
+                               const float2* __restrict__ cs_table, int rows, const int* rows_dev, int H, int Hkv,
                                int hd, int max_pages, int page_tokens, int64_t page_stride) {
     const int t = blockIdx.x;
     const int live = rows_dev ? *rows_dev : rows;
@@ -166,8 +204,8 @@ __global__ void rope_kv_kernel(const float* __restrict__ qkv, __nv_bfloat16* __r
     // (head, i) pairs over q and k heads: rotate; v heads: copy.
     for (int idx = threadIdx.x; idx < (H + Hkv) * half; idx += blockDim.x) {
         const int h = idx / half, i = idx % half;
-        float s, c;
-        sincosf(static_cast<float>(pos) * inv_freq[i], &s, &c);
+        const float2 cs = cs_table[static_cast<int64_t>(pos) * half + i];
+        const float c = cs.x, s = cs.y;
         const float a = src[h * hd + i], b = src[h * hd + i + half];
         const __nv_bfloat16 ra = __float2bfloat16_rn(a * c - b * s);
         const __nv_bfloat16 rb = __float2bfloat16_rn(b * c + a * s);
@@ -188,10 +226,10 @@ __global__ void rope_kv_kernel(const float* __restrict__ qkv, __nv_bfloat16* __r
 }
 
 void rope_kv(const float* qkv, __nv_bfloat16* q_out, __nv_bfloat16* kv_layer, const int32_t* tok_pos,
-             const int32_t* tok_slot, const int32_t* page_table, const float* inv_freq, int rows, const int* rows_dev,
+             const int32_t* tok_slot, const int32_t* page_table, const float2* cs_table, int rows, const int* rows_dev,
              int H, int Hkv, int hd, int max_pages, int page_tokens, cudaStream_t st) {
     const int64_t page_stride = 2LL * Hkv * page_tokens * hd;
-    rope_kv_kernel<<<rows, 256, 0, st>>>(qkv, q_out, kv_layer, tok_pos, tok_slot, page_table, inv_freq, rows,
+    rope_kv_kernel<<<rows, 256, 0, st>>>(qkv, q_out, kv_layer, tok_pos, tok_slot, page_table, cs_table, rows,
                                          rows_dev, H, Hkv, hd, max_pages, page_tokens, page_stride);
     SW_LAUNCH_CHECK();
 }

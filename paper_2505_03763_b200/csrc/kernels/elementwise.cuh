@@ -34,8 +34,9 @@ void embed_tokens(const int32_t* tokens, const int* n_tokens_dev, int rows, cons
                   cudaStream_t st);
 void rmsnorm(const float* x, const __nv_bfloat16* g, __nv_bfloat16* y, int rows, int d, float eps, const int* rows_dev,
              const int32_t* row_index, cudaStream_t st);
+void rope_table(const float* inv_freq, float2* table, int max_pos, int half, cudaStream_t st);
 void rope_kv(const float* qkv, __nv_bfloat16* q_out, __nv_bfloat16* kv_layer, const int32_t* tok_pos,
-             const int32_t* tok_slot, const int32_t* page_table, const float* inv_freq, int rows, const int* rows_dev,
+             const int32_t* tok_slot, const int32_t* page_table, const float2* cs_table, int rows, const int* rows_dev,
              int H, int Hkv, int hd, int max_pages, int page_tokens, cudaStream_t st);
 void finalize_tokens(unsigned long long* keys, const int32_t* slot, const int32_t* out_index, int rows,
                      const int* rows_dev, int32_t* last_token, int32_t* out_tokens, int max_out, cudaStream_t st);

@@ -20,6 +20,7 @@
 // 64-bit atomicMax per token: LM head + greedy sampling in one pass).
 #include <cuda.h>
 
+#include <algorithm>
 #include <map>
 #include <mutex>
 #include <tuple>
@@ -35,12 +36,14 @@ constexpr int BM = 128;
 constexpr int BK = 64;
 constexpr int kThreads = 192;
 
-template <int BN>
+template <int BN, bool SWAP>
 struct GemmCfg {
     static constexpr int kABytes = BM * BK * 2;
     static constexpr int kBBytes = BN * BK * 2;
     static constexpr int kStageBytes = kABytes + kBBytes;
-    static constexpr int kStages = (200 * 1024) / kStageBytes > 8 ? 8 : (200 * 1024) / kStageBytes;
+    // decode (swap) tiles: ~100 KB so two CTAs stream weights per SM
+    static constexpr int kBudget = (SWAP && BN <= 64) ? 100 * 1024 : 200 * 1024;
+    static constexpr int kStages = kBudget / kStageBytes > 8 ? 8 : kBudget / kStageBytes;
     static constexpr int kTmemCols = BN < 32 ? 32 : BN;
     static constexpr int kXchgBytes = 64 * 33 * 4;  // SwiGLU swap-mode exchange
     static constexpr int kSmem = 1024 + kStages * kStageBytes + kXchgBytes + 256;
@@ -51,7 +54,7 @@ __device__ __forceinline__ float silu_mul(float g, float u) { return g / (1.0f +
 template <int BN, int MODE, bool SWAP>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmArgs args) {
-    using C = GemmCfg<BN>;
+    using C = GemmCfg<BN, SWAP>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sA = smem;
@@ -66,7 +69,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int lane = threadIdx.x & 31;
     const int m0 = blockIdx.y * BM;
     const int n0 = blockIdx.x * BN;
-    const int nk = args.K / BK;
+    // split-K: this CTA owns K-blocks [kb0, kb1)
+    const int nk_total = args.K / BK;
+    const int kb0 = static_cast<int>(blockIdx.z) * nk_total / static_cast<int>(gridDim.z);
+    const int kb1 = (static_cast<int>(blockIdx.z) + 1) * nk_total / static_cast<int>(gridDim.z);
+    const int nk = kb1 - kb0;
 
     if (warp == 0 && lane == 0) {
         for (int s = 0; s < C::kStages; ++s) {
@@ -100,8 +107,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const uint32_t ph = (kb / C::kStages) & 1;
                 mbar_wait(&empty[s], ph ^ 1);
                 mbar_expect_tx(&full[s], C::kStageBytes);
-                tma_load_2d(sA + s * C::kABytes, &tmA, &full[s], kb * BK, m0, pol_a);
-                tma_load_2d(sB + s * C::kBBytes, &tmB, &full[s], kb * BK, n0, pol_b);
+                tma_load_2d(sA + s * C::kABytes, &tmA, &full[s], (kb0 + kb) * BK, m0, pol_a);
+                tma_load_2d(sB + s * C::kBBytes, &tmB, &full[s], (kb0 + kb) * BK, n0, pol_b);
             }
         }
         __syncwarp();
@@ -207,41 +214,37 @@ __global__ void __launch_bounds__(kThreads, 1)
         } else {
             // row = feature (weight row), columns = tokens
             const int f = m0 + row;
-            for (int c = 0; c < BN; c += 32) {
-                tmem_ld32(tbase + c, r);
-                tmem_ld_wait();
+            auto emit = [&](int c, const uint32_t (&v)[32]) {
                 const int tcount = min(32, n_live - (n0 + c));
                 if constexpr (MODE == EPI_STORE) {
                     _Pragma("unroll") for (int j = 0; j < 32; ++j) if (j < tcount)
                         static_cast<__nv_bfloat16*>(args.out)[static_cast<size_t>(n0 + c + j) * args.ldo + f] =
-                            __float2bfloat16_rn(__uint_as_float(r[j]));
+                            __float2bfloat16_rn(__uint_as_float(v[j]));
                 } else if constexpr (MODE == EPI_STORE_F32) {
                     _Pragma("unroll") for (int j = 0; j < 32; ++j) if (j < tcount)
                         static_cast<float*>(args.out)[static_cast<size_t>(n0 + c + j) * args.ldo + f] =
-                            __uint_as_float(r[j]);
+                            __uint_as_float(v[j]);
                 } else if constexpr (MODE == EPI_RESID) {
                     _Pragma("unroll") for (int j = 0; j < 32; ++j) if (j < tcount)
                         static_cast<float*>(args.out)[static_cast<size_t>(n0 + c + j) * args.ldo + f] +=
-                            __uint_as_float(r[j]);
+                            __uint_as_float(v[j]);
                 } else if constexpr (MODE == EPI_SWIGLU) {
                     // lanes 0-63 of the tile hold gate rows, 64-127 the matching up rows
-                    const int ew = threadIdx.x - 64;  // 0..127 over the epilogue warps
-                    (void)ew;
                     if (row >= 64) {
 #pragma unroll
-                        for (int j = 0; j < 32; ++j) xchg[(row - 64) * 33 + j] = __uint_as_float(r[j]);
+                        for (int j = 0; j < 32; ++j) xchg[(row - 64) * 33 + j] = __uint_as_float(v[j]);
                     }
                     asm volatile("bar.sync 1, 128;" ::: "memory");
                     if (row < 64) {
                         const int g = m0 / 2 + row;
                         _Pragma("unroll") for (int j = 0; j < 32; ++j) if (j < tcount)
                             static_cast<__nv_bfloat16*>(args.out)[static_cast<size_t>(n0 + c + j) * args.ldo + g] =
-                                __float2bfloat16_rn(silu_mul(__uint_as_float(r[j]), xchg[row * 33 + j]));
+                                __float2bfloat16_rn(silu_mul(__uint_as_float(v[j]), xchg[row * 33 + j]));
                     }
                     asm volatile("bar.sync 1, 128;" ::: "memory");
                 } else if constexpr (MODE == EPI_ARGMAX) {
                     _Pragma("unroll") for (int j = 0; j < 32; ++j) if (j < tcount) {
-                        unsigned long long key = argmax_key(__uint_as_float(r[j]),
+                        unsigned long long key = argmax_key(__uint_as_float(v[j]),
                                                             static_cast<uint32_t>(args.feature_offset + f));
 #pragma unroll
                         for (int o = 16; o > 0; o >>= 1) {
@@ -250,6 +253,51 @@ __global__ void __launch_bounds__(kThreads, 1)
                         }
                         if (lane == 0) atomicMax(args.argmax + n0 + c + j, key);
                     }
+                }
+            };
+            if (gridDim.z == 1) {
+                for (int c = 0; c < BN; c += 32) {
+                    tmem_ld32(tbase + c, r);
+                    tmem_ld_wait();
+                    emit(c, r);
+                }
+            } else {
+                // Split-K: park this CTA's fp32 partial tile in the (L2-resident)
+                // workspace; the last CTA of the tile to finish reduces all
+                // partials in split order (deterministic) and runs the epilogue.
+                const int tile = blockIdx.y * gridDim.x + blockIdx.x;
+                const int splits = gridDim.z;
+                float* part = args.ws + static_cast<size_t>(tile) * splits * BN * 128;
+                for (int c = 0; c < BN; c += 32) {
+                    tmem_ld32(tbase + c, r);
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int j = 0; j < 32; ++j)
+                        __stcg(part + (static_cast<size_t>(blockIdx.z) * BN + c + j) * 128 + row, __uint_as_float(r[j]));
+                }
+                __threadfence();
+                asm volatile("bar.sync 2, 128;" ::: "memory");
+                uint32_t* last_flag = reinterpret_cast<uint32_t*>(tmem_slot + 1);
+                if (threadIdx.x == 64) {
+                    const unsigned prev = atomicAdd(args.counters + tile, 1u);
+                    *last_flag = prev == static_cast<unsigned>(splits - 1);
+                }
+                asm volatile("bar.sync 2, 128;" ::: "memory");
+                if (*last_flag) {
+                    __threadfence();
+                    for (int c = 0; c < BN; c += 32) {
+                        float acc[32];
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) acc[j] = 0.f;
+                        for (int z = 0; z < splits; ++z)
+#pragma unroll
+                            for (int j = 0; j < 32; ++j)
+                                acc[j] += __ldcg(part + (static_cast<size_t>(z) * BN + c + j) * 128 + row);
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) r[j] = __float_as_uint(acc[j]);
+                        emit(c, r);
+                    }
+                    if (threadIdx.x == 64) args.counters[tile] = 0u;  // re-arm for the next launch
                 }
             }
         }
@@ -280,14 +328,14 @@ EncodeTiled encode_fn() {
 
 template <int BN, int MODE, bool SWAP>
 void launch_one(const CUtensorMap& a, const CUtensorMap& b, const GemmArgs& args, cudaStream_t st) {
-    using C = GemmCfg<BN>;
+    using C = GemmCfg<BN, SWAP>;
     static bool configured = false;  // per instantiation
     if (!configured) {
         SW_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<BN, MODE, SWAP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      C::kSmem));
         configured = true;
     }
-    dim3 grid(args.N / BN, cdiv(args.M, BM));
+    dim3 grid(args.N / BN, cdiv(args.M, BM), args.splits > 0 ? args.splits : 1);
     gemm_tc_kernel<BN, MODE, SWAP><<<grid, kThreads, C::kSmem, st>>>(a, b, args);
     SW_LAUNCH_CHECK();
 }
@@ -346,7 +394,21 @@ void gemm_run(const GemmProblem& p, cudaStream_t st) {
     a.feature_offset = p.feature_offset;
     a.valid_tokens = p.tokens;
     a.live_tokens = p.live_tokens;
+    a.splits = 1;
+    a.ws = p.ws;
+    a.counters = p.counters;
     if (p.swap) {
+        // split-K from the weight shape only (never the batch), so results are
+        // identical for every batch size: ~2 CTAs per SM of weight streams,
+        // >= 4 K-blocks per split.
+        if (p.ws && p.counters && p.mode != EPI_ARGMAX) {
+            const int tiles = p.features / BM, nk = p.K / BK;
+            int sp = std::max(1, 296 / tiles);
+            sp = std::min(sp, nk / 4);
+            sp = std::min(sp, 16);
+            a.splits = std::max(sp, 1);
+            if (static_cast<size_t>(tiles) * a.splits * 256 * 128 > p.ws_floats || tiles > p.n_counters) a.splits = 1;
+        }
         if (p.features % BM != 0)
             throw_cuda("gemm(swap): feature count must be a multiple of 128", cudaErrorInvalidValue, __FILE__, __LINE__);
         if (p.tokens > 256) throw_cuda("gemm(swap): at most 256 tokens", cudaErrorInvalidValue, __FILE__, __LINE__);

@@ -18,6 +18,9 @@ struct GemmArgs {
     const int* live_tokens;  // optional device bound (graph-captured decode)
     unsigned long long* argmax;
     int feature_offset;
+    int splits;          // split-K factor (grid z)
+    float* ws;           // split-K partial tiles [tiles][splits][BN][128]
+    unsigned* counters;  // split-K arrival counters [tiles], zero between launches
 };
 
 // Y[t, f] = sum_k X[t, k] W[f, k] over `tokens` rows of X and `features` rows of W.
@@ -36,6 +39,11 @@ struct GemmProblem {
     int ldo;
     unsigned long long* argmax;  // ARGMAX: packed key per token
     int feature_offset;          // ARGMAX: index of W row 0 in the full vocabulary
+    // optional split-K scratch (swap mode): enables split-K when present
+    float* ws = nullptr;
+    size_t ws_floats = 0;
+    unsigned* counters = nullptr;
+    int n_counters = 0;
 };
 
 CUtensorMap make_tmap_bf16(const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows);
