@@ -550,10 +550,9 @@ extern "C" int sw_kv_arena_create(sw_model* m, int64_t n_pages, int32_t n_slots,
         SW_CUDA(cudaMemset(kv->last_token, 0, static_cast<size_t>(n_slots) * 4));
         kv->out_tokens = dalloc<int32_t>(static_cast<size_t>(n_slots) * max_out_tokens);
         SW_CUDA(cudaMemset(kv->out_tokens, 0xff, static_cast<size_t>(n_slots) * max_out_tokens * 4));
-        // split-KV geometry: at most 16 splits of >= 256 keys (multiple of 64)
-        const int max_ctx = max_pages_per_slot * kv->page_tokens;
-        kv->chunk = std::max(256, (cdiv(max_ctx, 16) + 63) / 64 * 64);
-        kv->max_splits = cdiv(max_ctx, kv->chunk);
+        // split-KV: the kernel picks 1..16 splits per launch (grid x = 16)
+        kv->chunk = 0;
+        kv->max_splits = 16;
         *out = kv.release();
     });
 }

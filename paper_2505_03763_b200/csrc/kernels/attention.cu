@@ -53,6 +53,7 @@ __device__ __forceinline__ int swz(int row, int chunk) {
 
 constexpr int kQRows = 64;
 constexpr int kKeys = 64;
+constexpr int kMaxChunkPages = 2048;  // page ids of one decode split staged in smem
 
 template <int HD>
 __global__ void __launch_bounds__(128) attn_prefill_kernel(const __nv_bfloat16* __restrict__ q,
@@ -252,16 +253,29 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(const __nv_bfloat16* _
     float* co = cl + 4 * G;                                             // [4][G][HD]
     __shared__ uint32_t s_last;
 
+    __shared__ int32_t s_pages[kMaxChunkPages];
+    const int n_rows = a.meta->n;
     const int row = blockIdx.z;
-    if (row >= a.meta->n) return;
+    if (row >= n_rows) return;
     const int ctx = a.meta->pos[row] + 1;
-    const int splits = cdiv(ctx, a.chunk);
+    // splits chosen at run time: only as many as it takes to give the GPU
+    // ~4 CTAs per SM, each warp keeping >= 1 key block
+    const int want = cdiv(148 * 4, n_rows * a.Hkv);
+    const int splits0 = max(1, min(min(want, a.max_splits), cdiv(ctx, 4 * KB)));
+    const int chunk = cdiv(cdiv(ctx, splits0), KB) * KB;
+    const int splits = cdiv(ctx, chunk);  // every split non-empty
     const int split = blockIdx.x;
     if (split >= splits) return;
-    const int k_begin = split * a.chunk;
-    const int k_end = min(ctx, k_begin + a.chunk);
+    const int k_begin = split * chunk;
+    const int k_end = min(ctx, k_begin + chunk);
+    if (k_begin >= k_end) return;
     const int hk = blockIdx.y;
-    const int32_t* ptab = a.page_table + static_cast<int64_t>(a.meta->slot[row]) * a.max_pages;
+    {  // this split's page ids -> smem (one read per page, not per 16 B chunk)
+        const int32_t* ptab = a.page_table + static_cast<int64_t>(a.meta->slot[row]) * a.max_pages;
+        const int p0 = k_begin / a.page_tokens, p1 = (k_end - 1) / a.page_tokens;
+        for (int i = threadIdx.x; i <= p1 - p0; i += 128) s_pages[i] = ptab[p0 + i];
+    }
+    const int page_base = k_begin / a.page_tokens;
     const int n_blocks = cdiv(k_end - k_begin, KB);
 
     // Q fragment (A operand, rows = query heads of this kv head)
@@ -283,7 +297,7 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(const __nv_bfloat16* _
             const int kr = i / CH, c = i % CH;
             const int key = k0 + kr;
             const bool ok = key < k_end;
-            const int page = ok ? ptab[key / a.page_tokens] : 0;
+            const int page = ok ? s_pages[key / a.page_tokens - page_base] : 0;
             const __nv_bfloat16* src = kv_layer + static_cast<int64_t>(page) * a.page_stride +
                                        static_cast<int64_t>(hk) * a.page_tokens * HD +
                                        static_cast<int64_t>(key % a.page_tokens) * HD + c * 8;
@@ -297,6 +311,7 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(const __nv_bfloat16* _
     for (int i = 0; i < HD / 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
     float m_run = -INFINITY, l_run = 0.f;  // row r (c0/c1); rows r+8 are padding
 
+    __syncthreads();  // s_pages
     int it = 0;
     if (warp < n_blocks) {
         load(warp, 0);

@@ -197,17 +197,22 @@ __global__ void __launch_bounds__(kThreads, 1)
                             d4[q] = make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
                                                 __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]));
                     } else if constexpr (MODE == EPI_RESID) {
+                        // all loads first, then all stores: 8 independent requests in
+                        // flight instead of 8 serialised read-modify-write round trips
                         float4* d4 = reinterpret_cast<float4*>(static_cast<float*>(args.out) +
                                                                static_cast<size_t>(t) * args.ldo + n0 + c);
+                        float4 old[8];
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) old[q] = __ldcg(d4 + q);
 #pragma unroll
                         for (int q = 0; q < 8; ++q) {
-                            float4 v = d4[q];
-                            v.x += __uint_as_float(r[4 * q + 0]);
-                            v.y += __uint_as_float(r[4 * q + 1]);
-                            v.z += __uint_as_float(r[4 * q + 2]);
-                            v.w += __uint_as_float(r[4 * q + 3]);
-                            d4[q] = v;
+                            old[q].x += __uint_as_float(r[4 * q + 0]);
+                            old[q].y += __uint_as_float(r[4 * q + 1]);
+                            old[q].z += __uint_as_float(r[4 * q + 2]);
+                            old[q].w += __uint_as_float(r[4 * q + 3]);
                         }
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) d4[q] = old[q];
                     }
                 }
             }
@@ -225,9 +230,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                         static_cast<float*>(args.out)[static_cast<size_t>(n0 + c + j) * args.ldo + f] =
                             __uint_as_float(v[j]);
                 } else if constexpr (MODE == EPI_RESID) {
+                    float* col = static_cast<float*>(args.out) + static_cast<size_t>(n0 + c) * args.ldo + f;
+                    float old[32];
+                    _Pragma("unroll") for (int j = 0; j < 32; ++j) old[j] =
+                        j < tcount ? __ldcg(col + static_cast<size_t>(j) * args.ldo) : 0.f;
                     _Pragma("unroll") for (int j = 0; j < 32; ++j) if (j < tcount)
-                        static_cast<float*>(args.out)[static_cast<size_t>(n0 + c + j) * args.ldo + f] +=
-                            __uint_as_float(v[j]);
+                        col[static_cast<size_t>(j) * args.ldo] = old[j] + __uint_as_float(v[j]);
                 } else if constexpr (MODE == EPI_SWIGLU) {
                     // lanes 0-63 of the tile hold gate rows, 64-127 the matching up rows
                     if (row >= 64) {
@@ -289,6 +297,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         float acc[32];
 #pragma unroll
                         for (int j = 0; j < 32; ++j) acc[j] = 0.f;
+#pragma unroll 4
                         for (int z = 0; z < splits; ++z)
 #pragma unroll
                             for (int j = 0; j < 32; ++j)
