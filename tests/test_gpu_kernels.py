@@ -50,9 +50,9 @@ def test_gemm_residual(swlib, M):
     assert _rel(C, ref) < 1e-5 + 4e-3 * float((A.float() @ B.float().T).norm() / ref.norm())
 
 
-@pytest.mark.parametrize("M", [2, 40, 256, 300])
-def test_gemm_swiglu(swlib, M):
-    K, F = 256, 512  # 2F rows in [gate 64 | up 64] blocks
+@pytest.mark.parametrize("M,K", [(2, 256), (40, 2048), (256, 256), (300, 512), (64, 4096)])
+def test_gemm_swiglu(swlib, M, K):
+    F = 512  # 2F rows in [gate 64 | up 64] blocks
     g = torch.Generator(device="cuda").manual_seed(M + 11)
     A = torch.randn(M, K, device="cuda", generator=g).bfloat16()
     Wg = (torch.randn(F, K, device="cuda", generator=g) / K ** 0.5)

@@ -129,3 +129,46 @@ def test_decode_uses_device_resident_token(tiny, tiny_oracle):
     lg_dev = tiny.decode(slots, pos, tokens=None, new_page=[-1] * 3)
     ref = tiny_oracle.decode(t1, pos, rows)
     assert rel_rows(lg_dev, ref).max() < LOGIT_RTOL_FP32
+
+
+def _long_ctx_engine(desc, pages):
+    from paper_2505_03763_b200 import runtime
+
+    return runtime.Engine(desc, max_prefill_tokens=2048, max_decode_batch=8, n_pages=8 * pages + 8, n_slots=8,
+                          max_pages_per_slot=pages, max_out=16)
+
+
+@pytest.mark.parametrize("shape", ["TINY", "LLAMA_1B_2L"])
+def test_long_context_split_kv_and_split_k(shape):
+    """Contexts long enough for several split-KV chunks (multi-split merge) and,
+    at the 1B shape, split-K decode GEMMs with the last-CTA fixup."""
+    import dataclasses
+
+    d = M.TINY if shape == "TINY" else dataclasses.replace(M.LLAMA_1B, n_layers=2)
+    pages = 80
+    eng = _long_ctx_engine(d, pages)
+    try:
+        o = M.OracleModel(d)
+        emu = M.OracleModel(d, emulate_bf16=True, share_weights_with=o)
+        lens = [700, 1030]
+        prompts = [M.prompt_tokens(d.seed, 500 + i, n, d.vocab) for i, n in enumerate(lens)]
+        rows = [list(range(i * pages, (i + 1) * pages)) for i in range(2)]
+        lg = eng.prefill([0, 1], prompts, [r[:(n + 15) // 16] for r, n in zip(rows, lens)])
+        ref, em = o.prefill(prompts, rows), emu.prefill(prompts, rows)
+        e32, eem = [rel_rows(lg, ref)], [rel_rows(lg, em)]
+        toks = [int(np.argmax(l)) for l in ref]
+        pos = list(lens)
+        for _ in range(4):
+            newp = [rows[i][pos[i] // 16] if pos[i] % 16 == 0 else -1 for i in range(2)]
+            lg = eng.decode([0, 1], pos, tokens=toks, new_page=newp)
+            ref, em = o.decode(toks, pos, rows), emu.decode(toks, pos, rows)
+            e32.append(rel_rows(lg, ref))
+            eem.append(rel_rows(lg, em))
+            toks = [int(np.argmax(l)) for l in ref]
+            pos = [p + 1 for p in pos]
+        e32, eem = np.concatenate(e32), np.concatenate(eem)
+        print(f"\n{shape}: rel-L2 vs fp32 max {e32.max():.4f}; vs emulated max {eem.max():.4f}")
+        assert eem.max() < LOGIT_RTOL
+        assert e32.max() < LOGIT_RTOL_FP32
+    finally:
+        eng.close()
