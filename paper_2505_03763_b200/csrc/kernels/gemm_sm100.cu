@@ -21,6 +21,7 @@
 #include <cuda.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <tuple>
@@ -36,14 +37,16 @@ constexpr int BM = 128;
 constexpr int BK = 64;
 constexpr int kThreads = 192;
 
-template <int BN, bool SWAP>
+template <int BN, bool SWAP, bool SMALL = false>
 struct GemmCfg {
     static constexpr int kABytes = BM * BK * 2;
     static constexpr int kBBytes = BN * BK * 2;
     static constexpr int kStageBytes = kABytes + kBBytes;
-    // decode (swap) tiles: ~100 KB so two CTAs stream weights per SM
-    static constexpr int kBudget = (SWAP && BN <= 64) ? 100 * 1024 : 200 * 1024;
-    static constexpr int kStages = kBudget / kStageBytes > 8 ? 8 : kBudget / kStageBytes;
+    // SMALL: ~100 KB so two CTAs stream weights per SM
+    static constexpr int kBudget = SMALL ? 100 * 1024 : 200 * 1024;
+    static constexpr int kStagesRaw = kBudget / kStageBytes > 8 ? 8 : kBudget / kStageBytes;
+    static constexpr int kStages = kStagesRaw >= 8 ? 8 : 4;  // multiple of the 4 producer warps
+    static_assert(kStagesRaw >= 4, "smem budget below 4 stages");
     static constexpr int kTmemCols = BN < 32 ? 32 : BN;
     static constexpr int kXchgBytes = 64 * 33 * 4;  // SwiGLU swap-mode exchange
     static constexpr int kSmem = 1024 + kStages * kStageBytes + kXchgBytes + 256;
@@ -51,10 +54,10 @@ struct GemmCfg {
 
 __device__ __forceinline__ float silu_mul(float g, float u) { return g / (1.0f + __expf(-g)) * u; }
 
-template <int BN, int MODE, bool SWAP>
+template <int BN, int MODE, bool SWAP, bool SMALL>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmArgs args) {
-    using C = GemmCfg<BN, SWAP>;
+    using C = GemmCfg<BN, SWAP, SMALL>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sA = smem;
@@ -96,23 +99,38 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) {
             tma_prefetch_desc(&tmA);
             tma_prefetch_desc(&tmB);
+        }
+        __syncwarp();
+    } else if (warp >= 2) {
+        // ---------------------------------------------------------- producers
+        // One issuing thread completes only ~1 bulk copy per ~600 cycles
+        // (tools/tma_bench2.cu), so the four epilogue warps share the K loop:
+        // warp p issues K-blocks kb = p, p+4, ... (stages s = kb % S, S % 4 == 0,
+        // so each stage has one owner), then turns into an epilogue warp.
+        if (lane == 0) {
             // Weights are streamed once per launch (evict-first); activations
             // are re-read by every feature tile (evict-last).
             const uint64_t pol_w = l2_policy_evict_first();
             const uint64_t pol_x = l2_policy_evict_last();
             const uint64_t pol_a = SWAP ? pol_w : pol_x;
             const uint64_t pol_b = SWAP ? pol_x : pol_w;
-            for (int kb = 0; kb < nk; ++kb) {
+            // Tiles start their K walk at staggered offsets so the CTAs of a
+            // one-wave launch do not stream in lockstep.
+            const int rot = args.stagger ? static_cast<int>((blockIdx.y * 7u + blockIdx.x * 3u) % nk) : 0;
+            for (int kb = warp - 2; kb < nk; kb += 4) {
                 const int s = kb % C::kStages;
                 const uint32_t ph = (kb / C::kStages) & 1;
+                int kk = kb + rot;
+                kk = kk >= nk ? kk - nk : kk;
                 mbar_wait(&empty[s], ph ^ 1);
                 mbar_expect_tx(&full[s], C::kStageBytes);
-                tma_load_2d(sA + s * C::kABytes, &tmA, &full[s], (kb0 + kb) * BK, m0, pol_a);
-                tma_load_2d(sB + s * C::kBBytes, &tmB, &full[s], (kb0 + kb) * BK, n0, pol_b);
+                tma_load_2d(sA + s * C::kABytes, &tmA, &full[s], (kb0 + kk) * BK, m0, pol_a);
+                tma_load_2d(sB + s * C::kBBytes, &tmB, &full[s], (kb0 + kk) * BK, n0, pol_b);
             }
         }
         __syncwarp();
-    } else if (warp == 1) {
+    }
+    if (warp == 1) {
         if (lane == 0) {
             constexpr uint32_t idesc = umma_idesc_bf16(BM, BN);
             for (int kb = 0; kb < nk; ++kb) {
@@ -131,7 +149,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             umma_commit(acc_ready);
         }
         __syncwarp();
-    } else {
+    }
+    if (warp >= 2) {
         // ------------------------------------------------------------ epilogue
         const int quarter = warp & 3;  // TMEM lanes [32*quarter, 32*quarter+32)
         const int row = quarter * 32 + lane;  // accumulator row inside the tile
@@ -335,18 +354,33 @@ EncodeTiled encode_fn() {
     return fn;
 }
 
-template <int BN, int MODE, bool SWAP>
-void launch_one(const CUtensorMap& a, const CUtensorMap& b, const GemmArgs& args, cudaStream_t st) {
-    using C = GemmCfg<BN, SWAP>;
+template <int BN, int MODE, bool SWAP, bool SMALL>
+void launch_cfg(const CUtensorMap& a, const CUtensorMap& b, const GemmArgs& args, cudaStream_t st) {
+    using C = GemmCfg<BN, SWAP, SMALL>;
     static bool configured = false;  // per instantiation
     if (!configured) {
-        SW_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<BN, MODE, SWAP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     C::kSmem));
+        SW_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<BN, MODE, SWAP, SMALL>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
         configured = true;
     }
     dim3 grid(args.N / BN, cdiv(args.M, BM), args.splits > 0 ? args.splits : 1);
-    gemm_tc_kernel<BN, MODE, SWAP><<<grid, kThreads, C::kSmem, st>>>(a, b, args);
+    gemm_tc_kernel<BN, MODE, SWAP, SMALL><<<grid, kThreads, C::kSmem, st>>>(a, b, args);
     SW_LAUNCH_CHECK();
+}
+
+int env_int(const char* name, int dflt) {
+    const char* v = std::getenv(name);
+    return v && *v ? std::atoi(v) : dflt;
+}
+
+template <int BN, int MODE, bool SWAP>
+void launch_one(const CUtensorMap& a, const CUtensorMap& b, const GemmArgs& args, cudaStream_t st) {
+    // decode (swap) tiles with BN <= 64 default to the two-CTAs-per-SM budget;
+    // SW_GEMM_SMALL=0/1 overrides (tuning sweeps)
+    static const int small_env = env_int("SW_GEMM_SMALL", -1);
+    const bool small = small_env >= 0 ? small_env != 0 : (SWAP && BN <= 64);
+    if (small) launch_cfg<BN, MODE, SWAP, true>(a, b, args, st);
+    else launch_cfg<BN, MODE, SWAP, false>(a, b, args, st);
 }
 
 template <bool SWAP, int MODE>
@@ -415,6 +449,8 @@ void gemm_run(const GemmProblem& p, cudaStream_t st) {
             int sp = std::max(1, 296 / tiles);
             sp = std::min(sp, nk / 4);
             sp = std::min(sp, 16);
+            static const int forced = env_int("SW_GEMM_SPLITS", 0);  // tuning override
+            if (forced > 0) sp = std::min(forced, nk);
             a.splits = std::max(sp, 1);
             if (static_cast<size_t>(tiles) * a.splits * 256 * 128 > p.ws_floats || tiles > p.n_counters) a.splits = 1;
         }
@@ -424,6 +460,8 @@ void gemm_run(const GemmProblem& p, cudaStream_t st) {
         const int bn = gemm_pick_bn_swap(p.tokens);
         a.M = p.features;
         a.N = bn;
+        static const int stagger = env_int("SW_GEMM_STAGGER", 1);
+        a.stagger = stagger;
         const CUtensorMap& ta = tmap_cached(p.W, p.w_rows, p.K, BM);
         const CUtensorMap& tb = tmap_cached(p.X, p.x_rows, p.K, bn);
         switch (p.mode) {

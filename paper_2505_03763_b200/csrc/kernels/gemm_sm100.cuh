@@ -21,6 +21,7 @@ struct GemmArgs {
     int splits;          // split-K factor (grid z)
     float* ws;           // split-K partial tiles [tiles][splits][BN][128]
     unsigned* counters;  // split-K arrival counters [tiles], zero between launches
+    int stagger;         // rotate each tile's K-block order (DRAM channel spread)
 };
 
 // Y[t, f] = sum_k X[t, k] W[f, k] over `tokens` rows of X and `features` rows of W.
