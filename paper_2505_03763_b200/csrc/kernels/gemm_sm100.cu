@@ -43,7 +43,7 @@ struct GemmCfg {
     static constexpr int kBBytes = BN * BK * 2;
     static constexpr int kStageBytes = kABytes + kBBytes;
     // SMALL: ~100 KB so two CTAs stream weights per SM
-    static constexpr int kBudget = SMALL ? 100 * 1024 : 200 * 1024;
+    static constexpr int kBudget = (SMALL && BN <= 64) ? 100 * 1024 : 200 * 1024;
     static constexpr int kStagesRaw = kBudget / kStageBytes > 8 ? 8 : kBudget / kStageBytes;
     static constexpr int kStages = kStagesRaw >= 8 ? 8 : 4;  // multiple of the 4 producer warps
     static_assert(kStagesRaw >= 4, "smem budget below 4 stages");
