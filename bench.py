@@ -214,6 +214,22 @@ def spec_for(w, extra: str, rank: int, world: int) -> str:
     return s
 
 
+def gather_run_stats(dist, world: int, res: dict, device) -> dict:
+    """Result gathering across request-sharded replicas -- the only collective
+    (NCCL over NVLink on the GPU box, gloo in the CPU tests): makespan and wall
+    are the max over ranks, tokens the sum."""
+    import torch
+
+    t = torch.tensor([res["makespan"], res["wall"], float(res["tokens"])], device=device, dtype=torch.float64)
+    g = [torch.zeros_like(t) for _ in range(world)]
+    dist.all_gather(g, t)
+    out = dict(res)
+    out["makespan"] = max(float(x[0]) for x in g)
+    out["wall"] = max(float(x[1]) for x in g)
+    out["tokens"] = sum(float(x[2]) for x in g)
+    return out
+
+
 def run_many(eng, spec: str, k: int):
     import paper_2505_03763_b200 as sw
 
@@ -311,12 +327,7 @@ def main():
         res = run_many(eng, spec, args.steps)
         torch.cuda.synchronize()
         if dist:
-            t = torch.tensor([res["makespan"], res["wall"], float(res["tokens"])], device="cuda", dtype=torch.float64)
-            g = [torch.zeros_like(t) for _ in range(world)]
-            dist.all_gather(g, t)  # NCCL result gathering (the only collective)
-            res["makespan"] = max(float(x[0]) for x in g)
-            res["wall"] = max(float(x[1]) for x in g)
-            res["tokens"] = sum(float(x[2]) for x in g)
+            res = gather_run_stats(dist, world, res, "cuda")
         return res
 
     with ClockSampler(local) as clocks:
