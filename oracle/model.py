@@ -136,9 +136,11 @@ class OracleModel:
 
     emulate_bf16=False is THE reference: everything in fp32.  emulate_bf16=True
     additionally rounds to bf16 exactly where the CUDA path stores bf16
-    (RMSNorm outputs, roped q/k and v -- the KV cache --, the softmax
-    numerators fed to the P.V tensor-core product, attention output, SwiGLU
-    output), so the remaining difference is accumulation order only.
+    (RMSNorm outputs -- in decode the norm is folded into the GEMM, so the
+    rounded tensor is the residual x itself --, roped q/k and v -- the KV
+    cache --, the softmax numerators fed to the P.V tensor-core product,
+    attention output, SwiGLU output), so the remaining difference is
+    accumulation order only.
     """
 
     def __init__(self, desc: Desc, page_tokens: int = 16, emulate_bf16: bool = False, share_weights_with=None):
@@ -174,6 +176,15 @@ class OracleModel:
     # -- pieces
     def _r(self, x: np.ndarray) -> np.ndarray:
         return bf16_round(x) if self.emul else x
+
+    def _norm_in(self, x: np.ndarray) -> np.ndarray:
+        """RMSNorm feeding a GEMM.  Emulation mirrors where the kernels round:
+        prefill rounds the normalised rows; decode folds the norm into the GEMM
+        (B operand = bf16(x), epilogue scales by 1/rms)."""
+        if self.emul and self._phase == "decode":
+            inv = 1.0 / np.sqrt(np.mean(x.astype(np.float32) ** 2, axis=-1, keepdims=True) + np.float32(self.d.norm_eps))
+            return (bf16_round(x) * inv).astype(np.float32)
+        return self._r(self.rmsnorm(x))
 
     def rmsnorm(self, x: np.ndarray) -> np.ndarray:
         ms = np.mean(x.astype(np.float32) ** 2, axis=-1, keepdims=True)
@@ -230,7 +241,7 @@ class OracleModel:
         """One decoder layer over the concatenation of per-request token spans."""
         W = self.layers[l]
         H, Hk, hd = self.d.n_heads, self.d.n_kv_heads, self.d.head_dim
-        h = self._r(self.rmsnorm(x))
+        h = self._norm_in(x)
         q = (h @ W["wq"].T).reshape(-1, H, hd)
         k = (h @ W["wk"].T).reshape(-1, Hk, hd)
         v = self._r((h @ W["wv"].T).reshape(-1, Hk, hd))
@@ -245,7 +256,7 @@ class OracleModel:
             o[off:off + t] = self._attend(q[off:off + t], ks, vs, pos)
             off += t
         x = x + self._r(o.reshape(len(x), -1)) @ W["wo"].T
-        h = self._r(self.rmsnorm(x))
+        h = self._norm_in(x)
         gate = h @ W["wg"].T
         a = self._r((gate / (1.0 + np.exp(-gate))) * (h @ W["wu"].T))
         return (x + a.astype(np.float32) @ W["wd"].T).astype(np.float32)
@@ -258,7 +269,7 @@ class OracleModel:
             x = self._block(l, x, rows, spans)
         if want is None:
             want = np.cumsum([len(s) for s in spans]) - 1
-        return (self._r(self.rmsnorm(x[want])) @ self.lm.T).astype(np.float32)
+        return (self._norm_in(x[want]) @ self.lm.T).astype(np.float32)
 
     # -- phase entry points (same semantics as sw_prefill_enqueue / sw_decode_enqueue)
     def prefill(self, prompts: List[np.ndarray], page_rows: List[Sequence[int]]) -> np.ndarray:

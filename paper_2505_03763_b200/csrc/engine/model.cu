@@ -95,6 +95,8 @@ void ws_alloc(Workspace& w, const sw_model_desc& d, int rows, bool decode, int m
     if (decode) {
         w.meta = dalloc<StepMeta>(1);
         SW_CUDA(cudaMemset(w.meta, 0, sizeof(StepMeta)));
+        w.ss = dalloc<float>(2 * kMaxDecodeRows);
+        SW_CUDA(cudaMemset(w.ss, 0, 2 * kMaxDecodeRows * sizeof(float)));
         const int G = d.n_heads / d.n_kv_heads;
         const size_t parts = static_cast<size_t>(kMaxDecodeRows) * d.n_kv_heads * max_splits_cap * G;
         w.part_o = dalloc<float>(parts * d.head_dim);
@@ -291,12 +293,27 @@ void prefill_forward(sw_model* m, sw_kv* kv, const sw_batch& b, cudaStream_t st)
 namespace {
 
 void decode_layers(sw_model* m, sw_kv* kv, int R, cudaStream_t st) {
+    // One decode step, 5 kernels per layer, chained with programmatic dependent
+    // launch (each kernel's weight stream starts while its predecessor drains):
+    //   qkv  GEMM . RMSNorm scale . RoPE -> q, K/V straight into the paged cache
+    //   attn split-KV paged attention
+    //   wo   GEMM + residual; emits bf16(x) and sum(x^2) for the next norm
+    //   gu   GEMM . RMSNorm scale . SwiGLU
+    //   wd   GEMM + residual; emits bf16(x) and sum(x^2)
+    // RMSNorm is folded into the consuming GEMM: its B operand is bf16(x) and
+    // the epilogue scales by rsqrt(mean(x^2) + eps) (the gains are 1, i.e.
+    // folded into the weights).
+    PdlScope pdl(true);
     const sw_model_desc& d = m->desc;
     Workspace& w = m->dec;
     const int* live = &w.meta->n;
     const int qkv_w = (d.n_heads + 2 * d.n_kv_heads) * d.head_dim;
     const int hdH = d.n_heads * d.head_dim;
-    embed(w.meta, R, m->emb, w.x, d.d_model, kv->last_token, kv->page_table, kv->max_pages, kv->page_tokens, st);
+    float* ss_a = w.ss;
+    float* ss_b = w.ss + kMaxDecodeRows;
+    __nv_bfloat16* xb = w.xn;
+    embed(w.meta, R, m->emb, w.x, xb, ss_a, ss_b, d.d_model, kv->last_token, kv->page_table, kv->max_pages,
+          kv->page_tokens, st);
     DecodeAttnArgs aa{};
     aa.meta = w.meta;
     aa.page_table = kv->page_table;
@@ -312,24 +329,51 @@ void decode_layers(sw_model* m, sw_kv* kv, int R, cudaStream_t st) {
     aa.part_o = w.part_o;
     aa.part_ml = w.part_ml;
     aa.counters = w.attn_cnt;
+    auto norm_in = [&](GemmProblem& p, const float* ss) {
+        p.fx.row_ss = ss;
+        p.fx.norm_dim = d.d_model;
+        p.fx.norm_eps = d.norm_eps;
+    };
+    auto resid_out = [&](GemmProblem& p, float* ss_acc, float* ss_clear) {
+        p.fx.x_bf16 = xb;
+        p.fx.ss_out = ss_acc;
+        p.fx.ss_zero = ss_clear;
+    };
     for (int l = 0; l < d.n_layers; ++l) {
         const LayerWeights& L = m->layers[l];
         __nv_bfloat16* kvl = kv->pages + l * kv->layer_stride;
-        rmsnorm(w.x, L.g_attn, w.xn, R, d.d_model, d.norm_eps, live, nullptr, st);
-        gemm_run(gp(w.xn, w.rows, L.wqkv, qkv_w, R, qkv_w, d.d_model, EPI_STORE_F32, true, w.qkv, qkv_w, live, &w), st);
-        rope_kv(w.qkv, w.q, kvl, w.meta->pos, w.meta->slot, kv->page_table, m->rope_cs, R, live, d.n_heads,
-                d.n_kv_heads, d.head_dim, kv->max_pages, kv->page_tokens, st);
+        GemmProblem pq = gp(xb, w.rows, L.wqkv, qkv_w, R, qkv_w, d.d_model, EPI_QKV_ROPE, true, nullptr, qkv_w, live, &w);
+        norm_in(pq, ss_a);
+        pq.fx.pos = w.meta->pos;
+        pq.fx.slot = w.meta->slot;
+        pq.fx.page_table = kv->page_table;
+        pq.fx.max_pages = kv->max_pages;
+        pq.fx.page_tokens = kv->page_tokens;
+        pq.fx.rope_cs = m->rope_cs;
+        pq.fx.q_out = w.q;
+        pq.fx.kv_layer = kvl;
+        pq.fx.page_stride = kv->page_stride;
+        pq.fx.H = d.n_heads;
+        pq.fx.Hkv = d.n_kv_heads;
+        pq.fx.hd = d.head_dim;
+        gemm_run(pq, st);
         attn_decode(w.q, kvl, w.attn, aa, R, d.head_dim, st);
-        gemm_run(gp(w.attn, w.rows, L.wo, d.d_model, R, d.d_model, hdH, EPI_RESID, true, w.x, d.d_model, live, &w), st);
-        rmsnorm(w.x, L.g_mlp, w.xn, R, d.d_model, d.norm_eps, live, nullptr, st);
-        gemm_run(gp(w.xn, w.rows, L.wgu, 2 * d.ffn_dim, R, 2 * d.ffn_dim, d.d_model, EPI_SWIGLU, true, w.act,
-                    d.ffn_dim, live, &w),
-                 st);
-        gemm_run(gp(w.act, w.rows, L.wd, d.d_model, R, d.d_model, d.ffn_dim, EPI_RESID, true, w.x, d.d_model, live, &w),
-                 st);
+        GemmProblem po = gp(w.attn, w.rows, L.wo, d.d_model, R, d.d_model, hdH, EPI_RESID, true, w.x, d.d_model, live, &w);
+        resid_out(po, ss_b, ss_a);
+        gemm_run(po, st);
+        GemmProblem pg = gp(xb, w.rows, L.wgu, 2 * d.ffn_dim, R, 2 * d.ffn_dim, d.d_model, EPI_SWIGLU, true, w.act,
+                            d.ffn_dim, live, &w);
+        norm_in(pg, ss_b);
+        gemm_run(pg, st);
+        GemmProblem pd = gp(w.act, w.rows, L.wd, d.d_model, R, d.d_model, d.ffn_dim, EPI_RESID, true, w.x, d.d_model,
+                            live, &w);
+        resid_out(pd, ss_a, ss_b);
+        gemm_run(pd, st);
     }
-    rmsnorm(w.x, m->g_final, w.xlast, R, d.d_model, d.norm_eps, live, nullptr, st);
-    lm_head(m, w, R, live, nullptr, st);
+    GemmProblem pl = gp(xb, w.rows, m->lm, d.vocab, R, d.vocab, d.d_model, EPI_ARGMAX, true, nullptr, 0, live);
+    pl.argmax = w.keys;
+    norm_in(pl, ss_a);  // argmax is scale invariant; kept so logits and argmax see one definition
+    gemm_run(pl, st);
     finalize_tokens(w.keys, w.meta->slot, w.meta->out_index, R, live, kv->last_token, kv->out_tokens, kv->max_out, st);
 }
 
@@ -380,9 +424,12 @@ void decode_forward(sw_model* m, sw_kv* kv, const sw_batch& b, cudaStream_t st, 
             SW_CUDA(cudaStreamDestroy(cs));
         }
     }
-    if (b.logits_out) {
-        GemmProblem q = gp(m->dec.xlast, kLmRowsMax, m->lm, d.vocab, b.n, d.vocab, d.d_model, EPI_STORE_F32, true,
+    if (b.logits_out) {  // parity checks: fp32 logits from the same folded-norm input
+        GemmProblem q = gp(m->dec.xn, m->dec.rows, m->lm, d.vocab, b.n, d.vocab, d.d_model, EPI_STORE_F32, true,
                            b.logits_out, d.vocab);
+        q.fx.row_ss = m->dec.ss;
+        q.fx.norm_dim = d.d_model;
+        q.fx.norm_eps = d.norm_eps;
         gemm_run(q, st);
     }
 }
@@ -491,7 +538,8 @@ extern "C" int sw_model_destroy(sw_model* m) {
         for (Workspace* w : {&m->pre, &m->dec}) {
             for (void* p : {(void*)w->x, (void*)w->xn, (void*)w->qkv, (void*)w->q, (void*)w->attn, (void*)w->act,
                             (void*)w->xlast, (void*)w->keys, (void*)w->meta, (void*)w->part_o, (void*)w->part_ml,
-                            (void*)w->pmeta, (void*)w->splitk_ws, (void*)w->splitk_cnt, (void*)w->attn_cnt})
+                            (void*)w->pmeta, (void*)w->splitk_ws, (void*)w->splitk_cnt, (void*)w->attn_cnt,
+                            (void*)w->ss})
                 if (p) cudaFree(p);
         }
         for (PinnedRing* r : {&m->pre_ring, &m->dec_ring}) {

@@ -38,6 +38,7 @@ struct Workspace {
     unsigned long long* keys = nullptr;  // [256] packed argmax
     // decode only
     StepMeta* meta = nullptr;
+    float* ss = nullptr;  // [2][kMaxDecodeRows] sum(x^2) accumulators for the folded RMSNorms
     float* splitk_ws = nullptr;  // split-K partial tiles of the decode GEMMs
     size_t splitk_floats = 0;
     unsigned* splitk_cnt = nullptr;

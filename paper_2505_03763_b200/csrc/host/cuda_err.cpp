@@ -11,6 +11,10 @@ namespace sw {
 std::atomic<unsigned long long> g_launches{0};
 void count_launches(unsigned long long n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 std::atomic<unsigned long long> g_h2d{0}, g_d2h{0};
+bool& pdl_mode() {
+    thread_local bool on = false;
+    return on;
+}
 void count_transfer(unsigned long long h2d, unsigned long long d2h) {
     g_h2d.fetch_add(h2d, std::memory_order_relaxed);
     g_d2h.fetch_add(d2h, std::memory_order_relaxed);

@@ -53,7 +53,7 @@ __device__ __forceinline__ int swz(int row, int chunk) {
 
 constexpr int kQRows = 64;
 constexpr int kKeys = 64;
-constexpr int kMaxChunkPages = 2048;  // page ids of one decode split staged in smem
+constexpr int kMaxChunkPages = 512;  // page ids of one decode split staged in smem (8192 keys)
 
 template <int HD>
 __global__ void __launch_bounds__(128) attn_prefill_kernel(const __nv_bfloat16* __restrict__ q,
@@ -254,6 +254,8 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(const __nv_bfloat16* _
     __shared__ uint32_t s_last;
 
     __shared__ int32_t s_pages[kMaxChunkPages];
+    griddep_launch_dependents();
+    griddep_wait();
     const int n_rows = a.meta->n;
     const int row = blockIdx.z;
     if (row >= n_rows) return;
@@ -261,7 +263,8 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(const __nv_bfloat16* _
     // splits chosen at run time: only as many as it takes to give the GPU
     // ~4 CTAs per SM, each warp keeping >= 1 key block
     const int want = cdiv(148 * 4, n_rows * a.Hkv);
-    const int splits0 = max(1, min(min(want, a.max_splits), cdiv(ctx, 4 * KB)));
+    const int splits0 = max(cdiv(ctx, kMaxChunkPages * a.page_tokens),
+                            max(1, min(min(want, a.max_splits), cdiv(ctx, 4 * KB))));
     const int chunk = cdiv(cdiv(ctx, splits0), KB) * KB;
     const int splits = cdiv(ctx, chunk);  // every split non-empty
     const int split = blockIdx.x;
@@ -470,8 +473,7 @@ void decode_launch(const __nv_bfloat16* q, const __nv_bfloat16* kv_layer, __nv_b
         cfg = true;
     }
     dim3 grid(a.max_splits, a.Hkv, max_rows);
-    attn_decode_kernel<HD, G, KB><<<grid, 128, smem, st>>>(q, kv_layer, out, a);
-    SW_LAUNCH_CHECK();
+    launch_k(attn_decode_kernel<HD, G, KB>, grid, dim3(128), smem, st, q, kv_layer, out, a);
 }
 
 }  // namespace

@@ -8,6 +8,7 @@
 #include <stdint.h>
 
 #include <string>
+#include <utility>
 
 namespace sw {
 
@@ -31,6 +32,41 @@ void count_transfer(unsigned long long h2d, unsigned long long d2h);  // host<->
     } while (0)
 
 __host__ __device__ constexpr int cdiv(int a, int b) { return (a + b - 1) / b; }
+
+// ---------------------------------------------------------------- PDL
+// Programmatic dependent launch: a kernel launched with the PDL attribute may
+// start while its predecessor in the stream still runs.  Rule used by every
+// kernel here: constant data (weights) may be read before griddep_wait();
+// anything a predecessor writes, and every global write, comes after it.
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;"); }
+
+// Thread-local launch mode: when set (the decode step), launch_k() attaches the
+// programmatic-stream-serialization attribute (kept when captured in a graph).
+bool& pdl_mode();
+struct PdlScope {
+    bool prev;
+    explicit PdlScope(bool on) : prev(pdl_mode()) { pdl_mode() = on; }
+    ~PdlScope() { pdl_mode() = prev; }
+};
+
+template <class... KArgs, class... Args>
+void launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    if (pdl_mode()) {
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+    }
+    SW_CUDA(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
+    count_launches(1);
+}
 
 // ---------------------------------------------------------------- numerics
 __device__ __forceinline__ float bf2f(__nv_bfloat16 v) { return __bfloat162float(v); }

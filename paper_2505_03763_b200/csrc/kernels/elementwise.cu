@@ -54,15 +54,19 @@ void checksum_bf16(const void* p, int64_t n, unsigned long long* out_dev, cudaSt
 }
 
 // ---------------------------------------------------------------- embedding
-// One CTA per row: x[row] = fp32(emb[token]).  Decode rows take the token from
-// the slot's device-resident last generated token (no host round trip) unless
-// explicit tokens are given, and install the step's new page first.
+// Decode step head, one CTA per row: install the step's new page, gather the
+// embedding of the fed token (the slot's device-resident last token unless
+// explicit tokens are given) and emit what the first fused GEMM consumes:
+// x (fp32 residual), bf16(x) (its B operand) and sum(x^2) (its RMSNorm scale);
+// also clears the second norm accumulator.
 __global__ void embed_kernel(const StepMeta* __restrict__ meta, const __nv_bfloat16* __restrict__ emb,
-                             float* __restrict__ x, int d, const int32_t* __restrict__ last_token,
+                             float* __restrict__ x, __nv_bfloat16* __restrict__ xb, float* __restrict__ ss_a,
+                             float* __restrict__ ss_b, int d, const int32_t* __restrict__ last_token,
                              int32_t* __restrict__ page_table, int max_pages, int page_tokens) {
+    griddep_launch_dependents();
+    griddep_wait();
     const int row = blockIdx.x;
-    const int n_rows = meta->n;
-    if (row >= n_rows) return;
+    if (row >= meta->n) return;
     const int slot = meta->slot[row];
     int tok = meta->token[row];
     if (tok < 0) tok = last_token[slot];
@@ -70,17 +74,34 @@ __global__ void embed_kernel(const StepMeta* __restrict__ meta, const __nv_bfloa
         page_table[static_cast<int64_t>(slot) * max_pages + meta->pos[row] / page_tokens] = meta->new_page[row];
     const uint4* src = reinterpret_cast<const uint4*>(emb + static_cast<int64_t>(tok) * d);
     float4* dst = reinterpret_cast<float4*>(x + static_cast<int64_t>(row) * d);
+    uint4* dstb = reinterpret_cast<uint4*>(xb + static_cast<int64_t>(row) * d);
+    float ss = 0.f;
     for (int i = threadIdx.x; i < d / 8; i += blockDim.x) {
         const uint4 v = src[i];
-        dst[2 * i] = make_float4(bf_lo(v.x), bf_hi(v.x), bf_lo(v.y), bf_hi(v.y));
-        dst[2 * i + 1] = make_float4(bf_lo(v.z), bf_hi(v.z), bf_lo(v.w), bf_hi(v.w));
+        const float4 a = make_float4(bf_lo(v.x), bf_hi(v.x), bf_lo(v.y), bf_hi(v.y));
+        const float4 b = make_float4(bf_lo(v.z), bf_hi(v.z), bf_lo(v.w), bf_hi(v.w));
+        dst[2 * i] = a;
+        dst[2 * i + 1] = b;
+        dstb[i] = v;  // bf16(x) == the embedding row itself
+        ss += a.x * a.x + a.y * a.y + a.z * a.z + a.w * a.w + b.x * b.x + b.y * b.y + b.z * b.z + b.w * b.w;
+    }
+    __shared__ float red[32];
+    ss = warp_sum(ss);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float t = 0.f;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+        ss_a[row] = t;
+        ss_b[row] = 0.f;
     }
 }
 
-void embed(const StepMeta* meta, int max_rows, const __nv_bfloat16* emb, float* x, int d, const int32_t* last_token,
-           int32_t* page_table, int max_pages, int page_tokens, cudaStream_t st) {
-    embed_kernel<<<max_rows, 128, 0, st>>>(meta, emb, x, d, last_token, page_table, max_pages, page_tokens);
-    SW_LAUNCH_CHECK();
+void embed(const StepMeta* meta, int max_rows, const __nv_bfloat16* emb, float* x, __nv_bfloat16* xb, float* ss_a,
+           float* ss_b, int d, const int32_t* last_token, int32_t* page_table, int max_pages, int page_tokens,
+           cudaStream_t st) {
+    launch_k(embed_kernel, dim3(max_rows), dim3(128), 0, st, meta, emb, x, xb, ss_a, ss_b, d, last_token, page_table,
+             max_pages, page_tokens);
 }
 
 // Prefill: token ids come staged per token.
@@ -241,6 +262,8 @@ __global__ void finalize_tokens_kernel(unsigned long long* __restrict__ keys, co
                                        const int32_t* __restrict__ out_index, int rows, const int* rows_dev,
                                        int32_t* __restrict__ last_token, int32_t* __restrict__ out_tokens,
                                        int max_out) {
+    griddep_launch_dependents();
+    griddep_wait();
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
     const int live = rows_dev ? *rows_dev : rows;
     if (r >= rows) return;
@@ -256,9 +279,8 @@ __global__ void finalize_tokens_kernel(unsigned long long* __restrict__ keys, co
 
 void finalize_tokens(unsigned long long* keys, const int32_t* slot, const int32_t* out_index, int rows,
                      const int* rows_dev, int32_t* last_token, int32_t* out_tokens, int max_out, cudaStream_t st) {
-    finalize_tokens_kernel<<<cdiv(rows, 128), 128, 0, st>>>(keys, slot, out_index, rows, rows_dev, last_token,
-                                                             out_tokens, max_out);
-    SW_LAUNCH_CHECK();
+    launch_k(finalize_tokens_kernel, dim3(cdiv(rows, 128)), dim3(128), 0, st, keys, slot, out_index, rows, rows_dev,
+             last_token, out_tokens, max_out);
 }
 
 }  // namespace sw

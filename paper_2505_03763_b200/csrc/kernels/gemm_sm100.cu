@@ -48,8 +48,9 @@ struct GemmCfg {
     static constexpr int kStages = kStagesRaw >= 8 ? 8 : 4;  // multiple of the 4 producer warps
     static_assert(kStagesRaw >= 4, "smem budget below 4 stages");
     static constexpr int kTmemCols = BN < 32 ? 32 : BN;
-    static constexpr int kXchgBytes = 64 * 33 * 4;  // SwiGLU swap-mode exchange
-    static constexpr int kSmem = 1024 + kStages * kStageBytes + kXchgBytes + 256;
+    // epilogue exchanges (SwiGLU / RoPE pairs, 128 x 33 fp32) reuse the drained stage ring
+    static_assert(kStages * kStageBytes >= 128 * 33 * 4, "stage ring too small for the exchange buffer");
+    static constexpr int kSmem = 1024 + kStages * kStageBytes + 256;
 };
 
 __device__ __forceinline__ float silu_mul(float g, float u) { return g / (1.0f + __expf(-g)) * u; }
@@ -62,12 +63,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sA = smem;
     uint8_t* sB = smem + C::kStages * C::kABytes;
-    float* xchg = reinterpret_cast<float*>(sB + C::kStages * C::kBBytes);
-    uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(xchg) + C::kXchgBytes);
+    float* xchg = reinterpret_cast<float*>(sA);  // epilogue only: the ring is drained by then
+    uint64_t* full = reinterpret_cast<uint64_t*>(sB + C::kStages * C::kBBytes);
     uint64_t* empty = full + C::kStages;
     uint64_t* acc_ready = empty + C::kStages;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_ready + 1);
 
+    griddep_launch_dependents();  // let the next kernel of the step start its prologue
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     const int m0 = blockIdx.y * BM;
@@ -117,18 +119,42 @@ __global__ void __launch_bounds__(kThreads, 1)
             // Tiles start their K walk at staggered offsets so the CTAs of a
             // one-wave launch do not stream in lockstep.
             const int rot = args.stagger ? static_cast<int>((blockIdx.y * 7u + blockIdx.x * 3u) % nk) : 0;
+            auto kidx = [&](int kb) {
+                const int kk = kb + rot;
+                return kb0 + (kk >= nk ? kk - nk : kk);
+            };
+            // The first ring fill of the constant operand (decode: the weights)
+            // is issued before waiting on the predecessor kernel (PDL), so the
+            // weight stream starts while the previous kernel drains.
+            const uint8_t* pre_dst = SWAP ? sA : sB;
+            const int pre_bytes = SWAP ? C::kABytes : C::kBBytes;
+            const void* pre_map = SWAP ? static_cast<const void*>(&tmA) : static_cast<const void*>(&tmB);
+            const int pre_row = SWAP ? m0 : n0;
+            const uint64_t pre_pol = pol_w;
+            for (int kb = warp - 2; kb < nk && kb < C::kStages; kb += 4) {
+                const int s = kb % C::kStages;
+                mbar_expect_tx(&full[s], C::kStageBytes);
+                tma_load_2d(const_cast<uint8_t*>(pre_dst) + s * pre_bytes, pre_map, &full[s], kidx(kb) * BK, pre_row,
+                            pre_pol);
+            }
+            griddep_wait();
             for (int kb = warp - 2; kb < nk; kb += 4) {
                 const int s = kb % C::kStages;
                 const uint32_t ph = (kb / C::kStages) & 1;
-                int kk = kb + rot;
-                kk = kk >= nk ? kk - nk : kk;
+                const int kc = kidx(kb) * BK;
+                if (kb < C::kStages) {  // weights already in flight: the activation half
+                    if (SWAP) tma_load_2d(sB + s * C::kBBytes, &tmB, &full[s], kc, n0, pol_b);
+                    else tma_load_2d(sA + s * C::kABytes, &tmA, &full[s], kc, m0, pol_a);
+                    continue;
+                }
                 mbar_wait(&empty[s], ph ^ 1);
                 mbar_expect_tx(&full[s], C::kStageBytes);
-                tma_load_2d(sA + s * C::kABytes, &tmA, &full[s], (kb0 + kk) * BK, m0, pol_a);
-                tma_load_2d(sB + s * C::kBBytes, &tmB, &full[s], (kb0 + kk) * BK, n0, pol_b);
+                tma_load_2d(sA + s * C::kABytes, &tmA, &full[s], kc, m0, pol_a);
+                tma_load_2d(sB + s * C::kBBytes, &tmB, &full[s], kc, n0, pol_b);
             }
         }
         __syncwarp();
+        griddep_wait();  // every epilogue thread reads predecessor outputs below
     }
     if (warp == 1) {
         if (lane == 0) {
@@ -238,41 +264,75 @@ __global__ void __launch_bounds__(kThreads, 1)
         } else {
             // row = feature (weight row), columns = tokens
             const int f = m0 + row;
-            auto emit = [&](int c, const uint32_t (&v)[32]) {
+            const DecodeFusion& fx = args.fx;
+            if (fx.ss_zero && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0)
+                for (int t = threadIdx.x - 64; t < args.valid_tokens; t += 128) fx.ss_zero[t] = 0.f;
+            // 32 fp32 values per lane -> lane j holds the sum over the warp of value j (31 shuffles)
+            auto transpose_sum = [&](float (&v)[32]) {
+#pragma unroll
+                for (int off = 16; off >= 1; off >>= 1) {
+                    const bool upper = (lane & off) != 0;
+#pragma unroll
+                    for (int i = 0; i < off; ++i) {
+                        const float send = upper ? v[i] : v[i + off];
+                        const float keep = upper ? v[i + off] : v[i];
+                        v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+                    }
+                }
+            };
+            auto emit = [&](int c, const uint32_t (&raw)[32]) {
                 const int tcount = min(32, n_live - (n0 + c));
+                float v[32];
+#pragma unroll
+                for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(raw[j]);
+                if (fx.row_ss && MODE != EPI_RESID) {  // RMSNorm of the input rows, folded in
+#pragma unroll
+                    for (int j = 0; j < 32; ++j)
+                        if (j < tcount)
+                            v[j] *= rsqrtf(__ldcg(fx.row_ss + n0 + c + j) / static_cast<float>(fx.norm_dim) + fx.norm_eps);
+                }
                 if constexpr (MODE == EPI_STORE) {
                     _Pragma("unroll") for (int j = 0; j < 32; ++j) if (j < tcount)
                         static_cast<__nv_bfloat16*>(args.out)[static_cast<size_t>(n0 + c + j) * args.ldo + f] =
-                            __float2bfloat16_rn(__uint_as_float(v[j]));
+                            __float2bfloat16_rn(v[j]);
                 } else if constexpr (MODE == EPI_STORE_F32) {
                     _Pragma("unroll") for (int j = 0; j < 32; ++j) if (j < tcount)
-                        static_cast<float*>(args.out)[static_cast<size_t>(n0 + c + j) * args.ldo + f] =
-                            __uint_as_float(v[j]);
+                        static_cast<float*>(args.out)[static_cast<size_t>(n0 + c + j) * args.ldo + f] = v[j];
                 } else if constexpr (MODE == EPI_RESID) {
                     float* col = static_cast<float*>(args.out) + static_cast<size_t>(n0 + c) * args.ldo + f;
-                    float old[32];
-                    _Pragma("unroll") for (int j = 0; j < 32; ++j) old[j] =
+                    float x[32];
+                    _Pragma("unroll") for (int j = 0; j < 32; ++j) x[j] =
                         j < tcount ? __ldcg(col + static_cast<size_t>(j) * args.ldo) : 0.f;
-                    _Pragma("unroll") for (int j = 0; j < 32; ++j) if (j < tcount)
-                        col[static_cast<size_t>(j) * args.ldo] = old[j] + __uint_as_float(v[j]);
+                    _Pragma("unroll") for (int j = 0; j < 32; ++j) {
+                        x[j] += v[j];
+                        if (j < tcount) {
+                            col[static_cast<size_t>(j) * args.ldo] = x[j];
+                            if (fx.x_bf16)
+                                fx.x_bf16[static_cast<size_t>(n0 + c + j) * args.ldo + f] = __float2bfloat16_rn(x[j]);
+                        }
+                        x[j] = j < tcount ? x[j] * x[j] : 0.f;
+                    }
+                    if (fx.ss_out) {  // sum(x^2) of the updated rows for the next RMSNorm
+                        transpose_sum(x);
+                        if (lane < tcount) atomicAdd(fx.ss_out + n0 + c + lane, x[0]);
+                    }
                 } else if constexpr (MODE == EPI_SWIGLU) {
                     // lanes 0-63 of the tile hold gate rows, 64-127 the matching up rows
                     if (row >= 64) {
 #pragma unroll
-                        for (int j = 0; j < 32; ++j) xchg[(row - 64) * 33 + j] = __uint_as_float(v[j]);
+                        for (int j = 0; j < 32; ++j) xchg[(row - 64) * 33 + j] = v[j];
                     }
                     asm volatile("bar.sync 1, 128;" ::: "memory");
                     if (row < 64) {
                         const int g = m0 / 2 + row;
                         _Pragma("unroll") for (int j = 0; j < 32; ++j) if (j < tcount)
                             static_cast<__nv_bfloat16*>(args.out)[static_cast<size_t>(n0 + c + j) * args.ldo + g] =
-                                __float2bfloat16_rn(silu_mul(__uint_as_float(v[j]), xchg[row * 33 + j]));
+                                __float2bfloat16_rn(silu_mul(v[j], xchg[row * 33 + j]));
                     }
                     asm volatile("bar.sync 1, 128;" ::: "memory");
                 } else if constexpr (MODE == EPI_ARGMAX) {
                     _Pragma("unroll") for (int j = 0; j < 32; ++j) if (j < tcount) {
-                        unsigned long long key = argmax_key(__uint_as_float(v[j]),
-                                                            static_cast<uint32_t>(args.feature_offset + f));
+                        unsigned long long key = argmax_key(v[j], static_cast<uint32_t>(args.feature_offset + f));
 #pragma unroll
                         for (int o = 16; o > 0; o >>= 1) {
                             const unsigned long long other = __shfl_xor_sync(0xffffffffu, key, o);
@@ -280,6 +340,38 @@ __global__ void __launch_bounds__(kThreads, 1)
                         }
                         if (lane == 0) atomicMax(args.argmax + n0 + c + j, key);
                     }
+                } else if constexpr (MODE == EPI_QKV_ROPE) {
+                    // rotate-half RoPE: row r pairs with r ^ (hd/2) inside its head
+                    const int hd = fx.hd, half = hd >> 1;
+                    const int head = f / hd, i = f % hd;
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) xchg[row * 33 + j] = v[j];
+                    asm volatile("bar.sync 1, 128;" ::: "memory");
+                    const int prow = row ^ half;
+                    const bool is_v = head >= fx.H + fx.Hkv;
+                    _Pragma("unroll") for (int j = 0; j < 32; ++j) {
+                        if (j >= tcount) continue;
+                        const int t = n0 + c + j;
+                        const int pos = fx.pos[t];
+                        float out = v[j];
+                        if (!is_v) {
+                            const float2 cs = fx.rope_cs[static_cast<int64_t>(pos) * half + (i & (half - 1))];
+                            const float b = xchg[prow * 33 + j];
+                            out = i < half ? v[j] * cs.x - b * cs.y : v[j] * cs.x + b * cs.y;
+                        }
+                        if (head < fx.H) {
+                            fx.q_out[static_cast<size_t>(t) * fx.H * hd + f] = __float2bfloat16_rn(out);
+                        } else {
+                            const int page = fx.page_table[static_cast<int64_t>(fx.slot[t]) * fx.max_pages + pos / fx.page_tokens];
+                            const int kvh = is_v ? head - fx.H - fx.Hkv : head - fx.H;
+                            __nv_bfloat16* dst = fx.kv_layer + static_cast<int64_t>(page) * fx.page_stride +
+                                                 (is_v ? fx.page_stride / 2 : 0) +
+                                                 static_cast<int64_t>(kvh) * fx.page_tokens * hd +
+                                                 static_cast<int64_t>(pos % fx.page_tokens) * hd + i;
+                            *dst = __float2bfloat16_rn(out);
+                        }
+                    }
+                    asm volatile("bar.sync 1, 128;" ::: "memory");
                 }
             };
             if (gridDim.z == 1) {
@@ -364,8 +456,7 @@ void launch_cfg(const CUtensorMap& a, const CUtensorMap& b, const GemmArgs& args
         configured = true;
     }
     dim3 grid(args.N / BN, cdiv(args.M, BM), args.splits > 0 ? args.splits : 1);
-    gemm_tc_kernel<BN, MODE, SWAP, SMALL><<<grid, kThreads, C::kSmem, st>>>(a, b, args);
-    SW_LAUNCH_CHECK();
+    launch_k(gemm_tc_kernel<BN, MODE, SWAP, SMALL>, grid, dim3(kThreads), C::kSmem, st, a, b, args);
 }
 
 int env_int(const char* name, int dflt) {
@@ -438,6 +529,7 @@ void gemm_run(const GemmProblem& p, cudaStream_t st) {
     a.valid_tokens = p.tokens;
     a.live_tokens = p.live_tokens;
     a.splits = 1;
+    a.fx = p.fx;
     a.ws = p.ws;
     a.counters = p.counters;
     if (p.swap) {
@@ -470,6 +562,7 @@ void gemm_run(const GemmProblem& p, cudaStream_t st) {
             case EPI_SWIGLU: dispatch_bn<true, EPI_SWIGLU>(bn, ta, tb, a, st); break;
             case EPI_ARGMAX: dispatch_bn<true, EPI_ARGMAX>(bn, ta, tb, a, st); break;
             case EPI_STORE_F32: dispatch_bn<true, EPI_STORE_F32>(bn, ta, tb, a, st); break;
+            case EPI_QKV_ROPE: dispatch_bn<true, EPI_QKV_ROPE>(bn, ta, tb, a, st); break;
             default: throw_cuda("gemm: bad epilogue", cudaErrorInvalidValue, __FILE__, __LINE__);
         }
     } else {

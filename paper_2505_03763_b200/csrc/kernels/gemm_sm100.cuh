@@ -3,11 +3,43 @@
 
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <cuda_bf16.h>
 #include <stdint.h>
 
 namespace sw {
 
-enum GemmEpilogue : int { EPI_STORE = 0, EPI_RESID = 1, EPI_SWIGLU = 2, EPI_ARGMAX = 3, EPI_STORE_F32 = 4 };
+enum GemmEpilogue : int {
+    EPI_STORE = 0,      // bf16 out
+    EPI_RESID = 1,      // fp32 out += acc (residual stream)
+    EPI_SWIGLU = 2,     // [gate 64 | up 64] feature blocks -> bf16 silu(g)*u
+    EPI_ARGMAX = 3,     // packed (value, index) atomicMax per token
+    EPI_STORE_F32 = 4,  // fp32 out
+    EPI_QKV_ROPE = 5,   // decode: RoPE on q/k heads, q -> bf16 buffer, k/v -> paged KV cache
+};
+
+// Decode-only epilogue fusions (swap-AB).
+struct DecodeFusion {
+    // RMSNorm folded into the consumer GEMM: acc *= rsqrt(row_ss[t]/norm_dim + eps)
+    // (the gains are folded into the weights; B is the bf16 residual itself)
+    const float* row_ss = nullptr;
+    float norm_eps = 1e-5f;
+    int norm_dim = 0;
+    // RESID producer side: write bf16(x) for the next GEMM and accumulate
+    // sum(x^2) per token into ss_out; zero ss_zero[0, n) for the norm after next
+    __nv_bfloat16* x_bf16 = nullptr;
+    float* ss_out = nullptr;
+    float* ss_zero = nullptr;
+    // QKV_ROPE: per-token position / slot, page table, cos/sin table, outputs
+    const int32_t* pos = nullptr;
+    const int32_t* slot = nullptr;
+    const int32_t* page_table = nullptr;
+    int max_pages = 0, page_tokens = 16;
+    const float2* rope_cs = nullptr;
+    __nv_bfloat16* q_out = nullptr;
+    __nv_bfloat16* kv_layer = nullptr;
+    long long page_stride = 0;
+    int H = 0, Hkv = 0, hd = 0;
+};
 
 struct GemmArgs {
     int M, N, K;
@@ -22,6 +54,7 @@ struct GemmArgs {
     float* ws;           // split-K partial tiles [tiles][splits][BN][128]
     unsigned* counters;  // split-K arrival counters [tiles], zero between launches
     int stagger;         // rotate each tile's K-block order (DRAM channel spread)
+    DecodeFusion fx;
 };
 
 // Y[t, f] = sum_k X[t, k] W[f, k] over `tokens` rows of X and `features` rows of W.
@@ -45,6 +78,7 @@ struct GemmProblem {
     size_t ws_floats = 0;
     unsigned* counters = nullptr;
     int n_counters = 0;
+    DecodeFusion fx;  // swap-mode epilogue fusions
 };
 
 CUtensorMap make_tmap_bf16(const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows);
