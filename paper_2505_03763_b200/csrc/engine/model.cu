@@ -43,6 +43,7 @@ namespace {
 constexpr int kLmRowsMax = 256;  // LM-head rows per launch (swap-AB N <= 256)
 constexpr int kSplitTiles = 640;     // split-K scratch: (tiles x splits) capacity
 constexpr int kSplitCounters = 1024;
+constexpr int kSsParts = 64;  // sum(x^2) partial rows per norm (d_model / 128 <= 64)
 
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
@@ -95,8 +96,8 @@ void ws_alloc(Workspace& w, const sw_model_desc& d, int rows, bool decode, int m
     if (decode) {
         w.meta = dalloc<StepMeta>(1);
         SW_CUDA(cudaMemset(w.meta, 0, sizeof(StepMeta)));
-        w.ss = dalloc<float>(2 * kMaxDecodeRows);
-        SW_CUDA(cudaMemset(w.ss, 0, 2 * kMaxDecodeRows * sizeof(float)));
+        w.ss = dalloc<float>(2 * kSsParts * kSsStride);
+        SW_CUDA(cudaMemset(w.ss, 0, 2 * kSsParts * kSsStride * sizeof(float)));
         const int G = d.n_heads / d.n_kv_heads;
         const size_t parts = static_cast<size_t>(kMaxDecodeRows) * d.n_kv_heads * max_splits_cap * G;
         w.part_o = dalloc<float>(parts * d.head_dim);
@@ -309,10 +310,11 @@ void decode_layers(sw_model* m, sw_kv* kv, int R, cudaStream_t st) {
     const int* live = &w.meta->n;
     const int qkv_w = (d.n_heads + 2 * d.n_kv_heads) * d.head_dim;
     const int hdH = d.n_heads * d.head_dim;
-    float* ss_a = w.ss;
-    float* ss_b = w.ss + kMaxDecodeRows;
+    float* ss_a = w.ss;  // [kSsParts][kSsStride] partial sum(x^2) rows
+    float* ss_b = w.ss + kSsParts * kSsStride;
+    const int parts = d.d_model / 128;  // one partial row per feature tile of a residual GEMM
     __nv_bfloat16* xb = w.xn;
-    embed(w.meta, R, m->emb, w.x, xb, ss_a, ss_b, d.d_model, kv->last_token, kv->page_table, kv->max_pages,
+    embed(w.meta, R, m->emb, w.x, xb, ss_a, d.d_model, kv->last_token, kv->page_table, kv->max_pages,
           kv->page_tokens, st);
     DecodeAttnArgs aa{};
     aa.meta = w.meta;
@@ -329,21 +331,21 @@ void decode_layers(sw_model* m, sw_kv* kv, int R, cudaStream_t st) {
     aa.part_o = w.part_o;
     aa.part_ml = w.part_ml;
     aa.counters = w.attn_cnt;
-    auto norm_in = [&](GemmProblem& p, const float* ss) {
-        p.fx.row_ss = ss;
+    auto norm_in = [&](GemmProblem& p, const float* ss, int nparts) {
+        p.fx.ss_parts = ss;
+        p.fx.ss_nparts = nparts;
         p.fx.norm_dim = d.d_model;
         p.fx.norm_eps = d.norm_eps;
     };
-    auto resid_out = [&](GemmProblem& p, float* ss_acc, float* ss_clear) {
+    auto resid_out = [&](GemmProblem& p, float* ss_out) {
         p.fx.x_bf16 = xb;
-        p.fx.ss_out = ss_acc;
-        p.fx.ss_zero = ss_clear;
+        p.fx.ss_part_out = ss_out;
     };
     for (int l = 0; l < d.n_layers; ++l) {
         const LayerWeights& L = m->layers[l];
         __nv_bfloat16* kvl = kv->pages + l * kv->layer_stride;
         GemmProblem pq = gp(xb, w.rows, L.wqkv, qkv_w, R, qkv_w, d.d_model, EPI_QKV_ROPE, true, nullptr, qkv_w, live, &w);
-        norm_in(pq, ss_a);
+        norm_in(pq, ss_a, l == 0 ? 1 : parts);
         pq.fx.pos = w.meta->pos;
         pq.fx.slot = w.meta->slot;
         pq.fx.page_table = kv->page_table;
@@ -359,20 +361,20 @@ void decode_layers(sw_model* m, sw_kv* kv, int R, cudaStream_t st) {
         gemm_run(pq, st);
         attn_decode(w.q, kvl, w.attn, aa, R, d.head_dim, st);
         GemmProblem po = gp(w.attn, w.rows, L.wo, d.d_model, R, d.d_model, hdH, EPI_RESID, true, w.x, d.d_model, live, &w);
-        resid_out(po, ss_b, ss_a);
+        resid_out(po, ss_b);
         gemm_run(po, st);
         GemmProblem pg = gp(xb, w.rows, L.wgu, 2 * d.ffn_dim, R, 2 * d.ffn_dim, d.d_model, EPI_SWIGLU, true, w.act,
                             d.ffn_dim, live, &w);
-        norm_in(pg, ss_b);
+        norm_in(pg, ss_b, parts);
         gemm_run(pg, st);
         GemmProblem pd = gp(w.act, w.rows, L.wd, d.d_model, R, d.d_model, d.ffn_dim, EPI_RESID, true, w.x, d.d_model,
                             live, &w);
-        resid_out(pd, ss_a, ss_b);
+        resid_out(pd, ss_a);
         gemm_run(pd, st);
     }
     GemmProblem pl = gp(xb, w.rows, m->lm, d.vocab, R, d.vocab, d.d_model, EPI_ARGMAX, true, nullptr, 0, live);
     pl.argmax = w.keys;
-    norm_in(pl, ss_a);  // argmax is scale invariant; kept so logits and argmax see one definition
+    norm_in(pl, ss_a, parts);  // argmax is scale invariant; kept so logits and argmax see one definition
     gemm_run(pl, st);
     finalize_tokens(w.keys, w.meta->slot, w.meta->out_index, R, live, kv->last_token, kv->out_tokens, kv->max_out, st);
 }
@@ -427,7 +429,8 @@ void decode_forward(sw_model* m, sw_kv* kv, const sw_batch& b, cudaStream_t st, 
     if (b.logits_out) {  // parity checks: fp32 logits from the same folded-norm input
         GemmProblem q = gp(m->dec.xn, m->dec.rows, m->lm, d.vocab, b.n, d.vocab, d.d_model, EPI_STORE_F32, true,
                            b.logits_out, d.vocab);
-        q.fx.row_ss = m->dec.ss;
+        q.fx.ss_parts = m->dec.ss;
+        q.fx.ss_nparts = d.d_model / 128;
         q.fx.norm_dim = d.d_model;
         q.fx.norm_eps = d.norm_eps;
         gemm_run(q, st);

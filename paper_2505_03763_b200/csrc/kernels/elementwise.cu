@@ -57,11 +57,11 @@ void checksum_bf16(const void* p, int64_t n, unsigned long long* out_dev, cudaSt
 // Decode step head, one CTA per row: install the step's new page, gather the
 // embedding of the fed token (the slot's device-resident last token unless
 // explicit tokens are given) and emit what the first fused GEMM consumes:
-// x (fp32 residual), bf16(x) (its B operand) and sum(x^2) (its RMSNorm scale);
-// also clears the second norm accumulator.
+// x (fp32 residual), bf16(x) (its B operand) and sum(x^2) (its RMSNorm scale,
+// as a single partial row).
 __global__ void embed_kernel(const StepMeta* __restrict__ meta, const __nv_bfloat16* __restrict__ emb,
                              float* __restrict__ x, __nv_bfloat16* __restrict__ xb, float* __restrict__ ss_a,
-                             float* __restrict__ ss_b, int d, const int32_t* __restrict__ last_token,
+                             int d, const int32_t* __restrict__ last_token,
                              int32_t* __restrict__ page_table, int max_pages, int page_tokens) {
     griddep_launch_dependents();
     griddep_wait();
@@ -93,14 +93,12 @@ __global__ void embed_kernel(const StepMeta* __restrict__ meta, const __nv_bfloa
         float t = 0.f;
         for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
         ss_a[row] = t;
-        ss_b[row] = 0.f;
     }
 }
 
 void embed(const StepMeta* meta, int max_rows, const __nv_bfloat16* emb, float* x, __nv_bfloat16* xb, float* ss_a,
-           float* ss_b, int d, const int32_t* last_token, int32_t* page_table, int max_pages, int page_tokens,
-           cudaStream_t st) {
-    launch_k(embed_kernel, dim3(max_rows), dim3(128), 0, st, meta, emb, x, xb, ss_a, ss_b, d, last_token, page_table,
+           int d, const int32_t* last_token, int32_t* page_table, int max_pages, int page_tokens, cudaStream_t st) {
+    launch_k(embed_kernel, dim3(max_rows), dim3(128), 0, st, meta, emb, x, xb, ss_a, d, last_token, page_table,
              max_pages, page_tokens);
 }
 

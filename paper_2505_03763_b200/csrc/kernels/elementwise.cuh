@@ -29,8 +29,7 @@ void fill_bf16(__nv_bfloat16* dst, int64_t n, float v, cudaStream_t st);
 void checksum_bf16(const void* p, int64_t n, unsigned long long* out_dev, cudaStream_t st);
 
 void embed(const StepMeta* meta, int max_rows, const __nv_bfloat16* emb, float* x, __nv_bfloat16* xb, float* ss_a,
-           float* ss_b, int d, const int32_t* last_token, int32_t* page_table, int max_pages, int page_tokens,
-           cudaStream_t st);
+           int d, const int32_t* last_token, int32_t* page_table, int max_pages, int page_tokens, cudaStream_t st);
 void embed_tokens(const int32_t* tokens, const int* n_tokens_dev, int rows, const __nv_bfloat16* emb, float* x, int d,
                   cudaStream_t st);
 void rmsnorm(const float* x, const __nv_bfloat16* g, __nv_bfloat16* y, int rows, int d, float eps, const int* rows_dev,

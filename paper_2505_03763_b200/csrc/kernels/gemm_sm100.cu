@@ -50,7 +50,8 @@ struct GemmCfg {
     static constexpr int kTmemCols = BN < 32 ? 32 : BN;
     // epilogue exchanges (SwiGLU / RoPE pairs, 128 x 33 fp32) reuse the drained stage ring
     static_assert(kStages * kStageBytes >= 128 * 33 * 4, "stage ring too small for the exchange buffer");
-    static constexpr int kSmem = 1024 + kStages * kStageBytes + 256;
+    static constexpr int kTokInfoBytes = 256 * 16;  // per-token 1/rms, position, KV offset (decode)
+    static constexpr int kSmem = 1024 + kStages * kStageBytes + kTokInfoBytes + 256;
 };
 
 __device__ __forceinline__ float silu_mul(float g, float u) { return g / (1.0f + __expf(-g)) * u; }
@@ -64,7 +65,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint8_t* sA = smem;
     uint8_t* sB = smem + C::kStages * C::kABytes;
     float* xchg = reinterpret_cast<float*>(sA);  // epilogue only: the ring is drained by then
-    uint64_t* full = reinterpret_cast<uint64_t*>(sB + C::kStages * C::kBBytes);
+    float* tok_inv = reinterpret_cast<float*>(sB + C::kStages * C::kBBytes);  // [256]
+    int* tok_pos = reinterpret_cast<int*>(tok_inv + 256);                       // [256]
+    long long* tok_kv = reinterpret_cast<long long*>(tok_pos + 256);            // [256]
+    uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(tok_inv) + C::kTokInfoBytes);
     uint64_t* empty = full + C::kStages;
     uint64_t* acc_ready = empty + C::kStages;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_ready + 1);
@@ -180,6 +184,27 @@ __global__ void __launch_bounds__(kThreads, 1)
         // ------------------------------------------------------------ epilogue
         const int quarter = warp & 3;  // TMEM lanes [32*quarter, 32*quarter+32)
         const int row = quarter * 32 + lane;  // accumulator row inside the tile
+        if constexpr (SWAP) {
+            // per-token epilogue inputs, gathered while the MMAs still run
+            const DecodeFusion& fx = args.fx;
+            const int nl = args.live_tokens ? min(args.valid_tokens, *args.live_tokens) : args.valid_tokens;
+            for (int t = threadIdx.x - 64; t < BN && n0 + t < nl; t += 128) {
+                const int tg = n0 + t;
+                if (fx.ss_parts) {
+                    float ss = 0.f;
+                    for (int p = 0; p < fx.ss_nparts; ++p) ss += fx.ss_parts[p * kSsStride + tg];
+                    tok_inv[t] = rsqrtf(ss / static_cast<float>(fx.norm_dim) + fx.norm_eps);
+                }
+                if constexpr (MODE == EPI_QKV_ROPE) {
+                    const int pos = fx.pos[tg];
+                    const int page = fx.page_table[static_cast<int64_t>(fx.slot[tg]) * fx.max_pages + pos / fx.page_tokens];
+                    tok_pos[t] = pos;
+                    tok_kv[t] = static_cast<long long>(page) * fx.page_stride +
+                                static_cast<long long>(pos % fx.page_tokens) * fx.hd;
+                }
+            }
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+        }
         mbar_wait(acc_ready, 0);
         tc_fence_after();
         const uint32_t tbase = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
@@ -265,8 +290,6 @@ __global__ void __launch_bounds__(kThreads, 1)
             // row = feature (weight row), columns = tokens
             const int f = m0 + row;
             const DecodeFusion& fx = args.fx;
-            if (fx.ss_zero && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0)
-                for (int t = threadIdx.x - 64; t < args.valid_tokens; t += 128) fx.ss_zero[t] = 0.f;
             // 32 fp32 values per lane -> lane j holds the sum over the warp of value j (31 shuffles)
             auto transpose_sum = [&](float (&v)[32]) {
 #pragma unroll
@@ -285,11 +308,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                 float v[32];
 #pragma unroll
                 for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(raw[j]);
-                if (fx.row_ss && MODE != EPI_RESID) {  // RMSNorm of the input rows, folded in
+                if (fx.ss_parts && MODE != EPI_RESID) {  // RMSNorm of the input rows, folded in
 #pragma unroll
                     for (int j = 0; j < 32; ++j)
-                        if (j < tcount)
-                            v[j] *= rsqrtf(__ldcg(fx.row_ss + n0 + c + j) / static_cast<float>(fx.norm_dim) + fx.norm_eps);
+                        if (j < tcount) v[j] *= tok_inv[c + j];
                 }
                 if constexpr (MODE == EPI_STORE) {
                     _Pragma("unroll") for (int j = 0; j < 32; ++j) if (j < tcount)
@@ -312,9 +334,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                         }
                         x[j] = j < tcount ? x[j] * x[j] : 0.f;
                     }
-                    if (fx.ss_out) {  // sum(x^2) of the updated rows for the next RMSNorm
-                        transpose_sum(x);
-                        if (lane < tcount) atomicAdd(fx.ss_out + n0 + c + lane, x[0]);
+                    if (fx.ss_part_out) {  // this tile's sum(x^2) per token, for the next RMSNorm
+                        transpose_sum(x);  // lane j: the warp's partial for token c + j
+                        xchg[quarter * 32 + lane] = x[0];
+                        asm volatile("bar.sync 1, 128;" ::: "memory");
+                        if (quarter == 0 && lane < tcount)  // fixed order over the 4 warps: deterministic
+                            fx.ss_part_out[static_cast<size_t>(blockIdx.y) * kSsStride + n0 + c + lane] =
+                                (xchg[lane] + xchg[32 + lane]) + (xchg[64 + lane] + xchg[96 + lane]);
+                        asm volatile("bar.sync 1, 128;" ::: "memory");
                     }
                 } else if constexpr (MODE == EPI_SWIGLU) {
                     // lanes 0-63 of the tile hold gate rows, 64-127 the matching up rows
@@ -352,7 +379,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     _Pragma("unroll") for (int j = 0; j < 32; ++j) {
                         if (j >= tcount) continue;
                         const int t = n0 + c + j;
-                        const int pos = fx.pos[t];
+                        const int pos = tok_pos[c + j];
                         float out = v[j];
                         if (!is_v) {
                             const float2 cs = fx.rope_cs[static_cast<int64_t>(pos) * half + (i & (half - 1))];
@@ -362,12 +389,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                         if (head < fx.H) {
                             fx.q_out[static_cast<size_t>(t) * fx.H * hd + f] = __float2bfloat16_rn(out);
                         } else {
-                            const int page = fx.page_table[static_cast<int64_t>(fx.slot[t]) * fx.max_pages + pos / fx.page_tokens];
                             const int kvh = is_v ? head - fx.H - fx.Hkv : head - fx.H;
-                            __nv_bfloat16* dst = fx.kv_layer + static_cast<int64_t>(page) * fx.page_stride +
-                                                 (is_v ? fx.page_stride / 2 : 0) +
-                                                 static_cast<int64_t>(kvh) * fx.page_tokens * hd +
-                                                 static_cast<int64_t>(pos % fx.page_tokens) * hd + i;
+                            __nv_bfloat16* dst = fx.kv_layer + tok_kv[c + j] + (is_v ? fx.page_stride / 2 : 0) +
+                                                 static_cast<int64_t>(kvh) * fx.page_tokens * hd + i;
                             *dst = __float2bfloat16_rn(out);
                         }
                     }

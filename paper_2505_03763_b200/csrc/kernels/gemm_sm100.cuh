@@ -17,18 +17,21 @@ enum GemmEpilogue : int {
     EPI_QKV_ROPE = 5,   // decode: RoPE on q/k heads, q -> bf16 buffer, k/v -> paged KV cache
 };
 
+constexpr int kSsStride = 256;  // tokens per sum(x^2) partial row (max decode rows)
+
 // Decode-only epilogue fusions (swap-AB).
 struct DecodeFusion {
-    // RMSNorm folded into the consumer GEMM: acc *= rsqrt(row_ss[t]/norm_dim + eps)
-    // (the gains are folded into the weights; B is the bf16 residual itself)
-    const float* row_ss = nullptr;
+    // RMSNorm folded into the consumer GEMM: acc *= rsqrt(sum_p ss_parts[p][t] / norm_dim + eps),
+    // partial sums of squares added in a fixed order (deterministic); the gains
+    // are folded into the weights and B is the bf16 residual itself
+    const float* ss_parts = nullptr;  // [ss_nparts][kSsStride]
+    int ss_nparts = 0;
     float norm_eps = 1e-5f;
     int norm_dim = 0;
-    // RESID producer side: write bf16(x) for the next GEMM and accumulate
-    // sum(x^2) per token into ss_out; zero ss_zero[0, n) for the norm after next
+    // RESID producer side: write bf16(x) for the next GEMM and this tile's
+    // partial sum(x^2) per token to ss_part_out[tile][t]
     __nv_bfloat16* x_bf16 = nullptr;
-    float* ss_out = nullptr;
-    float* ss_zero = nullptr;
+    float* ss_part_out = nullptr;
     // QKV_ROPE: per-token position / slot, page table, cos/sin table, outputs
     const int32_t* pos = nullptr;
     const int32_t* slot = nullptr;
