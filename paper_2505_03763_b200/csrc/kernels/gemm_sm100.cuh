@@ -53,10 +53,9 @@ struct GemmArgs {
     const int* live_tokens;  // optional device bound (graph-captured decode)
     unsigned long long* argmax;
     int feature_offset;
-    int splits;          // split-K factor (grid z)
-    float* ws;           // split-K partial tiles [tiles][splits][BN][128]
-    unsigned* counters;  // split-K arrival counters [tiles], zero between launches
-    int stagger;         // rotate each tile's K-block order (DRAM channel spread)
+    int stream_k;        // decode: (tile, K-block) iterations split evenly over the CTAs
+    float* ws;           // stream-K partial tiles [ctas][2][BN][128]
+    unsigned* counters;  // stream-K arrival counters [tiles], zero between launches
     DecodeFusion fx;
 };
 

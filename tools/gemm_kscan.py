@@ -43,7 +43,7 @@ def t(feat, K, rows=64, epi=4, reps=20):
 
 
 if __name__ == "__main__":
-    os.environ.setdefault("SW_GEMM_SPLITS", "1")
+    pass
     for feat in (128, 128 * 148):
         for K in (64, 256, 1024, 2048, 4096, 8192):
             us, gbs = t(feat, K)
