@@ -50,6 +50,7 @@ constexpr int BK = 64;
 constexpr int kProducers = 2;
 constexpr int kThreads = 256;  // 8 warps
 constexpr int kEpiBase = 128;  // first epilogue thread (warp 4)
+constexpr int kMaxContrib = 8;  // stream-K: CTAs contributing to one tile (host enforces)
 
 template <int BN>
 struct GemmCfg {
@@ -511,12 +512,19 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const long long t0 = static_cast<long long>(g.tile) * sc.nk;
                 const int c_first = sc.owner(t0), c_last = sc.owner(t0 + sc.nk - 1);
                 const int slot = sc.beg(sc.c) >= t0 ? 0 : 1;  // the CTA's first or last segment
+                // partial layout [BN/8][128 rows][8]: a thread's 8 columns are 32 contiguous bytes
                 float* part = args.ws + (static_cast<size_t>(sc.c) * 2 + slot) * BN * 128;
                 for (int c = 0; c < BN; c += 32) {
                     tmem_ld32(tb + c, r);
                     tmem_ld_wait();
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) __stcg(part + static_cast<size_t>(c + j) * 128 + row, __uint_as_float(r[j]));
+                    for (int q = 0; q < 4; ++q) {
+                        float4* dst = reinterpret_cast<float4*>(part + ((static_cast<size_t>(c / 8 + q) * 128 + row) * 8));
+                        __stcg(dst, make_float4(__uint_as_float(r[8 * q]), __uint_as_float(r[8 * q + 1]),
+                                                __uint_as_float(r[8 * q + 2]), __uint_as_float(r[8 * q + 3])));
+                        __stcg(dst + 1, make_float4(__uint_as_float(r[8 * q + 4]), __uint_as_float(r[8 * q + 5]),
+                                                    __uint_as_float(r[8 * q + 6]), __uint_as_float(r[8 * q + 7])));
+                    }
                 }
                 release_acc(a);
                 __threadfence();
@@ -528,15 +536,34 @@ __global__ void __launch_bounds__(kThreads, 1)
                 asm volatile("bar.sync 2, 128;" ::: "memory");
                 if (*last_flag) {
                     __threadfence();
+                    const int ncon = c_last - c_first + 1;
                     for (int c = 0; c < BN; c += 32) {
                         float v[32];
 #pragma unroll
-                        for (int j = 0; j < 32; ++j) v[j] = 0.f;
-                        for (int cc = c_first; cc <= c_last; ++cc) {  // CTA order: deterministic
-                            const int sl = sc.beg(cc) >= t0 ? 0 : 1;
-                            const float* pp = args.ws + (static_cast<size_t>(cc) * 2 + sl) * BN * 128;
+                        for (int q = 0; q < 4; ++q) {  // 8 columns at a time, every contributor's load in flight
+                            float4 lo[kMaxContrib], hi[kMaxContrib];
 #pragma unroll
-                            for (int j = 0; j < 32; ++j) v[j] += __ldcg(pp + static_cast<size_t>(c + j) * 128 + row);
+                            for (int k = 0; k < kMaxContrib; ++k) {
+                                if (k < ncon) {
+                                    const int cc = c_first + k;
+                                    const int sl = sc.beg(cc) >= t0 ? 0 : 1;
+                                    const float4* pp = reinterpret_cast<const float4*>(
+                                        args.ws + (static_cast<size_t>(cc) * 2 + sl) * BN * 128 +
+                                        (static_cast<size_t>(c / 8 + q) * 128 + row) * 8);
+                                    lo[k] = __ldcg(pp);
+                                    hi[k] = __ldcg(pp + 1);
+                                }
+                            }
+                            float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+                            for (int k = 0; k < kMaxContrib; ++k) {  // contributor (CTA) order: deterministic
+                                if (k < ncon) {
+                                    acc[0] += lo[k].x; acc[1] += lo[k].y; acc[2] += lo[k].z; acc[3] += lo[k].w;
+                                    acc[4] += hi[k].x; acc[5] += hi[k].y; acc[6] += hi[k].z; acc[7] += hi[k].w;
+                                }
+                            }
+#pragma unroll
+                            for (int j = 0; j < 8; ++j) v[8 * q + j] = acc[j];
                         }
                         emit_swap(m0, c, v);
                     }
@@ -661,10 +688,15 @@ void gemm_run(const GemmProblem& p, cudaStream_t st) {
         const long long iters = static_cast<long long>(tiles) * (p.K / BK);
         // Stream-K over every SM when there is split-K scratch; the split
         // depends on the weight shape only, never on the batch.
+        // At most kMaxContrib CTAs per tile: each CTA gets >= nk/(kMaxContrib-1)
+        // K-blocks (a CTA range can straddle two tiles).
+        const int nk = p.K / BK;
+        const long long min_iters = std::max(2, cdiv(nk, kMaxContrib - 1));
+        const int sk_ctas = static_cast<int>(std::min<long long>(sms, iters / min_iters));
         const bool sk = p.ws && p.counters && tiles <= p.n_counters &&
-                        static_cast<size_t>(sms) * 2 * bn * BM <= p.ws_floats && iters > tiles;
+                        static_cast<size_t>(sms) * 2 * bn * BM <= p.ws_floats && sk_ctas > tiles;
         a.stream_k = sk ? 1 : 0;
-        const int ctas = sk ? static_cast<int>(std::min<long long>(sms, iters)) : std::min(sms, tiles);
+        const int ctas = sk ? sk_ctas : std::min(sms, tiles);
         const CUtensorMap& ta = tmap_cached(p.W, p.w_rows, p.K, BM);
         const CUtensorMap& tb = tmap_cached(p.X, p.x_rows, p.K, bn);
         switch (p.mode) {
