@@ -6,6 +6,7 @@
 #include "capi_util.hpp"
 
 #include <atomic>
+#include <cstdlib>
 
 namespace sw {
 std::atomic<unsigned long long> g_launches{0};
@@ -14,6 +15,13 @@ std::atomic<unsigned long long> g_h2d{0}, g_d2h{0};
 bool& pdl_mode() {
     thread_local bool on = false;
     return on;
+}
+bool pdl_allowed() {  // SW_PDL=1 enables programmatic dependent launch (measured slower: off)
+    static const bool ok = [] {
+        const char* v = std::getenv("SW_PDL");
+        return v && v[0] == '1';
+    }();
+    return ok;
 }
 void count_transfer(unsigned long long h2d, unsigned long long d2h) {
     g_h2d.fetch_add(h2d, std::memory_order_relaxed);

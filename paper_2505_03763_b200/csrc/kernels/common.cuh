@@ -44,6 +44,7 @@ __device__ __forceinline__ void griddep_launch_dependents() { asm volatile("grid
 // Thread-local launch mode: when set (the decode step), launch_k() attaches the
 // programmatic-stream-serialization attribute (kept when captured in a graph).
 bool& pdl_mode();
+bool pdl_allowed();
 struct PdlScope {
     bool prev;
     explicit PdlScope(bool on) : prev(pdl_mode()) { pdl_mode() = on; }
@@ -58,7 +59,7 @@ void launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cuda
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
-    if (pdl_mode()) {
+    if (pdl_mode() && pdl_allowed()) {
         attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
         attr[0].val.programmaticStreamSerializationAllowed = 1;
         cfg.attrs = attr;

@@ -693,7 +693,15 @@ void gemm_run(const GemmProblem& p, cudaStream_t st) {
         const int nk = p.K / BK;
         const long long min_iters = std::max(2, cdiv(nk, kMaxContrib - 1));
         const int sk_ctas = static_cast<int>(std::min<long long>(sms, iters / min_iters));
-        const bool sk = p.ws && p.counters && tiles <= p.n_counters &&
+        static const int sk_env = [] {
+            const char* v = std::getenv("SW_GEMM_SK");
+            return v && *v ? std::atoi(v) : -1;
+        }();
+        // Measured (tools/gemm_shapes.py, profiles/r01/gemm_shapes.txt): stream-K only
+        // pays for long-K projections over few tiles (Wd); shorter ones are
+        // faster as whole tiles (no partial-tile fixup).
+        const bool sk_shape = nk >= 96 && tiles * 2 <= sms;
+        const bool sk = (sk_env > 0 || (sk_env < 0 && sk_shape)) && p.ws && p.counters && tiles <= p.n_counters &&
                         static_cast<size_t>(sms) * 2 * bn * BM <= p.ws_floats && sk_ctas > tiles;
         a.stream_k = sk ? 1 : 0;
         const int ctas = sk ? sk_ctas : std::min(sms, tiles);
