@@ -24,6 +24,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstddef>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -331,6 +332,14 @@ void decode_layers(sw_model* m, sw_kv* kv, int R, cudaStream_t st) {
     aa.part_o = w.part_o;
     aa.part_ml = w.part_ml;
     aa.counters = w.attn_cnt;
+    {
+        static const int target = [] {
+            const char* v = std::getenv("SW_ATTN_CTAS");
+            return v && *v ? std::atoi(v) : 296;
+        }();
+        aa.target_ctas = target;
+        aa.max_ctx = kv->max_pages * kv->page_tokens;
+    }
     auto norm_in = [&](GemmProblem& p, const float* ss, int nparts) {
         p.fx.ss_parts = ss;
         p.fx.ss_nparts = nparts;

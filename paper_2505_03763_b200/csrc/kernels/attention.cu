@@ -9,6 +9,8 @@
 // Decode: split-KV paged attention on the tensor cores (see below); the G =
 //   H/Hkv query heads sharing a kv head are packed into one mma tile so every
 //   K/V byte is read once per step.  HBM-bound by design.
+#include <algorithm>
+
 #include "attention.cuh"
 #include "common.cuh"
 
@@ -53,6 +55,8 @@ __device__ __forceinline__ int swz(int row, int chunk) {
 
 constexpr int kQRows = 64;
 constexpr int kKeys = 64;
+constexpr int kPage = 16;        // tokens per KV page (fixed: shifts, not divisions, in the address math)
+constexpr int kPartSplits = 16;  // stride of the split-partial buffers (>= any grid x)
 constexpr int kMaxChunkPages = 512;  // page ids of one decode split staged in smem (8192 keys)
 
 template <int HD>
@@ -90,10 +94,10 @@ __global__ void __launch_bounds__(128) attn_prefill_kernel(const __nv_bfloat16* 
             const int r = i / CH, c = i % CH;
             const int key = blk * kKeys + r;
             const bool ok = key < len;
-            const int page = ok ? ptab[key / a.page_tokens] : 0;
+            const int page = ok ? ptab[key / kPage] : 0;
             const __nv_bfloat16* base = kv_layer + static_cast<int64_t>(page) * a.page_stride +
-                                        static_cast<int64_t>(hk) * a.page_tokens * HD +
-                                        static_cast<int64_t>(key % a.page_tokens) * HD + c * 8;
+                                        static_cast<int64_t>(hk) * kPage * HD +
+                                        static_cast<int64_t>(key % kPage) * HD + c * 8;
             cp_async16(sK + buf * kKeys * HD + swz<HD>(r, c), base, ok);
             cp_async16(sV + buf * kKeys * HD + swz<HD>(r, c), base + a.kv_stride, ok);
         }
@@ -260,11 +264,11 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(const __nv_bfloat16* _
     const int row = blockIdx.z;
     if (row >= n_rows) return;
     const int ctx = a.meta->pos[row] + 1;
-    // splits chosen at run time: only as many as it takes to give the GPU
-    // ~4 CTAs per SM, each warp keeping >= 1 key block
-    const int want = cdiv(148 * 4, n_rows * a.Hkv);
-    const int splits0 = max(cdiv(ctx, kMaxChunkPages * a.page_tokens),
-                            max(1, min(min(want, a.max_splits), cdiv(ctx, 4 * KB))));
+    // splits chosen at run time: only as many as it takes to reach
+    // a.target_ctas CTAs, each warp keeping >= 1 key block
+    const int want = cdiv(a.target_ctas, n_rows * a.Hkv);
+    const int splits0 = max(cdiv(ctx, kMaxChunkPages * kPage),
+                            max(1, min(min(want, static_cast<int>(gridDim.x)), cdiv(ctx, 4 * KB))));
     const int chunk = cdiv(cdiv(ctx, splits0), KB) * KB;
     const int splits = cdiv(ctx, chunk);  // every split non-empty
     const int split = blockIdx.x;
@@ -275,10 +279,10 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(const __nv_bfloat16* _
     const int hk = blockIdx.y;
     {  // this split's page ids -> smem (one read per page, not per 16 B chunk)
         const int32_t* ptab = a.page_table + static_cast<int64_t>(a.meta->slot[row]) * a.max_pages;
-        const int p0 = k_begin / a.page_tokens, p1 = (k_end - 1) / a.page_tokens;
+        const int p0 = k_begin / kPage, p1 = (k_end - 1) / kPage;
         for (int i = threadIdx.x; i <= p1 - p0; i += 128) s_pages[i] = ptab[p0 + i];
     }
-    const int page_base = k_begin / a.page_tokens;
+    const int page_base = k_begin / kPage;
     const int n_blocks = cdiv(k_end - k_begin, KB);
 
     // Q fragment (A operand, rows = query heads of this kv head)
@@ -300,10 +304,10 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(const __nv_bfloat16* _
             const int kr = i / CH, c = i % CH;
             const int key = k0 + kr;
             const bool ok = key < k_end;
-            const int page = ok ? s_pages[key / a.page_tokens - page_base] : 0;
+            const int page = ok ? s_pages[key / kPage - page_base] : 0;
             const __nv_bfloat16* src = kv_layer + static_cast<int64_t>(page) * a.page_stride +
-                                       static_cast<int64_t>(hk) * a.page_tokens * HD +
-                                       static_cast<int64_t>(key % a.page_tokens) * HD + c * 8;
+                                       static_cast<int64_t>(hk) * kPage * HD +
+                                       static_cast<int64_t>(key % kPage) * HD + c * 8;
             cp_async16(wK + buf * KB * HD + swz<HD>(kr, c), src, ok);
             cp_async16(wV + buf * KB * HD + swz<HD>(kr, c), src + a.kv_stride, ok);
         }
@@ -412,7 +416,7 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(const __nv_bfloat16* _
         }
     }
     __syncthreads();
-    const int64_t pidx = (static_cast<int64_t>(row) * a.Hkv + hk) * a.max_splits + split;
+    const int64_t pidx = (static_cast<int64_t>(row) * a.Hkv + hk) * kPartSplits + split;
     for (int idx = threadIdx.x; idx < G * HD; idx += 128) {
         const int g = idx / HD, d = idx % HD;
         float M = -INFINITY;
@@ -447,7 +451,7 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(const __nv_bfloat16* _
     __syncthreads();
     if (!s_last) return;
     __threadfence();
-    const int64_t base = (static_cast<int64_t>(row) * a.Hkv + hk) * a.max_splits;
+    const int64_t base = (static_cast<int64_t>(row) * a.Hkv + hk) * kPartSplits;
     for (int idx = threadIdx.x; idx < G * HD; idx += 128) {
         const int g = idx / HD;
         float M = -INFINITY;
@@ -472,8 +476,13 @@ void decode_launch(const __nv_bfloat16* q, const __nv_bfloat16* kv_layer, __nv_b
         SW_CUDA(cudaFuncSetAttribute(attn_decode_kernel<HD, G, KB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         cfg = true;
     }
-    dim3 grid(a.max_splits, a.Hkv, max_rows);
-    launch_k(attn_decode_kernel<HD, G, KB>, grid, dim3(128), smem, st, q, kv_layer, out, a);
+    // grid x: the most splits any row can take at this bucket size (the kernel
+    // picks <= gridDim.x per row at run time), plus what the smem page list needs
+    DecodeAttnArgs args = a;
+    const int want = std::max(1, std::min(a.max_splits, cdiv(a.target_ctas, max_rows * a.Hkv)));
+    args.max_splits = std::max(want, cdiv(a.max_ctx, kMaxChunkPages * kPage));
+    dim3 grid(args.max_splits, a.Hkv, max_rows);
+    launch_k(attn_decode_kernel<HD, G, KB>, grid, dim3(128), smem, st, q, kv_layer, out, args);
 }
 
 }  // namespace

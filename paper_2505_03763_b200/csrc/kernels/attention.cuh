@@ -39,6 +39,8 @@ struct DecodeAttnArgs {
     float* part_o;   // [rows][Hkv][max_splits][G][hd]
     float* part_ml;  // [rows][Hkv][max_splits][G][2]
     unsigned* counters;  // [rows][Hkv] split arrivals, zero between launches
+    int target_ctas;     // split-KV: split until rows * Hkv * splits reaches this
+    int max_ctx;         // longest context the arena holds (sizes the grid)
 };
 
 void attn_prefill(const __nv_bfloat16* q, const __nv_bfloat16* kv_layer, __nv_bfloat16* out, const PrefillAttnArgs& a,
