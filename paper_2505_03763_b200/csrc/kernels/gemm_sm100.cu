@@ -39,6 +39,7 @@
 #include <tuple>
 
 #include "common.cuh"
+#include "gemm_epilogue.cuh"
 #include "gemm_sm100.cuh"
 
 namespace sw {
@@ -66,8 +67,6 @@ struct GemmCfg {
     static constexpr int kBarBytes = 512;
     static constexpr int kSmem = 1024 + kStages * kStageBytes + kXchgBytes + kTokBytes + kBarBytes;
 };
-
-__device__ __forceinline__ float silu_mul(float g, float u) { return g / (1.0f + __expf(-g)) * u; }
 
 // Static work schedule shared by every role of a CTA.
 struct Sched {
@@ -283,116 +282,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             asm volatile("bar.sync 1, 128;" ::: "memory");
         }
 
-        // 32 fp32 values per lane -> lane j holds the warp sum of value j (31 shuffles)
-        auto transpose_sum = [&](float (&v)[32]) {
-#pragma unroll
-            for (int off = 16; off >= 1; off >>= 1) {
-                const bool upper = (lane & off) != 0;
-#pragma unroll
-                for (int i = 0; i < off; ++i) {
-                    const float send = upper ? v[i] : v[i + off];
-                    const float keep = upper ? v[i + off] : v[i];
-                    v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
-                }
-            }
-        };
-
-        // swap mode: row = feature f of tile m0, columns = tokens [0, BN)
-        auto emit_swap = [&](int m0, int c, const float (&vin)[32]) {
-            const int f = m0 + row;
-            const int tcount = min(32, n_live - c);
-            float v[32];
-#pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] = vin[j];
-            if (fx.ss_parts && MODE != EPI_RESID) {  // RMSNorm of the input rows, folded in
-#pragma unroll
-                for (int j = 0; j < 32; ++j)
-                    if (j < tcount) v[j] *= tok_inv[c + j];
-            }
-            if constexpr (MODE == EPI_STORE) {
-                _Pragma("unroll") for (int j = 0; j < 32; ++j) if (j < tcount)
-                    static_cast<__nv_bfloat16*>(args.out)[static_cast<size_t>(c + j) * args.ldo + f] =
-                        __float2bfloat16_rn(v[j]);
-            } else if constexpr (MODE == EPI_STORE_F32) {
-                _Pragma("unroll") for (int j = 0; j < 32; ++j) if (j < tcount)
-                    static_cast<float*>(args.out)[static_cast<size_t>(c + j) * args.ldo + f] = v[j];
-            } else if constexpr (MODE == EPI_RESID) {
-                float* col = static_cast<float*>(args.out) + static_cast<size_t>(c) * args.ldo + f;
-                float x[32];
-                _Pragma("unroll") for (int j = 0; j < 32; ++j) x[j] =
-                    j < tcount ? __ldcg(col + static_cast<size_t>(j) * args.ldo) : 0.f;
-                _Pragma("unroll") for (int j = 0; j < 32; ++j) {
-                    x[j] += v[j];
-                    if (j < tcount) {
-                        col[static_cast<size_t>(j) * args.ldo] = x[j];
-                        if (fx.x_bf16) fx.x_bf16[static_cast<size_t>(c + j) * args.ldo + f] = __float2bfloat16_rn(x[j]);
-                    }
-                    x[j] = j < tcount ? x[j] * x[j] : 0.f;
-                }
-                if (fx.ss_part_out) {  // this tile's sum(x^2) per token, for the next RMSNorm
-                    transpose_sum(x);  // lane j: the warp's partial for token c + j
-                    xchg[quarter * 32 + lane] = x[0];
-                    asm volatile("bar.sync 1, 128;" ::: "memory");
-                    if (quarter == 0 && lane < tcount)  // fixed order over the 4 warps: deterministic
-                        fx.ss_part_out[static_cast<size_t>(m0 / BM) * kSsStride + c + lane] =
-                            (xchg[lane] + xchg[32 + lane]) + (xchg[64 + lane] + xchg[96 + lane]);
-                    asm volatile("bar.sync 1, 128;" ::: "memory");
-                }
-            } else if constexpr (MODE == EPI_SWIGLU) {
-                // lanes 0-63 of the tile hold gate rows, 64-127 the matching up rows
-                if (row >= 64) {
-#pragma unroll
-                    for (int j = 0; j < 32; ++j) xchg[(row - 64) * 33 + j] = v[j];
-                }
-                asm volatile("bar.sync 1, 128;" ::: "memory");
-                if (row < 64) {
-                    const int gi = m0 / 2 + row;
-                    _Pragma("unroll") for (int j = 0; j < 32; ++j) if (j < tcount)
-                        static_cast<__nv_bfloat16*>(args.out)[static_cast<size_t>(c + j) * args.ldo + gi] =
-                            __float2bfloat16_rn(silu_mul(v[j], xchg[row * 33 + j]));
-                }
-                asm volatile("bar.sync 1, 128;" ::: "memory");
-            } else if constexpr (MODE == EPI_ARGMAX) {
-                _Pragma("unroll") for (int j = 0; j < 32; ++j) if (j < tcount) {
-                    unsigned long long key = argmax_key(v[j], static_cast<uint32_t>(args.feature_offset + f));
-#pragma unroll
-                    for (int o = 16; o > 0; o >>= 1) {
-                        const unsigned long long other = __shfl_xor_sync(0xffffffffu, key, o);
-                        key = other > key ? other : key;
-                    }
-                    if (lane == 0) atomicMax(args.argmax + c + j, key);
-                }
-            } else if constexpr (MODE == EPI_QKV_ROPE) {
-                // rotate-half RoPE: row r pairs with r ^ (hd/2) inside its head
-                const int hd = fx.hd, half = hd >> 1;
-                const int head = f / hd, i = f % hd;
-#pragma unroll
-                for (int j = 0; j < 32; ++j) xchg[row * 33 + j] = v[j];
-                asm volatile("bar.sync 1, 128;" ::: "memory");
-                const int prow = row ^ half;
-                const bool is_v = head >= fx.H + fx.Hkv;
-                _Pragma("unroll") for (int j = 0; j < 32; ++j) {
-                    if (j >= tcount) continue;
-                    const int t = c + j;
-                    const int pos = tok_pos[t];
-                    float out = v[j];
-                    if (!is_v) {
-                        const float2 cs = fx.rope_cs[static_cast<int64_t>(pos) * half + (i & (half - 1))];
-                        const float b = xchg[prow * 33 + j];
-                        out = i < half ? v[j] * cs.x - b * cs.y : v[j] * cs.x + b * cs.y;
-                    }
-                    if (head < fx.H) {
-                        fx.q_out[static_cast<size_t>(t) * fx.H * hd + f] = __float2bfloat16_rn(out);
-                    } else {
-                        const int kvh = is_v ? head - fx.H - fx.Hkv : head - fx.H;
-                        __nv_bfloat16* dst = fx.kv_layer + tok_kv[t] + (is_v ? fx.page_stride / 2 : 0) +
-                                             static_cast<int64_t>(kvh) * fx.page_tokens * hd + i;
-                        *dst = __float2bfloat16_rn(out);
-                    }
-                }
-                asm volatile("bar.sync 1, 128;" ::: "memory");
-            }
-        };
+        SwapEpi E{&args, xchg, tok_inv, tok_pos, tok_kv, row, lane, quarter, n_live};
+        auto emit_swap_l = [&](int m0, int c, const float (&v)[32]) { emit_swap<MODE>(E, m0, c, v); };
 
         // normal mode: row = token m0 + row, columns = features n0 + [c, c + 32)
         auto emit_normal = [&](int m0, int n0, int c, const uint32_t (&r)[32]) {
@@ -505,7 +396,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     float v[32];
 #pragma unroll
                     for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-                    emit_swap(m0, c, v);
+                    emit_swap_l(m0, c, v);
                 }
             } else {
                 // stream-K partial tile: park it, the last contributor reduces
@@ -565,7 +456,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                             for (int j = 0; j < 8; ++j) v[8 * q + j] = acc[j];
                         }
-                        emit_swap(m0, c, v);
+                        emit_swap_l(m0, c, v);
                     }
                     if (e == 0) args.counters[g.tile] = 0u;  // re-arm for the next launch
                 }
@@ -595,6 +486,11 @@ EncodeTiled encode_fn() {
         return reinterpret_cast<EncodeTiled>(p);
     }();
     return fn;
+}
+
+int env_flag(const char* name, int dflt) {
+    const char* v = std::getenv(name);
+    return v && *v ? std::atoi(v) : dflt;
 }
 
 int num_sms() {
@@ -685,6 +581,15 @@ void gemm_run(const GemmProblem& p, cudaStream_t st) {
         a.M = p.features;
         a.N = bn;
         const int tiles = p.features / BM;
+        static const int cl_env = env_flag("SW_GEMM_CLUSTER", 1);
+        if (cl_env && bn <= 64 && p.mode != EPI_ARGMAX && tiles < 2 * sms) {
+            // decode projections: a tile per cluster of k CTAs, reduced through DSMEM
+            const int k = gemm_cluster_size(tiles, p.K / BK, sms);
+            a.stream_k = 0;
+            gemm_cluster_run(tmap_cached(p.W, p.w_rows, p.K, BM), tmap_cached(p.X, p.x_rows, p.K, bn), a, bn, k,
+                             tiles, st);
+            return;
+        }
         const long long iters = static_cast<long long>(tiles) * (p.K / BK);
         // Stream-K over every SM when there is split-K scratch; the split
         // depends on the weight shape only, never on the batch.
