@@ -581,7 +581,7 @@ void gemm_run(const GemmProblem& p, cudaStream_t st) {
         a.M = p.features;
         a.N = bn;
         const int tiles = p.features / BM;
-        static const int cl_env = env_flag("SW_GEMM_CLUSTER", 1);
+        static const int cl_env = env_flag("SW_GEMM_CLUSTER", 0);  // measured slower at b=64 (profiles/r01)
         if (cl_env && bn <= 64 && p.mode != EPI_ARGMAX && tiles < 2 * sms) {
             // decode projections: a tile per cluster of k CTAs, reduced through DSMEM
             const int k = gemm_cluster_size(tiles, p.K / BK, sms);
