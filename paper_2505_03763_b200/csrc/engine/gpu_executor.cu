@@ -171,7 +171,7 @@ public:
         LogRecord end;
         end.kind = LogKind::RunEnd;
         append(end, {t_end});
-        finalize_times([&](int ev) { return elapsed(ev); });
+        clock_skew_ = finalize_times([&](int ev) { return elapsed(ev); }, /*align_device_clock=*/true);
         // RunEnd must stay last: after sorting it is (all stamps <= clock_).
         return log_;
     }
@@ -198,8 +198,9 @@ public:
             s += "\n";
         }
         char buf[256];
-        std::snprintf(buf, sizeof buf, "#gpu launches=%zu;prefill_launches=%d;decode_launches=%d;split=%d;coalesce=%d\n",
-                      launches_.size(), n_prefill_, n_decode_, opt_.split ? 1 : 0, opt_.coalesce ? 1 : 0);
+        std::snprintf(buf, sizeof buf,
+                      "#gpu launches=%zu;prefill_launches=%d;decode_launches=%d;split=%d;coalesce=%d;clock_skew_s=%.9g\n",
+                      launches_.size(), n_prefill_, n_decode_, opt_.split ? 1 : 0, opt_.coalesce ? 1 : 0, clock_skew_);
         s += buf;
         return s;
     }
@@ -351,6 +352,7 @@ private:
     std::vector<Launch> launches_;
     std::map<int, int> slot_of_;
     unsigned long long polls_ = 0;
+    double clock_skew_ = 0.0;
     int n_prefill_ = 0, n_decode_ = 0;
 };
 
@@ -383,8 +385,14 @@ extern "C" int sw_engine_run(sw_model* m, sw_kv* kv, const char* spec, char** ou
         const auto w0 = std::chrono::steady_clock::now();
         const EventLog log = ex.run();
         const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - w0).count();
-        const MetricsReport rep = build_report(log);
-        std::string text = serialize_event_log(log) + render_report(rep) + render_pages(ex.pages()) + ex.extras();
+        std::string text = serialize_event_log(log);
+        try {
+            text += render_report(build_report(log));
+        } catch (const ContractViolation& e) {
+            g_last_error = std::string("ContractViolation: ") + e.what();
+            text += std::string("#report_error ") + e.what() + "\n";
+        }
+        text += render_pages(ex.pages()) + ex.extras();
         text += "#wall wall_s=" + fmt17(wall) + "\n";
         *out = dup_text(text);
     });

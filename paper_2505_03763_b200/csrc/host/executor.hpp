@@ -26,6 +26,7 @@
 // the reference's.
 #pragma once
 
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <limits>
@@ -290,15 +291,31 @@ protected:
 
     // Resolve deferred stamps and restore time order (stable, so records that
     // share a timestamp keep their causal order).
+    // Device-clock backends: after resolving the deferred stamps, shift every
+    // non-arrival record by the smallest delta >= 0 that puts each prompt at or
+    // after its requests' (nominal, host-clock) arrivals.  This absorbs skew
+    // between the host clock that paces arrivals and the GPU event clock while
+    // keeping every device-measured duration and ordering.  Returns the delta.
     template <class Resolve>
-    void finalize_times(Resolve&& resolve) {
+    double finalize_times(Resolve&& resolve, bool align_device_clock = false) {
         bool deferred = false;
         for (std::size_t i = 0; i < log_.records.size(); ++i)
             if (stamps_[i] >= 0) {
                 log_.records[i].time_s = resolve(stamps_[i]);
                 deferred = true;
             }
-        if (!deferred) return;
+        if (!deferred) return 0.0;
+        double delta = 0.0;
+        if (align_device_clock) {
+            for (const LogRecord& r : log_.records) {
+                if (r.kind != LogKind::TaskStart || r.task_kind != TaskKind::Prompt) continue;
+                for (int rid : log_.batches[static_cast<std::size_t>(r.batch_id)])
+                    delta = std::max(delta, entry(rid).req.arrival_s - r.time_s);
+            }
+            if (delta > 0.0)
+                for (LogRecord& r : log_.records)
+                    if (r.kind != LogKind::Arrival) r.time_s += delta;
+        }
         std::vector<std::size_t> order(log_.records.size());
         for (std::size_t i = 0; i < order.size(); ++i) order[i] = i;
         std::stable_sort(order.begin(), order.end(), [&](std::size_t a, std::size_t b) {
@@ -308,6 +325,7 @@ protected:
         sorted.reserve(order.size());
         for (std::size_t i : order) sorted.push_back(log_.records[i]);
         log_.records.swap(sorted);
+        return delta;
     }
 
     SimulationInputs in_;
