@@ -42,6 +42,7 @@ namespace sw {
 
 struct GpuOptions {
     bool split = true;        // two streams (prefill || decode) vs one
+    int decode_lanes = 1;     // split mode: concurrent decode streams (instance i -> lane i % lanes)
     bool coalesce = true;     // one launch per kind per pass
     bool graphs = true;       // CUDA graphs for decode steps
     double peak_flops = 1.6932e15;
@@ -88,15 +89,20 @@ public:
         int lo, hi;
         SW_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
         SW_CUDA(cudaStreamCreateWithPriority(&s_prefill_, cudaStreamNonBlocking, lo));
-        if (opt_.split) SW_CUDA(cudaStreamCreateWithPriority(&s_decode_, cudaStreamNonBlocking, hi));
-        else s_decode_ = s_prefill_;
+        const int lanes = opt_.split ? std::max(1, std::min(opt_.decode_lanes, sw_model::kMaxDecodeLanes)) : 1;
+        for (int i = 0; i < lanes; ++i) {
+            cudaStream_t s = s_prefill_;
+            if (opt_.split) SW_CUDA(cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, hi));
+            s_decode_.push_back(s);
+        }
     }
 
     ~GpuExecutor() override {
         cudaStreamSynchronize(s_prefill_);
-        cudaStreamSynchronize(s_decode_);
+        for (cudaStream_t s : s_decode_) cudaStreamSynchronize(s);
         for (cudaEvent_t e : events_) cudaEventDestroy(e);
-        if (s_decode_ != s_prefill_) cudaStreamDestroy(s_decode_);
+        for (cudaStream_t s : s_decode_)
+            if (s != s_prefill_) cudaStreamDestroy(s);
         cudaStreamDestroy(s_prefill_);
     }
 
@@ -199,8 +205,10 @@ public:
         }
         char buf[256];
         std::snprintf(buf, sizeof buf,
-                      "#gpu launches=%zu;prefill_launches=%d;decode_launches=%d;split=%d;coalesce=%d;clock_skew_s=%.9g\n",
-                      launches_.size(), n_prefill_, n_decode_, opt_.split ? 1 : 0, opt_.coalesce ? 1 : 0, clock_skew_);
+                      "#gpu launches=%zu;prefill_launches=%d;decode_launches=%d;split=%d;coalesce=%d;decode_lanes=%zu;"
+                      "clock_skew_s=%.9g\n",
+                      launches_.size(), n_prefill_, n_decode_, opt_.split ? 1 : 0, opt_.coalesce ? 1 : 0,
+                      s_decode_.size(), clock_skew_);
         s += buf;
         return s;
     }
@@ -237,6 +245,7 @@ protected:
 private:
     struct Launch {
         TaskKind kind;
+        int lane = 0;
         int start_ev = -1, end_ev = -1;
         std::vector<long long> task_seqs;
         long long first_seq = 0;
@@ -262,16 +271,21 @@ private:
         if (trs.empty()) return;
         // group: coalesced -> one launch per kind; else one per task
         std::vector<Launch> group;
-        int prompt_launch = -1, step_launch = -1;
+        int prompt_launch = -1;
         std::vector<std::pair<int, std::size_t>> placement;  // (launch idx in group, active idx)
+        std::map<int, int> step_launch_of_lane;
         for (const TaskRequest& tr : trs) {
             int gi;
-            int& slot = tr.kind == TaskKind::Prompt ? prompt_launch : step_launch;
+            const int lane = static_cast<int>(tr.instance_id % static_cast<int>(s_decode_.size()));
+            int& slot = tr.kind == TaskKind::Prompt ? prompt_launch
+                                                    : (step_launch_of_lane.count(lane) ? step_launch_of_lane[lane]
+                                                                                       : (step_launch_of_lane[lane] = -1));
             if (opt_.coalesce && slot >= 0) {
                 gi = slot;
             } else {
                 Launch L;
                 L.kind = tr.kind;
+                L.lane = lane;
                 L.start_ev = new_event();
                 L.end_ev = new_event();
                 group.push_back(L);
@@ -335,9 +349,10 @@ private:
             b.positions = pos.data();
             b.new_page = newp.data();
             b.out_index = oidx.data();
-            SW_CUDA(cudaEventRecord(events_[L.start_ev], s_decode_));
-            decode_forward(m_, kv_, b, s_decode_, opt_.graphs);
-            SW_CUDA(cudaEventRecord(events_[L.end_ev], s_decode_));
+            cudaStream_t ds = s_decode_[static_cast<std::size_t>(L.lane)];
+            SW_CUDA(cudaEventRecord(events_[L.start_ev], ds));
+            decode_forward(m_, kv_, b, ds, opt_.graphs, L.lane);
+            SW_CUDA(cudaEventRecord(events_[L.end_ev], ds));
             ++n_decode_;
         }
     }
@@ -346,7 +361,8 @@ private:
     sw_kv* kv_;
     GpuOptions opt_;
     ModelWork work_;
-    cudaStream_t s_prefill_ = nullptr, s_decode_ = nullptr;
+    cudaStream_t s_prefill_ = nullptr;
+    std::vector<cudaStream_t> s_decode_;
     std::vector<cudaEvent_t> events_;
     int t0_ = -1;
     std::vector<Launch> launches_;
@@ -369,6 +385,7 @@ extern "C" int sw_engine_run(sw_model* m, sw_kv* kv, const char* spec, char** ou
             if (k == "engine.split") opt.split = v == "1" || v == "true";
             else if (k == "engine.coalesce") opt.coalesce = v == "1" || v == "true";
             else if (k == "engine.graphs") opt.graphs = v == "1" || v == "true";
+            else if (k == "engine.decode_lanes") opt.decode_lanes = std::stoi(v);
             else if (k == "engine.peak_flops") opt.peak_flops = std::stod(v);
             else if (k == "engine.peak_bytes") opt.peak_bytes = std::stod(v);
             else throw ConfigError("spec: unknown key '" + k + "'");

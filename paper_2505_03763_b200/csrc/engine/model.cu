@@ -294,7 +294,7 @@ void prefill_forward(sw_model* m, sw_kv* kv, const sw_batch& b, cudaStream_t st)
 // ------------------------------------------------------------------ decode
 namespace {
 
-void decode_layers(sw_model* m, sw_kv* kv, int R, cudaStream_t st) {
+void decode_layers(sw_model* m, sw_kv* kv, int R, cudaStream_t st, int lane) {
     // One decode step, 5 kernels per layer, chained with programmatic dependent
     // launch (each kernel's weight stream starts while its predecessor drains):
     //   qkv  GEMM . RMSNorm scale . RoPE -> q, K/V straight into the paged cache
@@ -307,7 +307,7 @@ void decode_layers(sw_model* m, sw_kv* kv, int R, cudaStream_t st) {
     // folded into the weights).
     PdlScope pdl(true);
     const sw_model_desc& d = m->desc;
-    Workspace& w = m->dec;
+    Workspace& w = m->dec[lane];
     const int* live = &w.meta->n;
     const int qkv_w = (d.n_heads + 2 * d.n_kv_heads) * d.head_dim;
     const int hdH = d.n_heads * d.head_dim;
@@ -390,12 +390,16 @@ void decode_layers(sw_model* m, sw_kv* kv, int R, cudaStream_t st) {
 
 }  // namespace
 
-void decode_forward(sw_model* m, sw_kv* kv, const sw_batch& b, cudaStream_t st, bool use_graph) {
+void decode_forward(sw_model* m, sw_kv* kv, const sw_batch& b, cudaStream_t st, bool use_graph, int lane) {
     const sw_model_desc& d = m->desc;
+    if (lane < 0 || lane >= sw_model::kMaxDecodeLanes) throw ContractViolation("decode: lane out of range");
+    Workspace& w = m->dec[lane];
+    if (!w.x) ws_alloc(w, d, std::min(d.max_decode_batch, kMaxDecodeRows), true, 16);  // lanes > 0 on first use
+    if (m->dec_ring[lane].slots.empty()) ring_init(m->dec_ring[lane], 8, sizeof(StepMeta));
     if (b.n < 1 || b.n > kMaxDecodeRows) throw ContractViolation("decode: batch size out of range");
-    if (b.n > m->dec.rows) throw ConfigError("decode: batch exceeds model.max_decode_batch");
+    if (b.n > w.rows) throw ConfigError("decode: batch exceeds model.max_decode_batch");
     int idx;
-    StepMeta* h = static_cast<StepMeta*>(ring_claim(m->dec_ring, idx));
+    StepMeta* h = static_cast<StepMeta*>(ring_claim(m->dec_ring[lane], idx));
     h->n = b.n;
     for (int i = 0; i < b.n; ++i) {
         const int slot = b.slots[i], pos = b.positions[i];
@@ -409,16 +413,16 @@ void decode_forward(sw_model* m, sw_kv* kv, const sw_batch& b, cudaStream_t st, 
         h->out_index[i] = b.out_index ? b.out_index[i] : -1;
     }
     const size_t bytes = offsetof(StepMeta, slot) + sizeof(StepMeta::slot) * 5;
-    SW_CUDA(cudaMemcpyAsync(m->dec.meta, h, bytes, cudaMemcpyHostToDevice, st));
+    SW_CUDA(cudaMemcpyAsync(w.meta, h, bytes, cudaMemcpyHostToDevice, st));
     count_transfer(bytes, 0);
-    ring_release(m->dec_ring, idx, st);
-    const int R = std::min(decode_bucket(b.n), m->dec.rows);
-    DecodeGraph& g = m->graphs[{kv, R}];
+    ring_release(m->dec_ring[lane], idx, st);
+    const int R = std::min(decode_bucket(b.n), w.rows);
+    DecodeGraph& g = m->graphs[{kv, R, lane}];
     if (use_graph && g.exec) {
         SW_CUDA(cudaGraphLaunch(g.exec, st));
         count_launches(g.kernels);
     } else {
-        decode_layers(m, kv, R, st);
+        decode_layers(m, kv, R, st, lane);
         if (use_graph && ++g.eager_runs >= 1) {
             // capture once the kernels' attributes are configured (first eager run)
             cudaStream_t cs;
@@ -426,7 +430,7 @@ void decode_forward(sw_model* m, sw_kv* kv, const sw_batch& b, cudaStream_t st, 
             cudaGraph_t graph;
             SW_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
             const unsigned long long before = g_launches.load();
-            decode_layers(m, kv, R, cs);
+            decode_layers(m, kv, R, cs, lane);
             g.kernels = g_launches.load() - before;
             g_launches.fetch_sub(g.kernels);  // captured, not launched
             SW_CUDA(cudaStreamEndCapture(cs, &graph));
@@ -436,9 +440,9 @@ void decode_forward(sw_model* m, sw_kv* kv, const sw_batch& b, cudaStream_t st, 
         }
     }
     if (b.logits_out) {  // parity checks: fp32 logits from the same folded-norm input
-        GemmProblem q = gp(m->dec.xn, m->dec.rows, m->lm, d.vocab, b.n, d.vocab, d.d_model, EPI_STORE_F32, true,
+        GemmProblem q = gp(w.xn, w.rows, m->lm, d.vocab, b.n, d.vocab, d.d_model, EPI_STORE_F32, true,
                            b.logits_out, d.vocab);
-        q.fx.ss_parts = m->dec.ss;
+        q.fx.ss_parts = w.ss;
         q.fx.ss_nparts = d.d_model / 128;
         q.fx.norm_dim = d.d_model;
         q.fx.norm_eps = d.norm_eps;
@@ -532,9 +536,9 @@ extern "C" int sw_model_create(const sw_model_desc* desc, int device, sw_model**
         m->rope_cs = dalloc<float2>(static_cast<size_t>(kMaxPositions) * (hd / 2));
         rope_table(m->inv_freq, m->rope_cs, kMaxPositions, static_cast<int>(hd / 2), st);
         ws_alloc(m->pre, d, d.max_prefill_tokens, false, 1);
-        ws_alloc(m->dec, d, std::min(d.max_decode_batch, kMaxDecodeRows), true, 16);
+        ws_alloc(m->dec[0], d, std::min(d.max_decode_batch, kMaxDecodeRows), true, 16);
         ring_init(m->pre_ring, 4, m->pre.pmeta_bytes);
-        ring_init(m->dec_ring, 8, sizeof(StepMeta));
+        ring_init(m->dec_ring[0], 8, sizeof(StepMeta));
         m->scratch_u64 = dalloc<unsigned long long>(1);
         SW_CUDA(cudaDeviceSynchronize());
         *out = m.release();
@@ -547,14 +551,18 @@ extern "C" int sw_model_destroy(sw_model* m) {
         cudaDeviceSynchronize();
         for (auto& [k, g] : m->graphs)
             if (g.exec) cudaGraphExecDestroy(g.exec);
-        for (Workspace* w : {&m->pre, &m->dec}) {
+        std::vector<Workspace*> all{&m->pre};
+        for (auto& w : m->dec) all.push_back(&w);
+        for (Workspace* w : all) {
             for (void* p : {(void*)w->x, (void*)w->xn, (void*)w->qkv, (void*)w->q, (void*)w->attn, (void*)w->act,
                             (void*)w->xlast, (void*)w->keys, (void*)w->meta, (void*)w->part_o, (void*)w->part_ml,
                             (void*)w->pmeta, (void*)w->splitk_ws, (void*)w->splitk_cnt, (void*)w->attn_cnt,
                             (void*)w->ss})
                 if (p) cudaFree(p);
         }
-        for (PinnedRing* r : {&m->pre_ring, &m->dec_ring}) {
+        std::vector<PinnedRing*> rings{&m->pre_ring};
+        for (auto& r : m->dec_ring) rings.push_back(&r);
+        for (PinnedRing* r : rings) {
             for (void* p : r->slots) cudaFreeHost(p);
             for (cudaEvent_t e : r->done) cudaEventDestroy(e);
         }
@@ -622,7 +630,7 @@ extern "C" int sw_kv_arena_destroy(sw_kv* kv) {
         if (!kv) return;
         cudaDeviceSynchronize();
         for (auto it = kv->model->graphs.begin(); it != kv->model->graphs.end();) {
-            if (it->first.first == kv) {
+            if (std::get<0>(it->first) == kv) {
                 if (it->second.exec) cudaGraphExecDestroy(it->second.exec);
                 it = kv->model->graphs.erase(it);
             } else {

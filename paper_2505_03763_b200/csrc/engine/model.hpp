@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <map>
+#include <tuple>
 #include <memory>
 #include <string>
 #include <vector>
@@ -77,9 +78,13 @@ struct sw_model {
     std::map<std::string, std::pair<void*, int64_t>> tensors;
     float* inv_freq = nullptr;
     float2* rope_cs = nullptr;  // [kMaxPositions][hd/2] (cos, sin)
-    sw::Workspace pre, dec;
-    sw::PinnedRing pre_ring, dec_ring;
-    std::map<std::pair<const sw_kv*, int>, sw::DecodeGraph> graphs;  // (arena, row bucket)
+    sw::Workspace pre;
+    // decode lanes: one workspace + staging ring + graph set per concurrent
+    // decode stream (lanes of different instances may step at the same time)
+    static constexpr int kMaxDecodeLanes = 4;
+    sw::Workspace dec[kMaxDecodeLanes];
+    sw::PinnedRing pre_ring, dec_ring[kMaxDecodeLanes];
+    std::map<std::tuple<const sw_kv*, int, int>, sw::DecodeGraph> graphs;  // (arena, row bucket, lane)
     unsigned long long* scratch_u64 = nullptr;
 };
 
@@ -102,6 +107,6 @@ namespace sw {
 constexpr int kMaxPositions = 32768;  // RoPE table extent (max context)
 // Forward passes (stream-ordered; host arrays staged internally).
 void prefill_forward(sw_model* m, sw_kv* kv, const sw_batch& b, cudaStream_t st);
-void decode_forward(sw_model* m, sw_kv* kv, const sw_batch& b, cudaStream_t st, bool use_graph);
+void decode_forward(sw_model* m, sw_kv* kv, const sw_batch& b, cudaStream_t st, bool use_graph, int lane = 0);
 int decode_bucket(int n);
 }  // namespace sw
