@@ -33,16 +33,16 @@ PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustain
 WORKLOADS = {
     # configs[1] of BASELINE.json -- the bench line
     "1b": dict(model="LLAMA_1B", n=64, input=512, output=128, arrival="zero", max_prefill=32768, max_decode=64,
-               split="policy=pipelined_splitwiser;P=4;max_batch=16;engine.split=1",
+               split="policy=pipelined_splitwiser;P=2;max_batch=32;engine.split=1;engine.decode_lanes=2",
                serial="policy=sequential;max_batch=64;engine.split=0"),
     # configs[2]: 8B shape, Poisson arrivals of mixed prompts, mixed batching vs continuous batching
     "8b-poisson": dict(model="LLAMA_8B", n=128, input="128..2048", output=256, arrival="poisson:32",
                        max_prefill=32768, max_decode=128,
-                       split="policy=mixed_batching;max_batch=128;engine.split=1",
+                       split="policy=mixed_batching;max_batch=128;engine.split=1",  # prefill || decode, one instance
                        serial="policy=continuous_batching;max_batch=128;engine.split=0"),
     # configs[0] shape on the GPU (fast sanity run)
     "tiny": dict(model="TINY", n=8, input=64, output=32, arrival="zero", max_prefill=1024, max_decode=16,
-                 split="policy=pipelined_splitwiser;P=2;max_batch=4;engine.split=1",
+                 split="policy=pipelined_splitwiser;P=2;max_batch=4;engine.split=1;engine.decode_lanes=2",
                  serial="policy=sequential;max_batch=8;engine.split=0"),
 }
 
