@@ -132,10 +132,32 @@ def cpu_sample(desc_name: str, n_req: int = 4, prompt: int = 512, gen: int = 8):
 
 
 # ----------------------------------------------------------------- roofline
+def graph_time(launch, reps: int) -> float:
+    """Average device time of one launch: `reps` launches captured in one CUDA
+    graph (no host launch gaps between them), replayed once to warm, then timed
+    with CUDA events on the replay stream."""
+    import torch
+
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for i in range(reps):
+            launch(i)
+    g.replay()
+    torch.cuda.synchronize()
+    st = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    g.replay()
+    e1.record(st)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / 1e3 / reps
+
+
 def roofline_decode_gemm(eng, desc, rows: int, peaks, reps: int = 20):
     """The dominant kernel: the decode step's gate/up projection (swap-AB
     tcgen05 GEMM with fused SwiGLU), HBM-bound.  Timed with CUDA events on the
-    stream it is launched on, rotating over all layers' weights (> L2) so every
+    stream it is launched on (captured in a CUDA graph), rotating over all layers' weights (> L2) so every
     launch streams from HBM.  Algorithmic bytes per launch = weights 2*ffn*d*2 +
     activations rows*d*2 in + rows*ffn*2 out."""
     import ctypes
@@ -146,23 +168,14 @@ def roofline_decode_gemm(eng, desc, rows: int, peaks, reps: int = 20):
     x = torch.randn(rows, d, device="cuda").bfloat16()
     y = torch.empty(rows, F, device="cuda", dtype=torch.bfloat16)
     ws = [eng.tensor(f"layer{l}.wgu")[0] for l in range(L)]
-    st = torch.cuda.current_stream()
-    sp = ctypes.c_void_p(st.cuda_stream)
-
     def launch(i):
         sw.check(sw.lib().sw_op_gemm(ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(ws[i % L]),
-                                     ctypes.c_void_p(y.data_ptr()), rows, 2 * F, d, 2, sp))
+                                     ctypes.c_void_p(y.data_ptr()), rows, 2 * F, d, 2,
+                                     ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)))
 
     for i in range(L):
         launch(i)
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(st)
-    for i in range(reps):
-        launch(i)
-    e1.record(st)
-    torch.cuda.synchronize()
-    t = e0.elapsed_time(e1) / 1e3 / reps
+    t = graph_time(launch, reps)
     nbytes = 2 * F * d * 2 + rows * d * 2 + rows * F * 2
     achieved = nbytes / t / 1e9
     peak = float(peaks["hbm_gbs"])
@@ -181,22 +194,13 @@ def roofline_prefill_gemm(eng, desc, tokens: int, peaks, reps: int = 10):
     x = torch.randn(tokens, d, device="cuda").bfloat16()
     y = torch.empty(tokens, F, device="cuda", dtype=torch.bfloat16)
     ws = [eng.tensor(f"layer{l}.wgu")[0] for l in range(L)]
-    st = torch.cuda.current_stream()
-    sp = ctypes.c_void_p(st.cuda_stream)
-
     def launch(i):
         sw.check(sw.lib().sw_op_gemm(ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(ws[i % L]),
-                                     ctypes.c_void_p(y.data_ptr()), tokens, 2 * F, d, 2, sp))
+                                     ctypes.c_void_p(y.data_ptr()), tokens, 2 * F, d, 2,
+                                     ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)))
 
     launch(0)
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(st)
-    for i in range(reps):
-        launch(i)
-    e1.record(st)
-    torch.cuda.synchronize()
-    t = e0.elapsed_time(e1) / 1e3 / reps
+    t = graph_time(launch, reps)
     flops = 2.0 * tokens * 2 * F * d
     achieved = flops / t / 1e12
     peak = float(peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"]))

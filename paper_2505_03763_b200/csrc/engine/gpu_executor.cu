@@ -351,7 +351,7 @@ private:
             b.out_index = oidx.data();
             cudaStream_t ds = s_decode_[static_cast<std::size_t>(L.lane)];
             SW_CUDA(cudaEventRecord(events_[L.start_ev], ds));
-            decode_forward(m_, kv_, b, ds, opt_.graphs, L.lane);
+            decode_forward(m_, kv_, b, ds, opt_.graphs, L.lane, static_cast<int>(s_decode_.size()));
             SW_CUDA(cudaEventRecord(events_[L.end_ev], ds));
             ++n_decode_;
         }

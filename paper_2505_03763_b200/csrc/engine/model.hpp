@@ -12,6 +12,7 @@
 
 #include "../../../include/splitwise.h"
 #include "../kernels/attention.cuh"
+#include "../kernels/decode_step.cuh"
 #include "../kernels/elementwise.cuh"
 
 namespace sw {
@@ -58,6 +59,21 @@ struct PinnedRing {
     int next = 0;
 };
 
+// Device-resident phase list of the persistent decode-step kernel for one
+// (arena, row bucket, lane): tensor maps of every weight matrix and of the
+// lane's activation buffers, the per-phase epilogue arguments, and the grid
+// barrier counters.
+struct StepPlan {
+    StepPhase* d_phases = nullptr;
+    CUtensorMap* d_maps = nullptr;
+    unsigned* d_bar = nullptr;  // [n_phases] barrier arrivals + [n_counters] split-K tile counters
+    int n_phases = 0;
+    int n_counters = 0;
+    int bn = 0;
+    int ctas = 0;
+    StepArgs args{};
+};
+
 struct DecodeGraph {
     cudaGraphExec_t exec = nullptr;
     int eager_runs = 0;
@@ -84,7 +100,8 @@ struct sw_model {
     static constexpr int kMaxDecodeLanes = 4;
     sw::Workspace dec[kMaxDecodeLanes];
     sw::PinnedRing pre_ring, dec_ring[kMaxDecodeLanes];
-    std::map<std::tuple<const sw_kv*, int, int>, sw::DecodeGraph> graphs;  // (arena, row bucket, lane)
+    std::map<std::tuple<const sw_kv*, int, int>, sw::DecodeGraph> graphs;  // (arena, row bucket, lane | mode)
+    std::map<std::tuple<const sw_kv*, int, int>, sw::StepPlan> step_plans;  // (arena, row bucket, lane)
     unsigned long long* scratch_u64 = nullptr;
 };
 
@@ -107,6 +124,7 @@ namespace sw {
 constexpr int kMaxPositions = 32768;  // RoPE table extent (max context)
 // Forward passes (stream-ordered; host arrays staged internally).
 void prefill_forward(sw_model* m, sw_kv* kv, const sw_batch& b, cudaStream_t st);
-void decode_forward(sw_model* m, sw_kv* kv, const sw_batch& b, cudaStream_t st, bool use_graph, int lane = 0);
+void decode_forward(sw_model* m, sw_kv* kv, const sw_batch& b, cudaStream_t st, bool use_graph, int lane = 0,
+                    int lanes = 1);
 int decode_bucket(int n);
 }  // namespace sw

@@ -12,52 +12,17 @@
 #include <algorithm>
 
 #include "attention.cuh"
+#include "attn_decode_unit.cuh"
 #include "common.cuh"
 
 namespace sw {
 
 namespace {
 
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
-    const int sz = valid ? 16 : 0;  // zero-fill when invalid
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_addr(smem)), "l"(gmem), "r"(sz)
-                 : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-
-__device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], const void* p) {
-    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
-                 : "r"(smem_addr(p)));
-}
-__device__ __forceinline__ void ldsm_x4_t(uint32_t (&r)[4], const void* p) {
-    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
-                 : "r"(smem_addr(p)));
-}
-__device__ __forceinline__ void mma_bf16(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
-    asm volatile(
-        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
-        "{%0,%1,%2,%3};"
-        : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
-        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
-}
-
-// [rows][HD] bf16 tile, 16 B chunks XOR-swizzled by row.
-template <int HD>
-__device__ __forceinline__ int swz(int row, int chunk) {
-    return row * HD + ((chunk ^ (row & 7)) << 3);
-}
+using namespace attn;
 
 constexpr int kQRows = 64;
 constexpr int kKeys = 64;
-constexpr int kPage = 16;        // tokens per KV page (fixed: shifts, not divisions, in the address math)
-constexpr int kPartSplits = 16;  // stride of the split-partial buffers (>= any grid x)
-constexpr int kMaxChunkPages = 512;  // page ids of one decode split staged in smem (8192 keys)
 
 template <int HD>
 __global__ void __launch_bounds__(128) attn_prefill_kernel(const __nv_bfloat16* __restrict__ q,
@@ -234,29 +199,13 @@ __global__ void __launch_bounds__(128) attn_prefill_kernel(const __nv_bfloat16* 
 }
 
 // ------------------------------------------------------------------ decode
-// One CTA = (row, kv head, split of the context).  Its 4 warps stream
-// disjoint KB-key blocks of the split (warp w takes blocks w, w+4, ...)
-// through private double-buffered smem, each with its own online softmax;
-// the G query heads of the kv head are the rows of a 16-row mma tile
-// (rows >= G are zero), so Q.K^T and P.V run on the tensor cores and the
-// kernel is a pure HBM stream of K/V pages.  Warps merge in smem; splits
-// merge in the last-arriving CTA of the (row, kv head) (ordered, so results
-// do not depend on timing).
+// One CTA = one unit (row, kv head, split of the context); see attn_decode_unit.cuh.
 template <int HD, int G, int KB>
 __global__ void __launch_bounds__(128) attn_decode_kernel(const __nv_bfloat16* __restrict__ q,
                                                           const __nv_bfloat16* __restrict__ kv_layer,
                                                           __nv_bfloat16* __restrict__ out, DecodeAttnArgs a) {
-    static_assert(G <= 8, "query rows live in the first 8 mma rows");
-    constexpr int CH = HD / 8;
     extern __shared__ __align__(128) uint8_t dsm[];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    __nv_bfloat16* wK = reinterpret_cast<__nv_bfloat16*>(dsm) + warp * (4 * KB * HD);  // [2][KB][HD]
-    __nv_bfloat16* wV = wK + 2 * KB * HD;                                               // [2][KB][HD]
-    float* cm = reinterpret_cast<float*>(dsm + 4 * (4 * KB * HD) * 2);  // [4][G]
-    float* cl = cm + 4 * G;                                             // [4][G]
-    float* co = cl + 4 * G;                                             // [4][G][HD]
     __shared__ uint32_t s_last;
-
     __shared__ int32_t s_pages[kMaxChunkPages];
     griddep_launch_dependents();
     griddep_wait();
@@ -266,211 +215,18 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(const __nv_bfloat16* _
     const int ctx = a.meta->pos[row] + 1;
     // splits chosen at run time: only as many as it takes to reach
     // a.target_ctas CTAs, each warp keeping >= 1 key block
-    const int want = cdiv(a.target_ctas, n_rows * a.Hkv);
-    const int splits0 = max(cdiv(ctx, kMaxChunkPages * kPage),
-                            max(1, min(min(want, static_cast<int>(gridDim.x)), cdiv(ctx, 4 * KB))));
-    const int chunk = cdiv(cdiv(ctx, splits0), KB) * KB;
-    const int splits = cdiv(ctx, chunk);  // every split non-empty
+    const SplitPlan plan = decode_split_plan<KB>(ctx, cdiv(a.target_ctas, n_rows * a.Hkv), static_cast<int>(gridDim.x));
     const int split = blockIdx.x;
-    if (split >= splits) return;
-    const int k_begin = split * chunk;
-    const int k_end = min(ctx, k_begin + chunk);
-    if (k_begin >= k_end) return;
-    const int hk = blockIdx.y;
-    {  // this split's page ids -> smem (one read per page, not per 16 B chunk)
-        const int32_t* ptab = a.page_table + static_cast<int64_t>(a.meta->slot[row]) * a.max_pages;
-        const int p0 = k_begin / kPage, p1 = (k_end - 1) / kPage;
-        for (int i = threadIdx.x; i <= p1 - p0; i += 128) s_pages[i] = ptab[p0 + i];
-    }
-    const int page_base = k_begin / kPage;
-    const int n_blocks = cdiv(k_end - k_begin, KB);
-
-    // Q fragment (A operand, rows = query heads of this kv head)
-    const int r = lane >> 2;
-    uint32_t qf[HD / 16][4];
-    const __nv_bfloat16* qrow = q + static_cast<int64_t>(row) * a.H * HD + static_cast<int64_t>(hk * G + r) * HD;
-#pragma unroll
-    for (int ks = 0; ks < HD / 16; ++ks) {
-        const int c = ks * 16 + (lane & 3) * 2;
-        qf[ks][0] = r < G ? *reinterpret_cast<const uint32_t*>(qrow + c) : 0u;
-        qf[ks][1] = 0u;
-        qf[ks][2] = r < G ? *reinterpret_cast<const uint32_t*>(qrow + c + 8) : 0u;
-        qf[ks][3] = 0u;
-    }
-
-    auto load = [&](int blk, int buf) {
-        const int k0 = k_begin + blk * KB;
-        for (int i = lane; i < KB * CH; i += 32) {
-            const int kr = i / CH, c = i % CH;
-            const int key = k0 + kr;
-            const bool ok = key < k_end;
-            const int page = ok ? s_pages[key / kPage - page_base] : 0;
-            const __nv_bfloat16* src = kv_layer + static_cast<int64_t>(page) * a.page_stride +
-                                       static_cast<int64_t>(hk) * kPage * HD +
-                                       static_cast<int64_t>(key % kPage) * HD + c * 8;
-            cp_async16(wK + buf * KB * HD + swz<HD>(kr, c), src, ok);
-            cp_async16(wV + buf * KB * HD + swz<HD>(kr, c), src + a.kv_stride, ok);
-        }
-    };
-
-    float o[HD / 8][4];
-#pragma unroll
-    for (int i = 0; i < HD / 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
-    float m_run = -INFINITY, l_run = 0.f;  // row r (c0/c1); rows r+8 are padding
-
-    __syncthreads();  // s_pages
-    int it = 0;
-    if (warp < n_blocks) {
-        load(warp, 0);
-        cp_async_commit();
-    }
-    for (int blk = warp; blk < n_blocks; blk += 4, ++it) {
-        const int buf = it & 1;
-        if (blk + 4 < n_blocks) {
-            load(blk + 4, buf ^ 1);
-            cp_async_commit();
-            cp_async_wait<1>();
-        } else {
-            cp_async_wait<0>();
-        }
-        __syncwarp();
-        const __nv_bfloat16* K = wK + buf * KB * HD;
-        const __nv_bfloat16* V = wV + buf * KB * HD;
-        float sc[KB / 8][4];
-#pragma unroll
-        for (int nb = 0; nb < KB / 8; ++nb) sc[nb][0] = sc[nb][1] = sc[nb][2] = sc[nb][3] = 0.f;
-#pragma unroll
-        for (int ks = 0; ks < HD / 16; ++ks) {
-#pragma unroll
-            for (int np = 0; np < KB / 16; ++np) {
-                uint32_t b[4];
-                const int key = np * 16 + (lane & 7) + ((lane >> 4) << 3);
-                const int c = ks * 2 + ((lane >> 3) & 1);
-                ldsm_x4(b, K + swz<HD>(key, c));
-                mma_bf16(sc[2 * np], qf[ks], b[0], b[1]);
-                mma_bf16(sc[2 * np + 1], qf[ks], b[2], b[3]);
-            }
-        }
-        const int kbase = k_begin + blk * KB;
-        float mx = -INFINITY;
-#pragma unroll
-        for (int nb = 0; nb < KB / 8; ++nb)
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-                const int key = kbase + nb * 8 + (lane & 3) * 2 + e;
-                const float v = key < k_end ? sc[nb][e] * a.scale_log2 : -INFINITY;
-                sc[nb][e] = v;
-                mx = fmaxf(mx, v);
-            }
-        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
-        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
-        const float m_new = fmaxf(m_run, mx);  // finite: the block's first key is valid
-        const float alpha = exp2f(m_run - m_new);
-        m_run = m_new;
-        float rs = 0.f;
-#pragma unroll
-        for (int nb = 0; nb < KB / 8; ++nb) {
-            sc[nb][0] = exp2f(sc[nb][0] - m_new);
-            sc[nb][1] = exp2f(sc[nb][1] - m_new);
-            sc[nb][2] = sc[nb][3] = 0.f;  // padding rows
-            rs += sc[nb][0] + sc[nb][1];
-        }
-        l_run = l_run * alpha + rs;
-#pragma unroll
-        for (int i = 0; i < HD / 8; ++i) {
-            o[i][0] *= alpha;
-            o[i][1] *= alpha;
-        }
-#pragma unroll
-        for (int kk = 0; kk < KB / 16; ++kk) {
-            uint32_t pa[4];
-            pa[0] = pack_bf2(sc[2 * kk][0], sc[2 * kk][1]);
-            pa[1] = 0u;
-            pa[2] = pack_bf2(sc[2 * kk + 1][0], sc[2 * kk + 1][1]);
-            pa[3] = 0u;
-#pragma unroll
-            for (int dp = 0; dp < HD / 16; ++dp) {
-                uint32_t b[4];
-                const int key = kk * 16 + (lane & 7) + (((lane >> 3) & 1) << 3);
-                const int c = dp * 2 + (lane >> 4);
-                ldsm_x4_t(b, V + swz<HD>(key, c));
-                mma_bf16(o[2 * dp], pa, b[0], b[1]);
-                mma_bf16(o[2 * dp + 1], pa, b[2], b[3]);
-            }
-        }
-        __syncwarp();
-    }
-    l_run += __shfl_xor_sync(0xffffffffu, l_run, 1);
-    l_run += __shfl_xor_sync(0xffffffffu, l_run, 2);
-    // ---- merge the 4 warps
-    if (r < G) {
-        if ((lane & 3) == 0) {
-            cm[warp * G + r] = m_run;
-            cl[warp * G + r] = l_run;
-        }
-#pragma unroll
-        for (int i = 0; i < HD / 8; ++i) {
-            float* dst = co + (warp * G + r) * HD + i * 8 + (lane & 3) * 2;
-            dst[0] = o[i][0];
-            dst[1] = o[i][1];
-        }
-    }
-    __syncthreads();
-    const int64_t pidx = (static_cast<int64_t>(row) * a.Hkv + hk) * kPartSplits + split;
-    for (int idx = threadIdx.x; idx < G * HD; idx += 128) {
-        const int g = idx / HD, d = idx % HD;
-        float M = -INFINITY;
-#pragma unroll
-        for (int w = 0; w < 4; ++w) M = fmaxf(M, cm[w * G + g]);
-        float L = 0.f, O = 0.f;
-#pragma unroll
-        for (int w = 0; w < 4; ++w) {
-            const float sc_w = cm[w * G + g] == -INFINITY ? 0.f : exp2f(cm[w * G + g] - M);
-            L += cl[w * G + g] * sc_w;
-            O += co[(w * G + g) * HD + d] * sc_w;
-        }
-        if (splits == 1) {
-            out[static_cast<int64_t>(row) * a.H * HD + (hk * G + g) * HD + d] = __float2bfloat16_rn(O / L);
-        } else {
-            __stcg(a.part_o + pidx * G * HD + idx, O);
-            if (d == 0) {
-                __stcg(a.part_ml + (pidx * G + g) * 2, M);
-                __stcg(a.part_ml + (pidx * G + g) * 2 + 1, L);
-            }
-        }
-    }
-    if (splits == 1) return;
-    // ---- last split to arrive merges all splits in order
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        unsigned* cnt = a.counters + static_cast<int64_t>(row) * a.Hkv + hk;
-        s_last = atomicAdd(cnt, 1u) == static_cast<unsigned>(splits - 1);
-        if (s_last) *cnt = 0u;
-    }
-    __syncthreads();
-    if (!s_last) return;
-    __threadfence();
-    const int64_t base = (static_cast<int64_t>(row) * a.Hkv + hk) * kPartSplits;
-    for (int idx = threadIdx.x; idx < G * HD; idx += 128) {
-        const int g = idx / HD;
-        float M = -INFINITY;
-        for (int sp = 0; sp < splits; ++sp) M = fmaxf(M, __ldcg(a.part_ml + ((base + sp) * G + g) * 2));
-        float L = 0.f, O = 0.f;
-        for (int sp = 0; sp < splits; ++sp) {
-            const float w = exp2f(__ldcg(a.part_ml + ((base + sp) * G + g) * 2) - M);
-            L += __ldcg(a.part_ml + ((base + sp) * G + g) * 2 + 1) * w;
-            O += __ldcg(a.part_o + (base + sp) * G * HD + idx) * w;
-        }
-        out[static_cast<int64_t>(row) * a.H * HD + (hk * G) * HD + idx] = __float2bfloat16_rn(O / L);
-    }
+    if (split >= plan.splits) return;
+    decode_unit<HD, G, KB>(a, q, kv_layer, out, row, blockIdx.y, split, plan, ctx, dsm, s_pages, &s_last, threadIdx.x,
+                           [] { __syncthreads(); });
 }
 
 template <int HD, int G>
 void decode_launch(const __nv_bfloat16* q, const __nv_bfloat16* kv_layer, __nv_bfloat16* out, const DecodeAttnArgs& a,
                    int max_rows, cudaStream_t st) {
-    constexpr int KB = HD <= 64 ? 32 : 16;
-    constexpr int smem = 4 * (4 * KB * HD) * 2 + (8 * G + 4 * G * HD) * 4;
+    constexpr int KB = decode_kb<HD>();
+    constexpr int smem = decode_unit_smem<HD, G>();
     static bool cfg = false;
     if (!cfg) {
         SW_CUDA(cudaFuncSetAttribute(attn_decode_kernel<HD, G, KB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));

@@ -34,10 +34,11 @@ __device__ __forceinline__ void transpose_sum(float (&v)[32], int lane) {
     }
 }
 
-// Apply the fused epilogue MODE to 32 token columns [c, c + 32) of feature
-// tile m0.  Uses named barrier 1 over the 128 epilogue threads.
+// Apply the fused epilogue MODE to token columns [c, c + min(32, width)) of
+// feature tile m0 (vin[j] = column c + j).  Uses named barrier 1 over the 128
+// epilogue threads.
 template <int MODE>
-__device__ __forceinline__ void emit_swap(const SwapEpi& E, int m0, int c, const float (&vin)[32]) {
+__device__ __forceinline__ void emit_swap(const SwapEpi& E, int m0, int c, const float (&vin)[32], int width = 32) {
     const GemmArgs& args = *E.args;
     const DecodeFusion& fx = args.fx;
     float* xchg = E.xchg;
@@ -47,7 +48,7 @@ __device__ __forceinline__ void emit_swap(const SwapEpi& E, int m0, int c, const
     const long long* tok_kv = E.tok_kv;
 
         const int f = m0 + row;
-        const int tcount = min(32, n_live - c);
+        const int tcount = min(min(32, width), n_live - c);
         float v[32];
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = vin[j];
