@@ -9,7 +9,8 @@
 
 namespace sw {
 
-__device__ __forceinline__ float silu_mul(float g, float u) { return g / (1.0f + __expf(-g)) * u; }
+// silu(g) * u; the fast reciprocal maps 1 + e^-g = inf to 0 (no IEEE slow path)
+__device__ __forceinline__ float silu_mul(float g, float u) { return __fdividef(g, 1.0f + __expf(-g)) * u; }
 
 struct SwapEpi {
     const GemmArgs* args;

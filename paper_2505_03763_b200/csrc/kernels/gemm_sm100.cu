@@ -581,6 +581,18 @@ void gemm_run(const GemmProblem& p, cudaStream_t st) {
         a.M = p.features;
         a.N = bn;
         const int tiles = p.features / BM;
+        static const int dec_env = env_flag("SW_GEMM_DEC", 1);
+        if (dec_env && p.mode != EPI_ARGMAX && p.ws) {
+            // decode projections: cluster split-K, column-distributed reduction
+            static const int dec_ctas = env_flag("SW_DEC_CTAS", 0);
+            const int S = gemm_decode_splits(tiles, p.K / BK, dec_ctas > 0 ? dec_ctas : sms);
+            if (S == 1 || gemm_decode_ws_floats(tiles, S, bn) <= p.ws_floats) {
+                a.stream_k = 0;
+                gemm_decode_run(tmap_cached(p.W, p.w_rows, p.K, BM), tmap_cached(p.X, p.x_rows, p.K, bn), a, bn, S,
+                                tiles, st);
+                return;
+            }
+        }
         static const int cl_env = env_flag("SW_GEMM_CLUSTER", 0);  // measured slower at b=64 (profiles/r01)
         if (cl_env && bn <= 64 && p.mode != EPI_ARGMAX && tiles < 2 * sms) {
             // decode projections: a tile per cluster of k CTAs, reduced through DSMEM

@@ -14,7 +14,7 @@ SHAPES = [("1b.qkv", 3072, 2048, 4), ("1b.wo", 2048, 2048, 1), ("1b.gu", 16384, 
           ("8b.wd", 4096, 14336, 1)]
 
 
-def t(feat, K, epi, rows, reps=20, copies=4):
+def t(feat, K, epi, rows, reps=int(os.environ.get("REPS", "20")), copies=int(os.environ.get("COPIES", "4"))):
     Ws = [torch.randn(feat, K, device="cuda").bfloat16() for _ in range(copies)]
     X = torch.randn(rows, K, device="cuda").bfloat16()
     out = torch.zeros(rows, feat, device="cuda")
@@ -46,6 +46,9 @@ def t(feat, K, epi, rows, reps=20, copies=4):
 
 if __name__ == "__main__":
     rows = int(os.environ.get("ROWS", "64"))
+    only = os.environ.get("ONLY")
     for name, feat, K, epi in SHAPES:
+        if only and name not in only.split(","):
+            continue
         us, gbs = t(feat, K, epi, rows)
         print(f"{name:8s} b={rows}: {us:8.2f} us {gbs:8.1f} GB/s", flush=True)
