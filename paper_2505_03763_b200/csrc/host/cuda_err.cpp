@@ -16,10 +16,10 @@ bool& pdl_mode() {
     thread_local bool on = false;
     return on;
 }
-bool pdl_allowed() {  // SW_PDL=1 enables programmatic dependent launch (measured slower: off)
+bool pdl_allowed() {  // programmatic dependent launch in the decode step; SW_PDL=0 disables (A/B)
     static const bool ok = [] {
         const char* v = std::getenv("SW_PDL");
-        return v && v[0] == '1';
+        return !(v && v[0] == '0');
     }();
     return ok;
 }

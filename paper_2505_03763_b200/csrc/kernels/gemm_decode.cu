@@ -389,14 +389,16 @@ void dispatch_mode(int mode, const CUtensorMap& a, const CUtensorMap& b, const G
     }
 }
 
-// Clusters of S CTAs that can be co-resident at one CTA per SM (the BN = 256
-// configuration, the largest): GPC sizes strand SMs for S > 2.
+// Clusters of S CTAs that can be co-resident (the BN <= 128 configurations,
+// two CTAs per SM; GPC sizes strand SMs for S > 2).  Only a performance
+// bound: clusters are independent, so a second wave is still correct.
 int max_active_clusters(int S) {
     static int cache[kMaxSplit + 1] = {};
     if (cache[S]) return cache[S];
-    using C = DecCfg<256>;
-    auto kern = gemm_decode_kernel<256, EPI_STORE>;
+    using C = DecCfg<128>;
+    auto kern = gemm_decode_kernel<128, EPI_STORE>;
     SW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
+    SW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared));
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(S, 1);
     cfg.blockDim = dim3(kThreads);

@@ -1,5 +1,5 @@
-// Swap-AB (decode) GEMM epilogue shared by the persistent kernel
-// (gemm_sm100.cu) and the cluster split-K kernel (gemm_cluster.cu).
+// Swap-AB (decode) GEMM epilogue of the persistent kernel (gemm_sm100.cu: the
+// LM head with greedy argmax) and the persistent decode-step kernel.
 // Thread = output feature row of a 128-row weight tile (TMEM lane order:
 // row = 32 * (warp % 4) + lane over the 4 epilogue warps); columns = tokens.
 #pragma once
@@ -19,6 +19,7 @@ struct SwapEpi {
     const int* tok_pos;     // [256] smem position per token (QKV_ROPE)
     const long long* tok_kv;  // [256] smem KV page offset per token (QKV_ROPE)
     int row, lane, quarter, n_live;
+    unsigned long long* best = nullptr;  // ARGMAX: smem running max per token (flushed once per CTA)
 };
 
 // 32 fp32 values per lane -> lane j holds the warp sum of value j (31 shuffles)
@@ -31,6 +32,21 @@ __device__ __forceinline__ void transpose_sum(float (&v)[32], int lane) {
             const float send = upper ? v[i] : v[i + off];
             const float keep = upper ? v[i + off] : v[i];
             v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+        }
+    }
+}
+
+// 32 packed keys per lane -> lane j holds the warp max of key j (31 shuffles)
+__device__ __forceinline__ void transpose_max(unsigned long long (&v)[32], int lane) {
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) {
+        const bool upper = (lane & off) != 0;
+#pragma unroll
+        for (int i = 0; i < off; ++i) {
+            const unsigned long long send = upper ? v[i] : v[i + off];
+            const unsigned long long keep = upper ? v[i + off] : v[i];
+            const unsigned long long other = __shfl_xor_sync(0xffffffffu, send, off);
+            v[i] = other > keep ? other : keep;
         }
     }
 }
@@ -102,6 +118,15 @@ __device__ __forceinline__ void emit_swap(const SwapEpi& E, int m0, int c, const
             }
             asm volatile("bar.sync 1, 128;" ::: "memory");
         } else if constexpr (MODE == EPI_ARGMAX) {
+            if (E.best) {  // per-CTA running max in smem: one global atomic per token per CTA
+                unsigned long long k[32];
+#pragma unroll
+                for (int j = 0; j < 32; ++j)
+                    k[j] = j < tcount ? argmax_key(v[j], static_cast<uint32_t>(args.feature_offset + f)) : 0ull;
+                transpose_max(k, lane);
+                if (lane < tcount) atomicMax(E.best + c + lane, k[0]);
+                return;
+            }
             _Pragma("unroll") for (int j = 0; j < 32; ++j) if (j < tcount) {
                 unsigned long long key = argmax_key(v[j], static_cast<uint32_t>(args.feature_offset + f));
 #pragma unroll

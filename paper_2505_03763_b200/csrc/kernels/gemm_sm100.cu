@@ -63,7 +63,7 @@ struct GemmCfg {
     static_assert(kStages >= 4, "stage ring too shallow");
     static constexpr int kTmemCols = 2 * BN < 64 ? 64 : 2 * BN;  // two accumulators
     static constexpr int kXchgBytes = 128 * 33 * 4;
-    static constexpr int kTokBytes = 256 * 16;
+    static constexpr int kTokBytes = 256 * 24;  // tok_inv, tok_pos, tok_kv, best
     static constexpr int kBarBytes = 512;
     static constexpr int kSmem = 1024 + kStages * kStageBytes + kXchgBytes + kTokBytes + kBarBytes;
 };
@@ -128,6 +128,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     float* tok_inv = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(xchg) + C::kXchgBytes);  // [256]
     int* tok_pos = reinterpret_cast<int*>(tok_inv + 256);                                // [256]
     long long* tok_kv = reinterpret_cast<long long*>(tok_pos + 256);                     // [256]
+    unsigned long long* best = reinterpret_cast<unsigned long long*>(tok_kv + 256);     // [256] ARGMAX
     uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(tok_inv) + C::kTokBytes);
     uint64_t* empty = full + C::kStages;
     uint64_t* acc_full = empty + C::kStages;  // [2]
@@ -283,6 +284,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
 
         SwapEpi E{&args, xchg, tok_inv, tok_pos, tok_kv, row, lane, quarter, n_live};
+        if constexpr (MODE == EPI_ARGMAX) {
+            for (int t = e; t < 256; t += 128) best[t] = 0ull;
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            E.best = best;
+        }
         auto emit_swap_l = [&](int m0, int c, const float (&v)[32]) { emit_swap<MODE>(E, m0, c, v); };
 
         // normal mode: row = token m0 + row, columns = features n0 + [c, c + 32)
@@ -463,6 +469,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                 asm volatile("bar.sync 2, 128;" ::: "memory");  // last_flag reuse
             }
         }
+        if constexpr (MODE == EPI_ARGMAX) {  // flush the CTA's per-token maxima
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            for (int t = e; t < BN && t < n_live; t += 128)
+                if (best[t]) atomicMax(args.argmax + t, best[t]);
+        }
     }
     tc_fence_before();
     __syncthreads();
@@ -584,23 +595,16 @@ void gemm_run(const GemmProblem& p, cudaStream_t st) {
         static const int dec_env = env_flag("SW_GEMM_DEC", 1);
         if (dec_env && p.mode != EPI_ARGMAX && p.ws) {
             // decode projections: cluster split-K, column-distributed reduction
+            // two CTAs per SM fit (<= 112 KB smem each); measured: 2 x SMs beats 1 x SMs
+            // on the Llama-1B step (tools/profile_step.py)
             static const int dec_ctas = env_flag("SW_DEC_CTAS", 0);
-            const int S = gemm_decode_splits(tiles, p.K / BK, dec_ctas > 0 ? dec_ctas : sms);
+            const int S = gemm_decode_splits(tiles, p.K / BK, dec_ctas > 0 ? dec_ctas : 2 * sms);
             if (S == 1 || gemm_decode_ws_floats(tiles, S, bn) <= p.ws_floats) {
                 a.stream_k = 0;
                 gemm_decode_run(tmap_cached(p.W, p.w_rows, p.K, BM), tmap_cached(p.X, p.x_rows, p.K, bn), a, bn, S,
                                 tiles, st);
                 return;
             }
-        }
-        static const int cl_env = env_flag("SW_GEMM_CLUSTER", 0);  // measured slower at b=64 (profiles/r01)
-        if (cl_env && bn <= 64 && p.mode != EPI_ARGMAX && tiles < 2 * sms) {
-            // decode projections: a tile per cluster of k CTAs, reduced through DSMEM
-            const int k = gemm_cluster_size(tiles, p.K / BK, sms);
-            a.stream_k = 0;
-            gemm_cluster_run(tmap_cached(p.W, p.w_rows, p.K, BM), tmap_cached(p.X, p.x_rows, p.K, bn), a, bn, k,
-                             tiles, st);
-            return;
         }
         const long long iters = static_cast<long long>(tiles) * (p.K / BK);
         // Stream-K over every SM when there is split-K scratch; the split

@@ -86,13 +86,10 @@ struct GemmProblem {
 CUtensorMap make_tmap_bf16(const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows);
 const CUtensorMap& tmap_cached(const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows);
 void gemm_run(const GemmProblem& p, cudaStream_t st);
-int gemm_cluster_size(int tiles, int nk, int sms);
 // decode projections: split-K over a cluster (gemm_decode.cu)
 int gemm_decode_splits(int tiles, int nk, int ctas);
 size_t gemm_decode_ws_floats(int tiles, int S, int bn);
 void gemm_decode_run(const CUtensorMap& a, const CUtensorMap& b, const GemmArgs& args, int bn, int S, int tiles,
                      cudaStream_t st);
-void gemm_cluster_run(const CUtensorMap& a, const CUtensorMap& b, const GemmArgs& args, int bn, int k, int tiles,
-                      cudaStream_t st);
 
 }  // namespace sw
