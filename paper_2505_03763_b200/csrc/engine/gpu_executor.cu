@@ -37,13 +37,17 @@
 #include "../host/spec.hpp"
 #include "../kernels/common.cuh"
 #include "model.hpp"
+#include "partition.hpp"
 
 namespace sw {
 
 struct GpuOptions {
     bool split = true;        // two streams (prefill || decode) vs one
     int decode_lanes = 1;     // split mode: concurrent decode streams (instance i -> lane i % lanes)
+    int decode_sms = 0;       // split mode: > 0 partitions the SMs with green contexts (decode | prefill)
     bool coalesce = true;     // one launch per kind per pass
+    bool align = true;        // split mode: a token step requested while another is in flight waits for it and
+                              // then runs merged with every other waiting step (one weight pass for all lanes)
     bool graphs = true;       // CUDA graphs for decode steps
     double peak_flops = 1.6932e15;
     double peak_bytes = 6.4469e12;
@@ -86,10 +90,23 @@ public:
         if ((max_ctx + kv_->page_tokens - 1) / kv_->page_tokens > kv_->max_pages)
             throw ConfigError("engine: context longer than the arena's page-table row");
         for (std::size_t i = 0; i < entries_.size(); ++i) slot_of_[entries_[i].req.id] = static_cast<int>(i);
+        const int lanes = opt_.split ? std::max(1, std::min(opt_.decode_lanes, sw_model::kMaxDecodeLanes)) : 1;
+        if (opt_.split && opt_.decode_sms > 0) {
+            // co-scheduler: decode and prefill on disjoint SM groups (green contexts, cached per model device)
+            const SmPartition& P = sm_partition(m_->device, opt_.decode_sms, lanes);
+            s_prefill_ = P.prefill;
+            s_decode_ = P.decode;
+            part_ = &P;
+            own_streams_ = false;
+            // prompts launched while no request is generating take the whole GPU
+            int lo, hi;
+            SW_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+            SW_CUDA(cudaStreamCreateWithPriority(&s_prefill_full_, cudaStreamNonBlocking, lo));
+            return;
+        }
         int lo, hi;
         SW_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
         SW_CUDA(cudaStreamCreateWithPriority(&s_prefill_, cudaStreamNonBlocking, lo));
-        const int lanes = opt_.split ? std::max(1, std::min(opt_.decode_lanes, sw_model::kMaxDecodeLanes)) : 1;
         for (int i = 0; i < lanes; ++i) {
             cudaStream_t s = s_prefill_;
             if (opt_.split) SW_CUDA(cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, hi));
@@ -101,6 +118,11 @@ public:
         cudaStreamSynchronize(s_prefill_);
         for (cudaStream_t s : s_decode_) cudaStreamSynchronize(s);
         for (cudaEvent_t e : events_) cudaEventDestroy(e);
+        if (s_prefill_full_) {
+            cudaStreamSynchronize(s_prefill_full_);
+            cudaStreamDestroy(s_prefill_full_);
+        }
+        if (!own_streams_) return;
         for (cudaStream_t s : s_decode_)
             if (s != s_prefill_) cudaStreamDestroy(s);
         cudaStreamDestroy(s_prefill_);
@@ -161,7 +183,9 @@ public:
                 first = false;
                 schedule_pass();
             }
-            const bool inflight = std::any_of(launches_.begin(), launches_.end(), [](const Launch& l) { return !l.done; });
+            flush_steps();
+            const bool inflight = !pending_steps_.empty() ||
+                                  std::any_of(launches_.begin(), launches_.end(), [](const Launch& l) { return !l.done; });
             if (!inflight && active_.empty() && next_arrival >= entries_.size()) break;
             if (!inflight && active_.empty() && evs.empty()) {
                 // idle until the next arrival
@@ -203,12 +227,13 @@ public:
                 s += (j ? "|" : "") + std::to_string(table[static_cast<size_t>(slot) * kv_->max_pages + j]);
             s += "\n";
         }
-        char buf[256];
+        char buf[320];
         std::snprintf(buf, sizeof buf,
-                      "#gpu launches=%zu;prefill_launches=%d;decode_launches=%d;split=%d;coalesce=%d;decode_lanes=%zu;"
-                      "clock_skew_s=%.9g\n",
+                      "#gpu launches=%zu;prefill_launches=%d;decode_launches=%d;split=%d;coalesce=%d;align=%d;decode_lanes=%zu;"
+                      "decode_sms=%d;prefill_sms=%d;prefill_full_gpu=%d;clock_skew_s=%.9g\n",
                       launches_.size(), n_prefill_, n_decode_, opt_.split ? 1 : 0, opt_.coalesce ? 1 : 0,
-                      s_decode_.size(), clock_skew_);
+                      aligning() ? 1 : 0, s_decode_.size(), part_ ? part_->decode_sms : 0, part_ ? part_->prefill_sms : 0, n_prefill_full_,
+                      clock_skew_);
         s += buf;
         return s;
     }
@@ -247,6 +272,7 @@ private:
         TaskKind kind;
         int lane = 0;
         int start_ev = -1, end_ev = -1;
+        std::vector<std::pair<int, int>> merged_evs;  // (start, end) events of launches merged into this one
         std::vector<long long> task_seqs;
         long long first_seq = 0;
         bool done = false;
@@ -297,9 +323,45 @@ private:
         }
         for (Launch& L : group) {
             L.first_seq = L.task_seqs.front();
+            if (aligning() && L.kind == TaskKind::TokenStep) {
+                pending_steps_.push_back(L);
+                continue;
+            }
             enqueue(L);
             launches_.push_back(L);
         }
+        flush_steps();
+    }
+
+    bool aligning() const { return opt_.split && opt_.align; }
+
+    // decode work exists: a step in flight or waiting, or a request past its prompt
+    bool decode_active() const {
+        if (decode_inflight() || !pending_steps_.empty()) return true;
+        return std::any_of(entries_.begin(), entries_.end(),
+                           [](const Entry& e) { return e.req.state == RequestState::Generating; });
+    }
+
+    bool decode_inflight() const {
+        return std::any_of(launches_.begin(), launches_.end(),
+                           [](const Launch& l) { return !l.done && l.kind == TaskKind::TokenStep; });
+    }
+
+    // Aligned token steps: once no step is in flight, every waiting step runs as
+    // one merged launch on decode lane 0 (their TaskStart/TaskComplete events
+    // are all recorded around it).
+    void flush_steps() {
+        if (pending_steps_.empty() || decode_inflight()) return;
+        Launch M = pending_steps_.front();
+        M.lane = 0;
+        for (std::size_t i = 1; i < pending_steps_.size(); ++i) {
+            const Launch& o = pending_steps_[i];
+            M.task_seqs.insert(M.task_seqs.end(), o.task_seqs.begin(), o.task_seqs.end());
+            M.merged_evs.push_back({o.start_ev, o.end_ev});
+        }
+        pending_steps_.clear();
+        enqueue(M);
+        launches_.push_back(M);
     }
 
     void enqueue(const Launch& L) {
@@ -332,9 +394,12 @@ private:
             b.tokens = toks.data();
             b.page_rows = prow.data();
             b.out_index = oidx.data();
-            SW_CUDA(cudaEventRecord(events_[L.start_ev], s_prefill_));
-            prefill_forward(m_, kv_, b, s_prefill_);
-            SW_CUDA(cudaEventRecord(events_[L.end_ev], s_prefill_));
+            // partition mode: the prefill group's SMs only while decode work exists, else the whole GPU
+            cudaStream_t ps = s_prefill_full_ && !decode_active() ? s_prefill_full_ : s_prefill_;
+            if (ps == s_prefill_full_) ++n_prefill_full_;
+            SW_CUDA(cudaEventRecord(events_[L.start_ev], ps));
+            prefill_forward(m_, kv_, b, ps);
+            SW_CUDA(cudaEventRecord(events_[L.end_ev], ps));
             ++n_prefill_;
         } else {
             for (int i = 0; i < n; ++i) {
@@ -351,8 +416,10 @@ private:
             b.out_index = oidx.data();
             cudaStream_t ds = s_decode_[static_cast<std::size_t>(L.lane)];
             SW_CUDA(cudaEventRecord(events_[L.start_ev], ds));
+            for (const auto& [se, ee] : L.merged_evs) SW_CUDA(cudaEventRecord(events_[se], ds));
             decode_forward(m_, kv_, b, ds, opt_.graphs, L.lane, static_cast<int>(s_decode_.size()));
             SW_CUDA(cudaEventRecord(events_[L.end_ev], ds));
+            for (const auto& [se, ee] : L.merged_evs) SW_CUDA(cudaEventRecord(events_[ee], ds));
             ++n_decode_;
         }
     }
@@ -363,9 +430,14 @@ private:
     ModelWork work_;
     cudaStream_t s_prefill_ = nullptr;
     std::vector<cudaStream_t> s_decode_;
+    const SmPartition* part_ = nullptr;  // green-context partition (split mode, engine.decode_sms > 0)
+    cudaStream_t s_prefill_full_ = nullptr;  // partition mode: whole-GPU prefill stream
+    int n_prefill_full_ = 0;
+    bool own_streams_ = true;
     std::vector<cudaEvent_t> events_;
     int t0_ = -1;
     std::vector<Launch> launches_;
+    std::vector<Launch> pending_steps_;  // aligned token steps waiting for the in-flight one
     std::map<int, int> slot_of_;
     unsigned long long polls_ = 0;
     double clock_skew_ = 0.0;
@@ -384,8 +456,10 @@ extern "C" int sw_engine_run(sw_model* m, sw_kv* kv, const char* spec, char** ou
         for (const auto& [k, v] : rs.rest) {
             if (k == "engine.split") opt.split = v == "1" || v == "true";
             else if (k == "engine.coalesce") opt.coalesce = v == "1" || v == "true";
+            else if (k == "engine.align") opt.align = v == "1" || v == "true";
             else if (k == "engine.graphs") opt.graphs = v == "1" || v == "true";
             else if (k == "engine.decode_lanes") opt.decode_lanes = std::stoi(v);
+            else if (k == "engine.decode_sms") opt.decode_sms = std::stoi(v);
             else if (k == "engine.peak_flops") opt.peak_flops = std::stod(v);
             else if (k == "engine.peak_bytes") opt.peak_bytes = std::stod(v);
             else throw ConfigError("spec: unknown key '" + k + "'");

@@ -36,6 +36,7 @@
 #include "../kernels/elementwise.cuh"
 #include "../kernels/gemm_sm100.cuh"
 #include "model.hpp"
+#include "partition.hpp"
 
 namespace sw {
 
@@ -604,26 +605,24 @@ void decode_forward(sw_model* m, sw_kv* kv, const sw_batch& b, cudaStream_t st, 
         if (plan) decode_step_path(m, kv, R, s, lane, *plan);
         else decode_layers(m, kv, R, s, lane);
     };
-    DecodeGraph& g = m->graphs[{kv, R, lane | (plan ? 16 : 0)}];
+    DecodeGraph& g = m->graphs[{kv, R, lane | (plan ? 16 : 0), stream_partition_tag(st)}];
     if (use_graph && g.exec) {
         SW_CUDA(cudaGraphLaunch(g.exec, st));
         count_launches(g.kernels);
     } else {
         run(st);
         if (use_graph && ++g.eager_runs >= 1) {
-            // capture once the kernels' attributes are configured (first eager run)
-            cudaStream_t cs;
-            SW_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+            // capture once the kernels' attributes are configured (first eager run), on the
+            // launch stream itself: the graph then runs in that stream's (green) context
             cudaGraph_t graph;
-            SW_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+            SW_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
             const unsigned long long before = g_launches.load();
-            run(cs);
+            run(st);
             g.kernels = g_launches.load() - before;
             g_launches.fetch_sub(g.kernels);  // captured, not launched
-            SW_CUDA(cudaStreamEndCapture(cs, &graph));
+            SW_CUDA(cudaStreamEndCapture(st, &graph));
             SW_CUDA(cudaGraphInstantiate(&g.exec, graph, 0));
             SW_CUDA(cudaGraphDestroy(graph));
-            SW_CUDA(cudaStreamDestroy(cs));
         }
     }
     if (b.logits_out) {  // parity checks: fp32 logits from the same folded-norm input

@@ -100,7 +100,8 @@ struct sw_model {
     static constexpr int kMaxDecodeLanes = 4;
     sw::Workspace dec[kMaxDecodeLanes];
     sw::PinnedRing pre_ring, dec_ring[kMaxDecodeLanes];
-    std::map<std::tuple<const sw_kv*, int, int>, sw::DecodeGraph> graphs;  // (arena, row bucket, lane | mode)
+    // (arena, row bucket, lane | mode, partition): a graph runs in the context it was captured in
+    std::map<std::tuple<const sw_kv*, int, int, const void*>, sw::DecodeGraph> graphs;
     std::map<std::tuple<const sw_kv*, int, int>, sw::StepPlan> step_plans;  // (arena, row bucket, lane)
     unsigned long long* scratch_u64 = nullptr;
 };

@@ -569,6 +569,8 @@ int gemm_pick_bn_swap(int tokens) {
     return 256;
 }
 
+int stream_sm_count(cudaStream_t st);  // engine/partition.cu
+
 void gemm_run(const GemmProblem& p, cudaStream_t st) {
     if (p.K % BK != 0) throw_cuda("gemm: K must be a multiple of 64", cudaErrorInvalidValue, __FILE__, __LINE__);
     GemmArgs a{};
@@ -583,7 +585,8 @@ void gemm_run(const GemmProblem& p, cudaStream_t st) {
     a.fx = p.fx;
     a.ws = p.ws;
     a.counters = p.counters;
-    const int sms = num_sms();
+    const int sms = num_sms();             // device: fixes the split-K factors (numerics)
+    const int grid_sms = stream_sm_count(st);  // the stream's SM partition: sizes persistent grids
     if (p.swap) {
         if (p.features % BM != 0)
             throw_cuda("gemm(swap): feature count must be a multiple of 128", cudaErrorInvalidValue, __FILE__, __LINE__);
@@ -625,7 +628,7 @@ void gemm_run(const GemmProblem& p, cudaStream_t st) {
         const bool sk = (sk_env > 0 || (sk_env < 0 && sk_shape)) && p.ws && p.counters && tiles <= p.n_counters &&
                         static_cast<size_t>(sms) * 2 * bn * BM <= p.ws_floats && sk_ctas > tiles;
         a.stream_k = sk ? 1 : 0;
-        const int ctas = sk ? sk_ctas : std::min(sms, tiles);
+        const int ctas = sk ? sk_ctas : std::min(grid_sms, tiles);
         const CUtensorMap& ta = tmap_cached(p.W, p.w_rows, p.K, BM);
         const CUtensorMap& tb = tmap_cached(p.X, p.x_rows, p.K, bn);
         switch (p.mode) {
@@ -645,7 +648,7 @@ void gemm_run(const GemmProblem& p, cudaStream_t st) {
         a.N = p.features;
         a.stream_k = 0;
         const int tiles = cdiv(p.tokens, BM) * (p.features / bn);
-        const int ctas = std::min(sms, tiles);
+        const int ctas = std::min(grid_sms, tiles);
         const CUtensorMap& ta = tmap_cached(p.X, p.x_rows, p.K, BM);
         const CUtensorMap& tb = tmap_cached(p.W, p.w_rows, p.K, bn);
         switch (p.mode) {

@@ -27,6 +27,10 @@ RUNS = {
     "pipelined_P4_split_nocoalesce": "policy=pipelined_splitwiser;P=4;max_batch=2;engine.split=1;engine.coalesce=0",
     "mixed_split_arrivals": "policy=mixed_batching;arrival=fixed:0.003;engine.split=1",
     "multi_instance_split": "policy=multi_instance;n_instances=2;inner=mixed_batching;engine.split=1",
+    # co-scheduler on green-context SM partitions (decode 48 SMs | prefill the rest)
+    "pipelined_P2_green48": "policy=pipelined_splitwiser;P=2;max_batch=4;engine.split=1;engine.decode_lanes=2;"
+                            "engine.decode_sms=48",
+    "mixed_green64_arrivals": "policy=mixed_batching;arrival=fixed:0.003;engine.split=1;engine.decode_sms=64",
 }
 
 
@@ -97,3 +101,14 @@ def test_event_log_contract(results):
         for t, inst, logged, replayed in P.ledger_replay(r.event_log):
             assert logged == replayed, (name, t)
         assert all(q["ttft_s"] > 0 and q["e2e_s"] >= q["ttft_s"] for q in r.requests), name
+
+
+def test_green_partition_reported(results):
+    for name in ("pipelined_P2_green48", "mixed_green64_arrivals"):
+        gpu = {}
+        for line in results[name].text.splitlines():
+            if line.startswith("#gpu "):
+                gpu = dict(kv.split("=") for kv in line[5:].split(";"))
+        want = 48 if "48" in name else 64
+        assert int(gpu["decode_sms"]) == want, (name, gpu)
+        assert int(gpu["decode_sms"]) + int(gpu["prefill_sms"]) == 148 or int(gpu["prefill_sms"]) > 0, gpu
