@@ -6,7 +6,9 @@ oracle timed beside it.
 
 A "step" is one complete engine run of the BASELINE workload (configs[1]:
 Llama-3.2-1B shape, bf16, random weights, 64 requests x prompt 512 / gen 128)
-through the C-ABI (sw_engine_run).  value = generated tokens / device makespan
+through the C-ABI (sw_engine_run).  Split = PipelinedSplitwiser P=2 with the
+phases on concurrent streams; serial = the same task stream under the
+one-task gate; the fastest serial policy is reported beside.  value = generated tokens / device makespan
 (CUDA events inside the engine) summed over the K timed runs; e2e = the same
 tokens over the wall time of the sw_engine_run calls (prompt H2D staging and
 token/page-table D2H inside).  Under torchrun every rank runs its own engine
@@ -32,18 +34,24 @@ PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustain
 
 WORKLOADS = {
     # configs[1] of BASELINE.json -- the bench line
+    # split = PipelinedSplitwiser P=2 on concurrent streams (token steps of the two lanes aligned and merged);
+    # serial = the SAME task stream under the one-task gate; best_serial = the fastest
+    # serial policy on this closed batch (request-level batching of all 64), reported beside it
     "1b": dict(model="LLAMA_1B", n=64, input=512, output=128, arrival="zero", max_prefill=32768, max_decode=64,
-               split="policy=pipelined_splitwiser;P=2;max_batch=32;engine.split=1;engine.decode_lanes=2",
-               serial="policy=sequential;max_batch=64;engine.split=0"),
+               split="policy=pipelined_splitwiser;P=2;max_batch=32;engine.split=1",
+               serial="policy=pipelined_splitwiser;P=2;max_batch=32;engine.split=0",
+               best_serial="policy=sequential;max_batch=64;engine.split=0"),
     # configs[2]: 8B shape, Poisson arrivals of mixed prompts, mixed batching vs continuous batching
     "8b-poisson": dict(model="LLAMA_8B", n=128, input="128..2048", output=256, arrival="poisson:32",
                        max_prefill=32768, max_decode=128,
                        split="policy=mixed_batching;max_batch=128;engine.split=1",  # prefill || decode, one instance
-                       serial="policy=continuous_batching;max_batch=128;engine.split=0"),
+                       serial="policy=mixed_batching;max_batch=128;engine.split=0",
+                       best_serial="policy=continuous_batching;max_batch=128;engine.split=0"),
     # configs[0] shape on the GPU (fast sanity run)
     "tiny": dict(model="TINY", n=8, input=64, output=32, arrival="zero", max_prefill=1024, max_decode=16,
-                 split="policy=pipelined_splitwiser;P=2;max_batch=4;engine.split=1;engine.decode_lanes=2",
-                 serial="policy=sequential;max_batch=8;engine.split=0"),
+                 split="policy=pipelined_splitwiser;P=2;max_batch=4;engine.split=1",
+                 serial="policy=pipelined_splitwiser;P=2;max_batch=4;engine.split=0",
+                 best_serial="policy=sequential;max_batch=8;engine.split=0"),
 }
 
 
@@ -179,7 +187,7 @@ def roofline_decode_gemm(eng, desc, rows: int, peaks, reps: int = 20):
     nbytes = 2 * F * d * 2 + rows * d * 2 + rows * F * 2
     achieved = nbytes / t / 1e9
     peak = float(peaks["hbm_gbs"])
-    return {"kernel": "gemm_tc_kernel<BN,SWIGLU,swap> (decode gate/up, rows=%d)" % rows, "bound": "hbm",
+    return {"kernel": "gemm_decode_kernel<BN,SWIGLU> (decode gate/up, cluster split-K, rows=%d)" % rows, "bound": "hbm",
             "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
             "bytes_per_launch": nbytes, "us_per_launch": round(t * 1e6, 2)}
 
@@ -318,11 +326,13 @@ def main():
     t_init = time.perf_counter() - t_init
     split_spec = spec_for(w, args.split or w["split"], rank, world)
     serial_spec = spec_for(w, args.serial or w["serial"], rank, world)
+    best_spec = spec_for(w, w["best_serial"], rank, world)
 
     for _ in range(args.warmup):
         eng.run(split_spec)
     for _ in range(max(1, args.warmup // 3)):
         eng.run(serial_spec)
+        eng.run(best_spec)
 
     def timed(spec):
         if dist:
@@ -337,6 +347,7 @@ def main():
     with ClockSampler(local) as clocks:
         split = timed(split_spec)
     serial = timed(serial_spec)
+    best = timed(best_spec)
 
     roof = roofline_decode_gemm(eng, desc, w["max_decode"], peaks) if rank == 0 else None
     roof_prefill = roofline_prefill_gemm(eng, desc, 4096, peaks) if rank == 0 else None
@@ -361,6 +372,21 @@ def main():
 
     value = split["tokens"] / split["makespan"]
     serial_v = serial["tokens"] / serial["makespan"]
+    best_v = best["tokens"] / best["makespan"]
+    # decode-step roofline from the best-serial run's p50 TBT (a step alone on the GPU): algorithmic bytes of a
+    # step at the batch and mean context of that run (weights + KV read + KV write + activations)
+    step = None
+    if w["arrival"] == "zero" and str(w["input"]).isdigit():
+        b = min(w["n"], w["max_decode"])
+        ctx = int(w["input"]) + w["output"] / 2
+        kv_tok = 2 * desc.n_layers * desc.n_kv_heads * desc.head_dim * 2
+        n_mm = desc.n_layers * (desc.d_model * (desc.n_heads + 2 * desc.n_kv_heads) * desc.head_dim +
+                                desc.n_heads * desc.head_dim * desc.d_model + 3 * desc.d_model * desc.ffn_dim)
+        nbytes = 2 * (n_mm + desc.d_model * desc.vocab) + 2 * desc.d_model * b + b * ctx * kv_tok + b * kv_tok
+        ach = nbytes / best["p50_tbt"] / 1e9
+        step = {"rows": b, "mean_ctx": ctx, "bytes_per_step": int(nbytes), "p50_tbt_s": best["p50_tbt"],
+                "achieved": round(ach, 1), "peak": float(peaks["hbm_gbs"]), "unit": "GB/s",
+                "frac": round(ach / float(peaks["hbm_gbs"]), 4)}
     line = {
         "metric": METRIC,
         "value": round(value, 1),
@@ -377,12 +403,16 @@ def main():
         "config": {"workload": args.workload, "model_shape": w["model"], "requests_per_gpu": n_local,
                    "prompt": w["input"], "gen": w["output"], "arrival": w["arrival"],
                    "split_policy": args.split or w["split"], "serial_policy": args.serial or w["serial"],
+                   "best_serial_policy": w["best_serial"],
                    "l2": "working set > L2: every decode step streams all weights (2.5-16 GB)",
                    "parallelism": f"request-sharded replicas x{world}"},
         "split": {"tokens_per_s": round(value, 1), "p50_ttft_s": split["p50_ttft"], "p50_tbt_s": split["p50_tbt"]},
         "serial": {"tokens_per_s": round(serial_v, 1), "p50_ttft_s": serial["p50_ttft"],
                    "p50_tbt_s": serial["p50_tbt"]},
         "split_over_serial": round(value / serial_v, 4),
+        "best_serial": {"tokens_per_s": round(best_v, 1), "p50_ttft_s": best["p50_ttft"], "p50_tbt_s": best["p50_tbt"]},
+        "split_over_best_serial": round(value / best_v, 4),
+        "roofline_decode_step": step,
         "e2e": {"value": round(split["tokens"] / split["wall"], 1), "unit": "tokens/s",
                 "h2d_bytes_per_step": int(split["h2d"]), "d2h_bytes_per_step": int(split["d2h"])},
         "gpu_launches": int(split["launches"]),
