@@ -369,6 +369,7 @@ void decode_layers(sw_model* m, sw_kv* kv, int R, cudaStream_t st, int lane) {
         p.fx.x_bf16 = xb;
         p.fx.ss_part_out = ss_out;
     };
+    static const int ablate = env_int("SW_ABLATE", 0);  // timing experiments only: skip kernel classes
     for (int l = 0; l < d.n_layers; ++l) {
         const LayerWeights& L = m->layers[l];
         __nv_bfloat16* kvl = kv->pages + l * kv->layer_stride;
@@ -386,24 +387,24 @@ void decode_layers(sw_model* m, sw_kv* kv, int R, cudaStream_t st, int lane) {
         pq.fx.H = d.n_heads;
         pq.fx.Hkv = d.n_kv_heads;
         pq.fx.hd = d.head_dim;
-        gemm_run(pq, st);
-        attn_decode(w.q, kvl, w.attn, aa, R, d.head_dim, st);
+        if (!(ablate & 2)) gemm_run(pq, st);
+        if (!(ablate & 1)) attn_decode(w.q, kvl, w.attn, aa, R, d.head_dim, st);
         GemmProblem po = gp(w.attn, w.rows, L.wo, d.d_model, R, d.d_model, hdH, EPI_RESID, true, w.x, d.d_model, live, &w);
         resid_out(po, ss_b);
-        gemm_run(po, st);
+        if (!(ablate & 4)) gemm_run(po, st);
         GemmProblem pg = gp(xb, w.rows, L.wgu, 2 * d.ffn_dim, R, 2 * d.ffn_dim, d.d_model, EPI_SWIGLU, true, w.act,
                             d.ffn_dim, live, &w);
         norm_in(pg, ss_b, parts);
-        gemm_run(pg, st);
+        if (!(ablate & 8)) gemm_run(pg, st);
         GemmProblem pd = gp(w.act, w.rows, L.wd, d.d_model, R, d.d_model, d.ffn_dim, EPI_RESID, true, w.x, d.d_model,
                             live, &w);
         resid_out(pd, ss_a);
-        gemm_run(pd, st);
+        if (!(ablate & 16)) gemm_run(pd, st);
     }
     GemmProblem pl = gp(xb, w.rows, m->lm, d.vocab, R, d.vocab, d.d_model, EPI_ARGMAX, true, nullptr, 0, live);
     pl.argmax = w.keys;
     norm_in(pl, ss_a, parts);  // argmax is scale invariant; kept so logits and argmax see one definition
-    gemm_run(pl, st);
+    if (!(ablate & 32)) gemm_run(pl, st);
     finalize_tokens(w.keys, w.meta->slot, w.meta->out_index, R, live, kv->last_token, kv->out_tokens, kv->max_out, st);
 }
 
@@ -614,15 +615,20 @@ void decode_forward(sw_model* m, sw_kv* kv, const sw_batch& b, cudaStream_t st, 
         if (use_graph && ++g.eager_runs >= 1) {
             // capture once the kernels' attributes are configured (first eager run), on the
             // launch stream itself: the graph then runs in that stream's (green) context
+            // (the legacy default stream cannot capture: use a scratch stream of the primary context)
+            const bool legacy = st == nullptr || st == cudaStreamLegacy || st == cudaStreamPerThread;
+            cudaStream_t cs = st;
+            if (legacy) SW_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
             cudaGraph_t graph;
-            SW_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+            SW_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
             const unsigned long long before = g_launches.load();
-            run(st);
+            run(cs);
             g.kernels = g_launches.load() - before;
             g_launches.fetch_sub(g.kernels);  // captured, not launched
-            SW_CUDA(cudaStreamEndCapture(st, &graph));
+            SW_CUDA(cudaStreamEndCapture(cs, &graph));
             SW_CUDA(cudaGraphInstantiate(&g.exec, graph, 0));
             SW_CUDA(cudaGraphDestroy(graph));
+            if (legacy) SW_CUDA(cudaStreamDestroy(cs));
         }
     }
     if (b.logits_out) {  // parity checks: fp32 logits from the same folded-norm input

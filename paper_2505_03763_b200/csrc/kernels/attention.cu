@@ -207,7 +207,8 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(const __nv_bfloat16* _
     extern __shared__ __align__(128) uint8_t dsm[];
     __shared__ uint32_t s_last;
     __shared__ int32_t s_pages[kMaxChunkPages];
-    griddep_launch_dependents();
+    // No early launch_dependents: the successor GEMM's CTAs (~112 KB smem) would
+    // take the SM slots this kernel's later waves need; it launches as we exit.
     griddep_wait();
     const int n_rows = a.meta->n;
     const int row = blockIdx.z;

@@ -33,6 +33,7 @@
 #include <cuda.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <map>
 #include <mutex>
@@ -602,6 +603,14 @@ void gemm_run(const GemmProblem& p, cudaStream_t st) {
             // on the Llama-1B step (tools/profile_step.py)
             static const int dec_ctas = env_flag("SW_DEC_CTAS", 0);
             const int S = gemm_decode_splits(tiles, p.K / BK, dec_ctas > 0 ? dec_ctas : 2 * sms);
+            static const int dec_log = env_flag("SW_DEC_LOG", 0);
+            if (dec_log) {
+                static std::mutex mu;
+                static std::map<std::tuple<int, int, int>, int> seen;
+                std::lock_guard<std::mutex> lk(mu);
+                if (seen.emplace(std::make_tuple(tiles, p.K, bn), S).second)
+                    std::fprintf(stderr, "[gemm_decode] tiles=%d K=%d bn=%d mode=%d -> S=%d\n", tiles, p.K, bn, p.mode, S);
+            }
             if (S == 1 || gemm_decode_ws_floats(tiles, S, bn) <= p.ws_floats) {
                 a.stream_k = 0;
                 gemm_decode_run(tmap_cached(p.W, p.w_rows, p.K, BM), tmap_cached(p.X, p.x_rows, p.K, bn), a, bn, S,
