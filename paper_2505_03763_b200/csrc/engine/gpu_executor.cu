@@ -45,6 +45,7 @@ struct GpuOptions {
     bool split = true;        // two streams (prefill || decode) vs one
     int decode_lanes = 1;     // split mode: concurrent decode streams (instance i -> lane i % lanes)
     int decode_sms = 0;       // split mode: > 0 partitions the SMs with green contexts (decode | prefill)
+    bool lean_prefill = false;  // split mode: prompts launched while decode work exists use co-resident GEMM tiles
     bool coalesce = true;     // one launch per kind per pass
     bool align = true;        // split mode: a token step requested while another is in flight waits for it and
                               // then runs merged with every other waiting step (one weight pass for all lanes)
@@ -230,10 +231,10 @@ public:
         char buf[320];
         std::snprintf(buf, sizeof buf,
                       "#gpu launches=%zu;prefill_launches=%d;decode_launches=%d;split=%d;coalesce=%d;align=%d;decode_lanes=%zu;"
-                      "decode_sms=%d;prefill_sms=%d;prefill_full_gpu=%d;clock_skew_s=%.9g\n",
+                      "decode_sms=%d;prefill_sms=%d;prefill_full_gpu=%d;prefill_lean=%d;clock_skew_s=%.9g\n",
                       launches_.size(), n_prefill_, n_decode_, opt_.split ? 1 : 0, opt_.coalesce ? 1 : 0,
                       aligning() ? 1 : 0, s_decode_.size(), part_ ? part_->decode_sms : 0, part_ ? part_->prefill_sms : 0, n_prefill_full_,
-                      clock_skew_);
+                      n_prefill_lean_, clock_skew_);
         s += buf;
         return s;
     }
@@ -395,10 +396,13 @@ private:
             b.page_rows = prow.data();
             b.out_index = oidx.data();
             // partition mode: the prefill group's SMs only while decode work exists, else the whole GPU
-            cudaStream_t ps = s_prefill_full_ && !decode_active() ? s_prefill_full_ : s_prefill_;
+            const bool active = decode_active();
+            cudaStream_t ps = s_prefill_full_ && !active ? s_prefill_full_ : s_prefill_;
             if (ps == s_prefill_full_) ++n_prefill_full_;
+            const bool lean = opt_.split && opt_.lean_prefill && active;
+            n_prefill_lean_ += lean ? 1 : 0;
             SW_CUDA(cudaEventRecord(events_[L.start_ev], ps));
-            prefill_forward(m_, kv_, b, ps);
+            prefill_forward(m_, kv_, b, ps, lean);
             SW_CUDA(cudaEventRecord(events_[L.end_ev], ps));
             ++n_prefill_;
         } else {
@@ -433,6 +437,7 @@ private:
     const SmPartition* part_ = nullptr;  // green-context partition (split mode, engine.decode_sms > 0)
     cudaStream_t s_prefill_full_ = nullptr;  // partition mode: whole-GPU prefill stream
     int n_prefill_full_ = 0;
+    int n_prefill_lean_ = 0;
     bool own_streams_ = true;
     std::vector<cudaEvent_t> events_;
     int t0_ = -1;
@@ -460,6 +465,7 @@ extern "C" int sw_engine_run(sw_model* m, sw_kv* kv, const char* spec, char** ou
             else if (k == "engine.graphs") opt.graphs = v == "1" || v == "true";
             else if (k == "engine.decode_lanes") opt.decode_lanes = std::stoi(v);
             else if (k == "engine.decode_sms") opt.decode_sms = std::stoi(v);
+            else if (k == "engine.lean_prefill") opt.lean_prefill = v == "1" || v == "true";
             else if (k == "engine.peak_flops") opt.peak_flops = std::stod(v);
             else if (k == "engine.peak_bytes") opt.peak_bytes = std::stod(v);
             else throw ConfigError("spec: unknown key '" + k + "'");

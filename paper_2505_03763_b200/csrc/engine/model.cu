@@ -177,8 +177,12 @@ int decode_bucket(int n) {
 }
 
 // ------------------------------------------------------------------ prefill
-void prefill_forward(sw_model* m, sw_kv* kv, const sw_batch& b, cudaStream_t st) {
+void prefill_forward(sw_model* m, sw_kv* kv, const sw_batch& b, cudaStream_t st, bool lean) {
     const sw_model_desc& d = m->desc;
+    auto lp = [lean](GemmProblem p) {
+        p.lean = lean;
+        return p;
+    };
     Workspace& w = m->pre;
     const int B = kv->page_tokens;
     // Split the batch into chunks of whole prompts that fit the workspace.
@@ -275,16 +279,16 @@ void prefill_forward(sw_model* m, sw_kv* kv, const sw_batch& b, cudaStream_t st)
             const LayerWeights& L = m->layers[l];
             __nv_bfloat16* kvl = kv->pages + l * kv->layer_stride;
             rmsnorm(w.x, L.g_attn, w.xn, T, d.d_model, d.norm_eps, nullptr, nullptr, st);
-            gemm_run(gp(w.xn, w.rows, L.wqkv, qkv_w, T, qkv_w, d.d_model, EPI_STORE_F32, false, w.qkv, qkv_w), st);
+            gemm_run(lp(gp(w.xn, w.rows, L.wqkv, qkv_w, T, qkv_w, d.d_model, EPI_STORE_F32, false, w.qkv, qkv_w)), st);
             rope_kv(w.qkv, w.q, kvl, dev(tpos), dev(tslot), kv->page_table, m->rope_cs, T, nullptr, d.n_heads,
                     d.n_kv_heads, d.head_dim, kv->max_pages, B, st);
             attn_prefill(w.q, kvl, w.attn, aa, n_tiles, d.head_dim, st);
-            gemm_run(gp(w.attn, w.rows, L.wo, d.d_model, T, d.d_model, hdH, EPI_RESID, false, w.x, d.d_model), st);
+            gemm_run(lp(gp(w.attn, w.rows, L.wo, d.d_model, T, d.d_model, hdH, EPI_RESID, false, w.x, d.d_model)), st);
             rmsnorm(w.x, L.g_mlp, w.xn, T, d.d_model, d.norm_eps, nullptr, nullptr, st);
-            gemm_run(gp(w.xn, w.rows, L.wgu, 2 * d.ffn_dim, T, 2 * d.ffn_dim, d.d_model, EPI_SWIGLU, false, w.act,
-                        d.ffn_dim),
+            gemm_run(lp(gp(w.xn, w.rows, L.wgu, 2 * d.ffn_dim, T, 2 * d.ffn_dim, d.d_model, EPI_SWIGLU, false, w.act,
+                           d.ffn_dim)),
                      st);
-            gemm_run(gp(w.act, w.rows, L.wd, d.d_model, T, d.d_model, d.ffn_dim, EPI_RESID, false, w.x, d.d_model), st);
+            gemm_run(lp(gp(w.act, w.rows, L.wd, d.d_model, T, d.d_model, d.ffn_dim, EPI_RESID, false, w.x, d.d_model)), st);
         }
         // ---- last position of every prompt -> LM head + greedy token
         rmsnorm(w.x, m->g_final, w.xlast, S, d.d_model, d.norm_eps, nullptr, dev(lastrow), st);

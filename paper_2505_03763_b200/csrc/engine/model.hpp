@@ -124,7 +124,8 @@ struct sw_kv {
 namespace sw {
 constexpr int kMaxPositions = 32768;  // RoPE table extent (max context)
 // Forward passes (stream-ordered; host arrays staged internally).
-void prefill_forward(sw_model* m, sw_kv* kv, const sw_batch& b, cudaStream_t st);
+// lean: 128-wide prefill GEMM tiles in ~105 KB smem, so decode CTAs can share the SMs
+void prefill_forward(sw_model* m, sw_kv* kv, const sw_batch& b, cudaStream_t st, bool lean = false);
 void decode_forward(sw_model* m, sw_kv* kv, const sw_batch& b, cudaStream_t st, bool use_graph, int lane = 0,
                     int lanes = 1);
 int decode_bucket(int n);

@@ -54,16 +54,21 @@ constexpr int kThreads = 256;  // 8 warps
 constexpr int kEpiBase = 128;  // first epilogue thread (warp 4)
 constexpr int kMaxContrib = 8;  // stream-K: CTAs contributing to one tile (host enforces)
 
-template <int BN>
+// LEAN (prefill, BN = 128): ~105 KB of smem and 256 TMEM columns, so a decode
+// CTA (<= ~104 KB, <= 128 columns) fits on the same SM -- the co-resident
+// prefill the split executor launches while decode work exists.
+template <int BN, bool SWAP>
 struct GemmCfg {
+    static constexpr bool kLean = !SWAP && BN == 128;
     static constexpr int kABytes = BM * BK * 2;
     static constexpr int kBBytes = BN * BK * 2;
     static constexpr int kStageBytes = kABytes + kBBytes;
-    static constexpr int kStagesRaw = (192 * 1024) / kStageBytes > 8 ? 8 : (192 * 1024) / kStageBytes;
-    static constexpr int kStages = kStagesRaw & ~1;  // even: each producer owns fixed stages
-    static_assert(kStages >= 4, "stage ring too shallow");
+    static constexpr int kBudget = kLean ? 96 * 1024 : 192 * 1024;
+    static constexpr int kStagesRaw = kBudget / kStageBytes > 8 ? 8 : kBudget / kStageBytes;
+    static constexpr int kStages = kLean ? kStagesRaw : (kStagesRaw & ~1);
+    static_assert(kStages >= (kLean ? 3 : 4), "stage ring too shallow");
     static constexpr int kTmemCols = 2 * BN < 64 ? 64 : 2 * BN;  // two accumulators
-    static constexpr int kXchgBytes = 128 * 33 * 4;
+    static constexpr int kXchgBytes = SWAP ? 128 * 33 * 4 : 0;
     static constexpr int kTokBytes = 256 * 24;  // tok_inv, tok_pos, tok_kv, best
     static constexpr int kBarBytes = 512;
     static constexpr int kSmem = 1024 + kStages * kStageBytes + kXchgBytes + kTokBytes + kBarBytes;
@@ -120,7 +125,7 @@ struct SegIter {
 template <int BN, int MODE, bool SWAP>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmArgs args) {
-    using C = GemmCfg<BN>;
+    using C = GemmCfg<BN, SWAP>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sA = smem;
@@ -517,7 +522,7 @@ int num_sms() {
 
 template <int BN, int MODE, bool SWAP>
 void launch_one(const CUtensorMap& a, const CUtensorMap& b, const GemmArgs& args, int ctas, cudaStream_t st) {
-    using C = GemmCfg<BN>;
+    using C = GemmCfg<BN, SWAP>;
     static bool configured = false;  // per instantiation
     if (!configured) {
         SW_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<BN, MODE, SWAP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -650,7 +655,7 @@ void gemm_run(const GemmProblem& p, cudaStream_t st) {
             default: throw_cuda("gemm: bad epilogue", cudaErrorInvalidValue, __FILE__, __LINE__);
         }
     } else {
-        const int bn = 256;
+        const int bn = p.lean ? 128 : 256;
         if (p.features % bn != 0)
             throw_cuda("gemm: feature count must be a multiple of 256", cudaErrorInvalidValue, __FILE__, __LINE__);
         a.M = p.tokens;

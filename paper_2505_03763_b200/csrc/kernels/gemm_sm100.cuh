@@ -81,6 +81,7 @@ struct GemmProblem {
     unsigned* counters = nullptr;
     int n_counters = 0;
     DecodeFusion fx;  // swap-mode epilogue fusions
+    bool lean = false;  // normal mode: 128-wide tiles in ~105 KB smem (co-resident with decode CTAs)
 };
 
 CUtensorMap make_tmap_bf16(const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows);
