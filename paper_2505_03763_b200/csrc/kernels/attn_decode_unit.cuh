@@ -120,18 +120,29 @@ __device__ __forceinline__ void decode_unit(const DecodeAttnArgs& a, const __nv_
         qf[ks][3] = 0u;
     }
 
+    // A block is KB / kPage whole pages (blocks start page aligned); a (layer,
+    // page, kv head) K or V slice is one contiguous kPage x HD run, so lane l
+    // copies 16 B chunks l, l + 32, ... of it: one page-id read and one base
+    // address per page, the rest compile-time offsets (the generic per-chunk
+    // index math made this kernel integer-issue bound, profiles/r01b).
+    const char* kv_head = reinterpret_cast<const char*>(kv_layer + static_cast<int64_t>(hk) * kPage * HD);
+    const int64_t page_bytes = a.page_stride * 2, v_off = a.kv_stride * 2;
     auto load = [&](int blk, int buf) {
         const int k0 = k_begin + blk * KB;
-        for (int i = lane; i < KB * CH; i += 32) {
-            const int kr = i / CH, c = i % CH;
-            const int key = k0 + kr;
-            const bool ok = key < k_end;
-            const int page = ok ? s_pages[key / kPage - page_base] : 0;
-            const __nv_bfloat16* src = kv_layer + static_cast<int64_t>(page) * a.page_stride +
-                                       static_cast<int64_t>(hk) * kPage * HD +
-                                       static_cast<int64_t>(key % kPage) * HD + c * 8;
-            cp_async16(wK + buf * KB * HD + swz<HD>(kr, c), src, ok);
-            cp_async16(wV + buf * KB * HD + swz<HD>(kr, c), src + a.kv_stride, ok);
+#pragma unroll
+        for (int pg = 0; pg < KB / kPage; ++pg) {
+            const int key0 = k0 + pg * kPage;
+            const int page = key0 < k_end ? s_pages[key0 / kPage - page_base] : 0;
+            const char* src = kv_head + static_cast<int64_t>(page) * page_bytes;
+#pragma unroll
+            for (int j = 0; j < kPage * CH / 32; ++j) {
+                const int idx = lane + 32 * j;  // 16 B chunk of the page slice
+                const int r = idx / CH, c = idx % CH;
+                const bool ok = key0 + r < k_end;
+                const int dst = swz<HD>(pg * kPage + r, c);
+                cp_async16(wK + buf * KB * HD + dst, src + idx * 16, ok);
+                cp_async16(wV + buf * KB * HD + dst, src + v_off + idx * 16, ok);
+            }
         }
     };
 
