@@ -10,6 +10,7 @@
 //   H/Hkv query heads sharing a kv head are packed into one mma tile so every
 //   K/V byte is read once per step.  HBM-bound by design.
 #include <algorithm>
+#include <cstdlib>
 
 #include "attention.cuh"
 #include "attn_decode_unit.cuh"
@@ -200,10 +201,12 @@ __global__ void __launch_bounds__(128) attn_prefill_kernel(const __nv_bfloat16* 
 
 // ------------------------------------------------------------------ decode
 // One CTA = one unit (row, kv head, split of the context); see attn_decode_unit.cuh.
-template <int HD, int G, int KB>
-__global__ void __launch_bounds__(128) attn_decode_kernel(const __nv_bfloat16* __restrict__ q,
-                                                          const __nv_bfloat16* __restrict__ kv_layer,
-                                                          __nv_bfloat16* __restrict__ out, DecodeAttnArgs a) {
+// NS-stage per-warp K/V rings: NS = 3 keeps 2 blocks per warp in flight at two
+// CTAs per SM (more bytes in flight per SM than 3 CTAs x double buffers).
+template <int HD, int G, int KB, int NS>
+__global__ void __launch_bounds__(128, NS == 2 ? 3 : (NS == 3 ? 2 : 1))
+    attn_decode_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ kv_layer,
+                       __nv_bfloat16* __restrict__ out, DecodeAttnArgs a) {
     extern __shared__ __align__(128) uint8_t dsm[];
     __shared__ uint32_t s_last;
     __shared__ int32_t s_pages[kMaxChunkPages];
@@ -219,18 +222,19 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(const __nv_bfloat16* _
     const SplitPlan plan = decode_split_plan<KB>(ctx, cdiv(a.target_ctas, n_rows * a.Hkv), static_cast<int>(gridDim.x));
     const int split = blockIdx.x;
     if (split >= plan.splits) return;
-    decode_unit<HD, G, KB>(a, q, kv_layer, out, row, blockIdx.y, split, plan, ctx, dsm, s_pages, &s_last, threadIdx.x,
-                           [] { __syncthreads(); });
+    decode_unit<HD, G, KB, NS>(a, q, kv_layer, out, row, blockIdx.y, split, plan, ctx, dsm, s_pages, &s_last,
+                               threadIdx.x, [] { __syncthreads(); });
 }
 
-template <int HD, int G>
-void decode_launch(const __nv_bfloat16* q, const __nv_bfloat16* kv_layer, __nv_bfloat16* out, const DecodeAttnArgs& a,
-                   int max_rows, cudaStream_t st) {
+template <int HD, int G, int NS>
+void decode_launch_ns(const __nv_bfloat16* q, const __nv_bfloat16* kv_layer, __nv_bfloat16* out,
+                      const DecodeAttnArgs& a, int max_rows, cudaStream_t st) {
     constexpr int KB = decode_kb<HD>();
-    constexpr int smem = decode_unit_smem<HD, G>();
+    constexpr int smem = decode_unit_smem<HD, G, NS>();
     static bool cfg = false;
     if (!cfg) {
-        SW_CUDA(cudaFuncSetAttribute(attn_decode_kernel<HD, G, KB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        SW_CUDA(cudaFuncSetAttribute(attn_decode_kernel<HD, G, KB, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     smem));
         cfg = true;
     }
     // grid x: the most splits any row can take at this bucket size (the kernel
@@ -239,7 +243,19 @@ void decode_launch(const __nv_bfloat16* q, const __nv_bfloat16* kv_layer, __nv_b
     const int want = std::max(1, std::min(a.max_splits, cdiv(a.target_ctas, max_rows * a.Hkv)));
     args.max_splits = std::max(want, cdiv(a.max_ctx, kMaxChunkPages * kPage));
     dim3 grid(args.max_splits, a.Hkv, max_rows);
-    launch_k(attn_decode_kernel<HD, G, KB>, grid, dim3(128), smem, st, q, kv_layer, out, args);
+    launch_k(attn_decode_kernel<HD, G, KB, NS>, grid, dim3(128), smem, st, q, kv_layer, out, args);
+}
+
+template <int HD, int G>
+void decode_launch(const __nv_bfloat16* q, const __nv_bfloat16* kv_layer, __nv_bfloat16* out, const DecodeAttnArgs& a,
+                   int max_rows, cudaStream_t st) {
+    static const int ns = [] {
+        const char* v = std::getenv("SW_ATTN_STAGES");  // measured: 3 (profiles/r01b/step_ablation.txt)
+        return v && *v ? std::atoi(v) : 3;
+    }();
+    if (ns == 3) decode_launch_ns<HD, G, 3>(q, kv_layer, out, a, max_rows, st);
+    else if (ns == 4) decode_launch_ns<HD, G, 4>(q, kv_layer, out, a, max_rows, st);
+    else decode_launch_ns<HD, G, 2>(q, kv_layer, out, a, max_rows, st);
 }
 
 }  // namespace

@@ -60,10 +60,10 @@ template <int HD>
 constexpr int decode_kb() {
     return HD <= 64 ? 32 : 16;
 }
-// dynamic smem of one unit runner (4 warps): K/V double buffers + warp-merge scratch
-template <int HD, int G>
+// dynamic smem of one unit runner (4 warps): per-warp NS-stage K/V rings + warp-merge scratch
+template <int HD, int G, int NS = 2>
 constexpr int decode_unit_smem() {
-    return 4 * (4 * decode_kb<HD>() * HD) * 2 + (8 * G + 4 * G * HD) * 4;
+    return 4 * (2 * NS * decode_kb<HD>() * HD) * 2 + (8 * G + 4 * G * HD) * 4;
 }
 
 // Split plan of one row: how many units its context is cut into and the keys
@@ -82,7 +82,7 @@ __device__ __forceinline__ SplitPlan decode_split_plan(int ctx, int want, int ca
 // One unit.  `tid` in [0, 128); `sync()` synchronises exactly the 128
 // threads running the unit.  smem: dsm (decode_unit_smem bytes), s_pages
 // (kMaxChunkPages ints), s_last (one word).
-template <int HD, int G, int KB, class Sync>
+template <int HD, int G, int KB, int NS = 2, class Sync>
 __device__ __forceinline__ void decode_unit(const DecodeAttnArgs& a, const __nv_bfloat16* __restrict__ q,
                                             const __nv_bfloat16* __restrict__ kv_layer,
                                             __nv_bfloat16* __restrict__ out, int row, int hk, int split,
@@ -91,9 +91,9 @@ __device__ __forceinline__ void decode_unit(const DecodeAttnArgs& a, const __nv_
     static_assert(G <= 8, "query rows live in the first 8 mma rows");
     constexpr int CH = HD / 8;
     const int warp = tid >> 5, lane = tid & 31;
-    __nv_bfloat16* wK = reinterpret_cast<__nv_bfloat16*>(dsm) + warp * (4 * KB * HD);  // [2][KB][HD]
-    __nv_bfloat16* wV = wK + 2 * KB * HD;                                               // [2][KB][HD]
-    float* cm = reinterpret_cast<float*>(dsm + 4 * (4 * KB * HD) * 2);  // [4][G]
+    __nv_bfloat16* wK = reinterpret_cast<__nv_bfloat16*>(dsm) + warp * (2 * NS * KB * HD);  // [NS][KB][HD]
+    __nv_bfloat16* wV = wK + NS * KB * HD;                                                  // [NS][KB][HD]
+    float* cm = reinterpret_cast<float*>(dsm + 4 * (2 * NS * KB * HD) * 2);  // [4][G]
     float* cl = cm + 4 * G;                                             // [4][G]
     float* co = cl + 4 * G;                                             // [4][G][HD]
     const int splits = plan.splits;
@@ -152,20 +152,19 @@ __device__ __forceinline__ void decode_unit(const DecodeAttnArgs& a, const __nv_
     float m_run = -INFINITY, l_run = 0.f;  // row r (c0/c1); rows r+8 are padding
 
     sync();  // s_pages
-    int it = 0;
-    if (warp < n_blocks) {
-        load(warp, 0);
+    // warp w streams blocks w, w + 4, ... through an NS-stage ring (NS - 1 in flight while one is computed)
+    const int my_blocks = n_blocks > warp ? (n_blocks - warp + 3) / 4 : 0;
+#pragma unroll
+    for (int i = 0; i < NS - 1; ++i) {
+        if (i < my_blocks) load(warp + 4 * i, i);
         cp_async_commit();
     }
-    for (int blk = warp; blk < n_blocks; blk += 4, ++it) {
-        const int buf = it & 1;
-        if (blk + 4 < n_blocks) {
-            load(blk + 4, buf ^ 1);
-            cp_async_commit();
-            cp_async_wait<1>();
-        } else {
-            cp_async_wait<0>();
-        }
+    for (int it = 0; it < my_blocks; ++it) {
+        const int blk = warp + 4 * it;
+        const int buf = it % NS;
+        if (it + NS - 1 < my_blocks) load(blk + 4 * (NS - 1), (it + NS - 1) % NS);
+        cp_async_commit();
+        cp_async_wait<NS - 1>();
         __syncwarp();
         const __nv_bfloat16* K = wK + buf * KB * HD;
         const __nv_bfloat16* V = wV + buf * KB * HD;
