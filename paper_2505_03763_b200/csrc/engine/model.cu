@@ -106,6 +106,12 @@ void ws_alloc(Workspace& w, const sw_model_desc& d, int rows, bool decode, int m
         const size_t parts = static_cast<size_t>(kMaxDecodeRows) * d.n_kv_heads * max_splits_cap * G;
         w.part_o = dalloc<float>(parts * d.head_dim);
         w.part_ml = dalloc<float>(parts * 2);
+        int dev = 0, sms = 0;
+        SW_CUDA(cudaGetDevice(&dev));
+        SW_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        const size_t flat = attn_decode_flat_part_rows(sms) * G;
+        w.flat_o = dalloc<float>(flat * d.head_dim);
+        w.flat_ml = dalloc<float>(flat * 2);
         w.attn_cnt = dalloc<unsigned>(static_cast<size_t>(kMaxDecodeRows) * d.n_kv_heads);
         SW_CUDA(cudaMemset(w.attn_cnt, 0, static_cast<size_t>(kMaxDecodeRows) * d.n_kv_heads * sizeof(unsigned)));
         w.splitk_floats = static_cast<size_t>(kSplitTiles) * 256 * 128;
@@ -339,7 +345,7 @@ DecodeAttnArgs decode_attn_args(const sw_model* m, const sw_kv* kv, const Worksp
     return aa;
 }
 
-void decode_layers(sw_model* m, sw_kv* kv, int R, cudaStream_t st, int lane) {
+void decode_layers(sw_model* m, sw_kv* kv, int R, cudaStream_t st, int lane, bool use_flat) {
     // One decode step, 5 kernels per layer, chained with programmatic dependent
     // launch (each kernel's weight stream starts while its predecessor drains):
     //   qkv  GEMM . RMSNorm scale . RoPE -> q, K/V straight into the paged cache
@@ -374,6 +380,21 @@ void decode_layers(sw_model* m, sw_kv* kv, int R, cudaStream_t st, int lane) {
         p.fx.ss_part_out = ss_out;
     };
     static const int ablate = env_int("SW_ABLATE", 0);  // timing experiments only: skip kernel classes
+    DecodeFlatArgs fa{};
+    const int flat_ctas = stream_sm_count(st);
+    if (use_flat) {
+        fa.meta = w.meta;
+        fa.page_table = kv->page_table;
+        fa.max_pages = kv->max_pages;
+        fa.H = d.n_heads;
+        fa.Hkv = d.n_kv_heads;
+        fa.scale_log2 = aa.scale_log2;
+        fa.page_rows = static_cast<int>(kv->page_stride / d.head_dim);
+        fa.v_rows = static_cast<int>(kv->page_stride / 2 / d.head_dim);
+        fa.part_o = w.flat_o;
+        fa.part_ml = w.flat_ml;
+        fa.counters = w.attn_cnt;
+    }
     for (int l = 0; l < d.n_layers; ++l) {
         const LayerWeights& L = m->layers[l];
         __nv_bfloat16* kvl = kv->pages + l * kv->layer_stride;
@@ -392,7 +413,14 @@ void decode_layers(sw_model* m, sw_kv* kv, int R, cudaStream_t st, int lane) {
         pq.fx.Hkv = d.n_kv_heads;
         pq.fx.hd = d.head_dim;
         if (!(ablate & 2)) gemm_run(pq, st);
-        if (!(ablate & 1)) attn_decode(w.q, kvl, w.attn, aa, R, d.head_dim, st);
+        if (!(ablate & 1)) {
+            if (use_flat) {
+                fa.layer_row0 = static_cast<int>(l * kv->layer_stride / d.head_dim);
+                attn_decode_flat(kv->tm_kv, w.q, w.attn, fa, flat_ctas, d.head_dim, d.n_heads / d.n_kv_heads, st);
+            } else {
+                attn_decode(w.q, kvl, w.attn, aa, R, d.head_dim, st);
+            }
+        }
         GemmProblem po = gp(w.attn, w.rows, L.wo, d.d_model, R, d.d_model, hdH, EPI_RESID, true, w.x, d.d_model, live, &w);
         resid_out(po, ss_b);
         if (!(ablate & 4)) gemm_run(po, st);
@@ -606,11 +634,24 @@ void decode_forward(sw_model* m, sw_kv* kv, const sw_batch& b, cudaStream_t st, 
     ring_release(m->dec_ring[lane], idx, st);
     const int R = std::min(decode_bucket(b.n), w.rows);
     const StepPlan* plan = decode_mode() == 1 ? step_plan(m, kv, R, lane, lanes) : nullptr;
+    // decode attention kernel: the flat page-balanced one for long contexts, the per-unit
+    // split-KV one below (its independent CTAs flow around concurrent prefill work);
+    // SW_ATTN_FLAT=0/1 forces one (profiles/r01c/attn_flat_sweep.txt)
+    static const int flat_env = env_int("SW_ATTN_FLAT", 2);
+    static const int flat_ctx = env_int("SW_ATTN_FLAT_CTX", 2048);
+    bool flat = false;
+    if (kv->tm_kv_ok && flat_env == 1) {
+        flat = true;
+    } else if (kv->tm_kv_ok && flat_env == 2) {
+        long long ctx = 0;
+        for (int i = 0; i < b.n; ++i) ctx += b.positions[i] + 1;
+        flat = ctx >= static_cast<long long>(flat_ctx) * b.n;
+    }
     auto run = [&](cudaStream_t s) {
         if (plan) decode_step_path(m, kv, R, s, lane, *plan);
-        else decode_layers(m, kv, R, s, lane);
+        else decode_layers(m, kv, R, s, lane, flat);
     };
-    DecodeGraph& g = m->graphs[{kv, R, lane | (plan ? 16 : 0), stream_partition_tag(st)}];
+    DecodeGraph& g = m->graphs[{kv, R, lane | (plan ? 16 : 0) | (flat ? 32 : 0), stream_partition_tag(st)}];
     if (use_graph && g.exec) {
         SW_CUDA(cudaGraphLaunch(g.exec, st));
         count_launches(g.kernels);
@@ -754,7 +795,7 @@ extern "C" int sw_model_destroy(sw_model* m) {
             for (void* p : {(void*)w->x, (void*)w->xn, (void*)w->qkv, (void*)w->q, (void*)w->attn, (void*)w->act,
                             (void*)w->xlast, (void*)w->keys, (void*)w->meta, (void*)w->part_o, (void*)w->part_ml,
                             (void*)w->pmeta, (void*)w->splitk_ws, (void*)w->splitk_cnt, (void*)w->attn_cnt,
-                            (void*)w->ss})
+                            (void*)w->ss, (void*)w->flat_o, (void*)w->flat_ml})
                 if (p) cudaFree(p);
         }
         std::vector<PinnedRing*> rings{&m->pre_ring};
@@ -809,6 +850,16 @@ extern "C" int sw_kv_arena_create(sw_model* m, int64_t n_pages, int32_t n_slots,
         kv->layer_stride = kv->page_stride * n_pages;
         const size_t bytes = static_cast<size_t>(kv->layer_stride) * d.n_layers * 2;
         SW_CUDA(cudaMalloc(&kv->pages, bytes));
+        // rows past a context inside its last page are read (and masked) by the
+        // decode attention: keep them finite
+        SW_CUDA(cudaMemset(kv->pages, 0, bytes));
+        {
+            const uint64_t rows = bytes / (2ull * d.head_dim);
+            if (rows < (1ull << 31) && d.head_dim % 64 == 0) {
+                kv->tm_kv = make_tmap_bf16(kv->pages, rows, d.head_dim, 16);
+                kv->tm_kv_ok = true;
+            }
+        }
         kv->page_table = dalloc<int32_t>(static_cast<size_t>(n_slots) * max_pages_per_slot);
         SW_CUDA(cudaMemset(kv->page_table, 0, static_cast<size_t>(n_slots) * max_pages_per_slot * 4));
         kv->last_token = dalloc<int32_t>(n_slots);

@@ -1,6 +1,7 @@
 // Model + KV arena objects behind the kernel-level C-ABI (sw_model / sw_kv).
 #pragma once
 
+#include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -47,6 +48,9 @@ struct Workspace {
     float* part_o = nullptr;
     float* part_ml = nullptr;
     unsigned* attn_cnt = nullptr;  // split-KV arrival counters [rows][Hkv]
+    // flat decode attention: per-warp partials
+    float* flat_o = nullptr;
+    float* flat_ml = nullptr;
     // prefill only: device metadata block
     int32_t* pmeta = nullptr;
     size_t pmeta_bytes = 0;
@@ -119,6 +123,9 @@ struct sw_kv {
     int64_t page_stride = 0;         // elements per page (one layer)
     int chunk = 256;
     int max_splits = 1;
+    // the whole arena as one 2-D TMA map of head_dim-element rows (flat decode attention)
+    CUtensorMap tm_kv{};
+    bool tm_kv_ok = false;
 };
 
 namespace sw {

@@ -1,6 +1,7 @@
 // Host-facing interface of the attention kernels (attention.cu).
 #pragma once
 
+#include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -43,9 +44,31 @@ struct DecodeAttnArgs {
     int max_ctx;         // longest context the arena holds (sizes the grid)
 };
 
+// Flat page-balanced decode attention (attn_decode_flat.cu): persistent grid,
+// TMA page-slice loads through a 2-D map of the whole KV arena (rows of hd
+// elements; K slice of (layer l, page p, kv head h) at row
+// layer_row0 + p * page_rows + h * 16, its V slice v_rows further).
+struct DecodeFlatArgs {
+    const StepMeta* meta;
+    const int32_t* page_table;
+    int max_pages;
+    int H, Hkv;
+    float scale_log2;
+    int layer_row0;
+    int page_rows;
+    int v_rows;
+    float* part_o;       // [2 * warps][G][hd]
+    float* part_ml;      // [2 * warps][G][2]
+    unsigned* counters;  // [rows][Hkv], zero between launches
+};
+// partial slots (each G x hd floats) the flat kernel needs on `sms` SMs
+size_t attn_decode_flat_part_rows(int sms);
+
 void attn_prefill(const __nv_bfloat16* q, const __nv_bfloat16* kv_layer, __nv_bfloat16* out, const PrefillAttnArgs& a,
                   int max_tiles, int hd, cudaStream_t st);
 void attn_decode(const __nv_bfloat16* q, const __nv_bfloat16* kv_layer, __nv_bfloat16* out, const DecodeAttnArgs& a,
                  int max_rows, int hd, cudaStream_t st);
+void attn_decode_flat(const CUtensorMap& tm_kv, const __nv_bfloat16* q, __nv_bfloat16* out, const DecodeFlatArgs& a,
+                      int ctas, int hd, int G, cudaStream_t st);
 
 }  // namespace sw
