@@ -312,16 +312,6 @@ int env_int(const char* name, int dflt) {
     return v && *v ? std::atoi(v) : dflt;
 }
 
-int device_sms() {
-    static const int n = [] {
-        int dev = 0, v = 0;
-        SW_CUDA(cudaGetDevice(&dev));
-        SW_CUDA(cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev));
-        return v;
-    }();
-    return n;
-}
-
 DecodeAttnArgs decode_attn_args(const sw_model* m, const sw_kv* kv, const Workspace& w) {
     const sw_model_desc& d = m->desc;
     DecodeAttnArgs aa{};
@@ -441,169 +431,6 @@ void decode_layers(sw_model* m, sw_kv* kv, int R, cudaStream_t st, int lane, boo
 }
 
 
-// ---- persistent decode-step kernel (decode_step.cu): one launch per step
-int decode_mode() {
-    // 1: persistent step kernel, 0: one kernel per projection (default until the step kernel is faster)
-    return env_int("SW_DECODE_STEP", 0);
-}
-
-StepPlan* step_plan(sw_model* m, sw_kv* kv, int R, int lane, int lanes) {
-    const sw_model_desc& d = m->desc;
-    const int bn = R <= 32 ? 32 : R <= 64 ? 64 : R <= 128 ? 128 : 256;
-    const int G = d.n_heads / d.n_kv_heads;
-    if (!decode_step_supported(bn, d.head_dim, G)) return nullptr;
-    auto key = std::make_tuple(static_cast<const sw_kv*>(kv), R, lane);
-    auto it = m->step_plans.find(key);
-    if (it != m->step_plans.end()) return &it->second;
-    Workspace& w = m->dec[lane];
-    const int sms = device_sms();
-    const int ctas = std::max(1, std::min(sms, env_int("SW_STEP_CTAS", sms / std::max(1, lanes))));
-    if (static_cast<size_t>(ctas) * 2 * bn * 128 > w.splitk_floats) return nullptr;
-    const int qkv_w = (d.n_heads + 2 * d.n_kv_heads) * d.head_dim;
-    const int hdH = d.n_heads * d.head_dim;
-    const int parts = d.d_model / 128;
-    float* ss_a = w.ss;
-    float* ss_b = w.ss + kSsParts * kSsStride;
-    __nv_bfloat16* xb = w.xn;
-
-    std::vector<CUtensorMap> maps;
-    auto map = [&](const void* base, int64_t rows, int64_t cols, int box) {
-        maps.push_back(make_tmap_bf16(base, rows, cols, box));
-        return static_cast<int>(maps.size()) - 1;
-    };
-    const int x_xb = map(xb, w.rows, d.d_model, bn);
-    const int x_attn = map(w.attn, w.rows, hdH, bn);
-    const int x_act = map(w.act, w.rows, d.ffn_dim, bn);
-    std::vector<StepPhase> ph;
-    auto gemm = [&](int mode, int wmap, int xmap, int M, int K, void* out, int ldo) {
-        StepPhase p{};
-        p.kind = PHASE_GEMM;
-        p.mode = mode;
-        p.w_map = wmap;
-        p.x_map = xmap;
-        p.M = M;
-        p.K = K;
-        p.g.mode = mode;
-        p.g.out = out;
-        p.g.ldo = ldo;
-        p.g.valid_tokens = R;
-        p.g.live_tokens = &w.meta->n;
-        return p;
-    };
-    auto norm_in = [&](StepPhase& p, const float* ss, int nparts) {
-        p.g.fx.ss_parts = ss;
-        p.g.fx.ss_nparts = nparts;
-        p.g.fx.norm_dim = d.d_model;
-        p.g.fx.norm_eps = d.norm_eps;
-    };
-    for (int l = 0; l < d.n_layers; ++l) {
-        const LayerWeights& L = m->layers[l];
-        __nv_bfloat16* kvl = kv->pages + l * kv->layer_stride;
-        StepPhase q = gemm(EPI_QKV_ROPE, map(L.wqkv, qkv_w, d.d_model, 128), x_xb, qkv_w, d.d_model, nullptr, qkv_w);
-        norm_in(q, ss_a, l == 0 ? 1 : parts);
-        q.g.fx.pos = w.meta->pos;
-        q.g.fx.slot = w.meta->slot;
-        q.g.fx.page_table = kv->page_table;
-        q.g.fx.max_pages = kv->max_pages;
-        q.g.fx.page_tokens = kv->page_tokens;
-        q.g.fx.rope_cs = m->rope_cs;
-        q.g.fx.q_out = w.q;
-        q.g.fx.kv_layer = kvl;
-        q.g.fx.page_stride = kv->page_stride;
-        q.g.fx.H = d.n_heads;
-        q.g.fx.Hkv = d.n_kv_heads;
-        q.g.fx.hd = d.head_dim;
-        ph.push_back(q);
-        StepPhase a{};
-        a.kind = PHASE_ATTN;
-        a.q = w.q;
-        a.kv = kvl;
-        a.out = w.attn;
-        ph.push_back(a);
-        StepPhase o = gemm(EPI_RESID, map(L.wo, d.d_model, hdH, 128), x_attn, d.d_model, hdH, w.x, d.d_model);
-        o.g.fx.x_bf16 = xb;
-        o.g.fx.ss_part_out = ss_b;
-        ph.push_back(o);
-        StepPhase g = gemm(EPI_SWIGLU, map(L.wgu, 2 * d.ffn_dim, d.d_model, 128), x_xb, 2 * d.ffn_dim, d.d_model, w.act,
-                           d.ffn_dim);
-        norm_in(g, ss_b, parts);
-        ph.push_back(g);
-        StepPhase dn = gemm(EPI_RESID, map(L.wd, d.d_model, d.ffn_dim, 128), x_act, d.d_model, d.ffn_dim, w.x, d.d_model);
-        dn.g.fx.x_bf16 = xb;
-        dn.g.fx.ss_part_out = ss_a;
-        ph.push_back(dn);
-    }
-    StepPhase lm = gemm(EPI_ARGMAX, map(m->lm, d.vocab, d.d_model, 128), x_xb, d.vocab, d.d_model, nullptr, 0);
-    lm.g.argmax = w.keys;
-    norm_in(lm, ss_a, parts);  // argmax is scale invariant; kept so logits and argmax see one definition
-    ph.push_back(lm);
-
-    StepPlan P;
-    P.n_phases = static_cast<int>(ph.size());
-    for (StepPhase& p : ph) {
-        if (p.kind != PHASE_GEMM) continue;
-        p.cnt_off = P.n_counters;
-        P.n_counters += p.M / 128;
-    }
-    P.bn = bn;
-    P.ctas = ctas;
-    SW_CUDA(cudaMalloc(&P.d_phases, ph.size() * sizeof(StepPhase)));
-    SW_CUDA(cudaMemcpy(P.d_phases, ph.data(), ph.size() * sizeof(StepPhase), cudaMemcpyHostToDevice));
-    SW_CUDA(cudaMalloc(&P.d_maps, maps.size() * sizeof(CUtensorMap)));  // 256 B aligned
-    SW_CUDA(cudaMemcpy(P.d_maps, maps.data(), maps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice));
-    const size_t words = static_cast<size_t>(P.n_phases) + P.n_counters;
-    SW_CUDA(cudaMalloc(&P.d_bar, words * sizeof(unsigned)));
-    SW_CUDA(cudaMemset(P.d_bar, 0, words * sizeof(unsigned)));
-    P.args.phases = P.d_phases;
-    P.args.n_phases = P.n_phases;
-    P.args.maps = P.d_maps;
-    P.args.bar = P.d_bar;
-    P.args.ws = w.splitk_ws;
-    P.args.counters = P.d_bar + P.n_phases;
-    P.args.meta = w.meta;
-    P.args.attn = decode_attn_args(m, kv, w);
-    P.args.attn_target = env_int("SW_STEP_ATTN_UNITS", 4 * ctas);
-    P.args.debug_single_reducer = env_int("SW_STEP_SINGLE_REDUCER", 0);
-    return &m->step_plans.emplace(key, P).first->second;
-}
-
-void step_plan_free(StepPlan& P) {
-    cudaFree(P.d_phases);
-    cudaFree(P.d_maps);
-    cudaFree(P.d_bar);
-}
-
-void decode_step_path(sw_model* m, sw_kv* kv, int R, cudaStream_t st, int lane, const StepPlan& P) {
-    const sw_model_desc& d = m->desc;
-    Workspace& w = m->dec[lane];
-    SW_CUDA(cudaMemsetAsync(P.d_bar, 0, (static_cast<size_t>(P.n_phases) + P.n_counters) * sizeof(unsigned), st));
-    embed(w.meta, R, m->emb, w.x, w.xn, w.ss, d.d_model, kv->last_token, kv->page_table, kv->max_pages,
-          kv->page_tokens, st);
-    static const char* trace_path = std::getenv("SW_STEP_TRACE");  // eager steps only: dump phase stamps
-    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-    SW_CUDA(cudaStreamIsCapturing(st, &cap));
-    if (trace_path && *trace_path && cap == cudaStreamCaptureStatusNone) {
-        const size_t n = static_cast<size_t>(P.n_phases) * P.ctas * 8;
-        StepArgs a = P.args;
-        SW_CUDA(cudaMalloc(&a.trace, n * 8));
-        SW_CUDA(cudaMemsetAsync(a.trace, 0, n * 8, st));
-        decode_step_launch(a, P.bn, d.head_dim, d.n_heads / d.n_kv_heads, P.ctas, st);
-        std::vector<unsigned long long> h(n);
-        SW_CUDA(cudaMemcpyAsync(h.data(), a.trace, n * 8, cudaMemcpyDeviceToHost, st));
-        SW_CUDA(cudaStreamSynchronize(st));
-        SW_CUDA(cudaFree(a.trace));
-        if (FILE* f = std::fopen(trace_path, "ab")) {
-            const int hdr[3] = {P.n_phases, P.ctas, R};
-            std::fwrite(hdr, sizeof(hdr), 1, f);
-            std::fwrite(h.data(), 8, n, f);
-            std::fclose(f);
-        }
-    } else {
-        decode_step_launch(P.args, P.bn, d.head_dim, d.n_heads / d.n_kv_heads, P.ctas, st);
-    }
-    finalize_tokens(w.keys, w.meta->slot, w.meta->out_index, R, &w.meta->n, kv->last_token, kv->out_tokens,
-                    kv->max_out, st);
-}
 }  // namespace
 
 void decode_forward(sw_model* m, sw_kv* kv, const sw_batch& b, cudaStream_t st, bool use_graph, int lane, int lanes) {
@@ -633,7 +460,6 @@ void decode_forward(sw_model* m, sw_kv* kv, const sw_batch& b, cudaStream_t st, 
     count_transfer(bytes, 0);
     ring_release(m->dec_ring[lane], idx, st);
     const int R = std::min(decode_bucket(b.n), w.rows);
-    const StepPlan* plan = decode_mode() == 1 ? step_plan(m, kv, R, lane, lanes) : nullptr;
     // decode attention kernel: the flat page-balanced one for long contexts, the per-unit
     // split-KV one below (its independent CTAs flow around concurrent prefill work);
     // SW_ATTN_FLAT=0/1 forces one (profiles/r01c/attn_flat_sweep.txt)
@@ -648,10 +474,9 @@ void decode_forward(sw_model* m, sw_kv* kv, const sw_batch& b, cudaStream_t st, 
         flat = ctx >= static_cast<long long>(flat_ctx) * b.n;
     }
     auto run = [&](cudaStream_t s) {
-        if (plan) decode_step_path(m, kv, R, s, lane, *plan);
-        else decode_layers(m, kv, R, s, lane, flat);
+        decode_layers(m, kv, R, s, lane, flat);
     };
-    DecodeGraph& g = m->graphs[{kv, R, lane | (plan ? 16 : 0) | (flat ? 32 : 0), stream_partition_tag(st)}];
+    DecodeGraph& g = m->graphs[{kv, R, lane | (flat ? 32 : 0), stream_partition_tag(st)}];
     if (use_graph && g.exec) {
         SW_CUDA(cudaGraphLaunch(g.exec, st));
         count_launches(g.kernels);
@@ -788,7 +613,6 @@ extern "C" int sw_model_destroy(sw_model* m) {
         cudaDeviceSynchronize();
         for (auto& [k, g] : m->graphs)
             if (g.exec) cudaGraphExecDestroy(g.exec);
-        for (auto& [k, p] : m->step_plans) step_plan_free(p);
         std::vector<Workspace*> all{&m->pre};
         for (auto& w : m->dec) all.push_back(&w);
         for (Workspace* w : all) {
@@ -881,14 +705,6 @@ extern "C" int sw_kv_arena_destroy(sw_kv* kv) {
             if (std::get<0>(it->first) == kv) {
                 if (it->second.exec) cudaGraphExecDestroy(it->second.exec);
                 it = kv->model->graphs.erase(it);
-            } else {
-                ++it;
-            }
-        }
-        for (auto it = kv->model->step_plans.begin(); it != kv->model->step_plans.end();) {
-            if (std::get<0>(it->first) == kv) {
-                step_plan_free(it->second);
-                it = kv->model->step_plans.erase(it);
             } else {
                 ++it;
             }

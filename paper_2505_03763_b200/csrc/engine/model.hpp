@@ -13,7 +13,6 @@
 
 #include "../../../include/splitwise.h"
 #include "../kernels/attention.cuh"
-#include "../kernels/decode_step.cuh"
 #include "../kernels/elementwise.cuh"
 
 namespace sw {
@@ -63,21 +62,6 @@ struct PinnedRing {
     int next = 0;
 };
 
-// Device-resident phase list of the persistent decode-step kernel for one
-// (arena, row bucket, lane): tensor maps of every weight matrix and of the
-// lane's activation buffers, the per-phase epilogue arguments, and the grid
-// barrier counters.
-struct StepPlan {
-    StepPhase* d_phases = nullptr;
-    CUtensorMap* d_maps = nullptr;
-    unsigned* d_bar = nullptr;  // [n_phases] barrier arrivals + [n_counters] split-K tile counters
-    int n_phases = 0;
-    int n_counters = 0;
-    int bn = 0;
-    int ctas = 0;
-    StepArgs args{};
-};
-
 struct DecodeGraph {
     cudaGraphExec_t exec = nullptr;
     int eager_runs = 0;
@@ -106,7 +90,6 @@ struct sw_model {
     sw::PinnedRing pre_ring, dec_ring[kMaxDecodeLanes];
     // (arena, row bucket, lane | mode, partition): a graph runs in the context it was captured in
     std::map<std::tuple<const sw_kv*, int, int, const void*>, sw::DecodeGraph> graphs;
-    std::map<std::tuple<const sw_kv*, int, int>, sw::StepPlan> step_plans;  // (arena, row bucket, lane)
     unsigned long long* scratch_u64 = nullptr;
 };
 

@@ -1,5 +1,7 @@
-// Decode attention work unit shared by the standalone split-KV kernel
-// (attention.cu) and the persistent decode-step kernel (decode_step.cu).
+// Decode attention work unit of the per-unit split-KV kernel (attention.cu).
+// (A persistent whole-step kernel also ran this unit; measured 2.8x slower than
+// the per-projection kernels, profiles/r01c/step_check_persistent_vs_kernels.txt,
+// and removed.)
 //
 // One unit = (row, kv head, split of the context), run by 128 threads (4
 // warps).  The warps stream disjoint KB-key blocks of the split (warp w takes
