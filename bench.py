@@ -47,6 +47,13 @@ WORKLOADS = {
                        split="policy=mixed_batching;max_batch=128;engine.split=1",  # prefill || decode, one instance
                        serial="policy=mixed_batching;max_batch=128;engine.split=0",
                        best_serial="policy=continuous_batching;max_batch=128;engine.split=0"),
+    # configs[4]: 8B long-context decode-heavy, prompt 8192 / gen 512, the KV arena near HBM capacity
+    # (112 requests x 544 pages x 2 MiB = 128 GB of KV next to 16 GB of weights); AllAtZero
+    "8b-long": dict(model="LLAMA_8B", n=112, input=8192, output=512, arrival="zero", max_prefill=32768,
+                    max_decode=112,
+                    split="policy=mixed_batching;max_batch=112;engine.split=1",
+                    serial="policy=continuous_batching;max_batch=112;engine.split=0",
+                    best_serial="policy=sequential;max_batch=112;engine.split=0"),
     # configs[0] shape on the GPU (fast sanity run)
     "tiny": dict(model="TINY", n=8, input=64, output=32, arrival="zero", max_prefill=1024, max_decode=16,
                  split="policy=pipelined_splitwiser;P=2;max_batch=4;engine.split=1",
