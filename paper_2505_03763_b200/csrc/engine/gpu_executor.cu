@@ -46,6 +46,7 @@ struct GpuOptions {
     int decode_lanes = 1;     // split mode: concurrent decode streams (instance i -> lane i % lanes)
     int decode_sms = 0;       // split mode: > 0 partitions the SMs with green contexts (decode | prefill)
     bool lean_prefill = false;  // split mode: prompts launched while decode work exists use co-resident GEMM tiles
+    int prefill_yield = 0;      // split mode: prompts launched while decode work exists cap GEMM tiles per CTA
     bool coalesce = true;     // one launch per kind per pass
     bool align = true;        // split mode: a token step requested while another is in flight waits for it and
                               // then runs merged with every other waiting step (one weight pass for all lanes)
@@ -99,10 +100,17 @@ public:
             s_decode_ = P.decode;
             part_ = &P;
             own_streams_ = false;
-            // prompts launched while no request is generating take the whole GPU
+            // prompts launched while no request is generating take the whole GPU, and so do
+            // token steps launched while no prompt is in flight (the partition only pays
+            // while both phases run: profiles/r01c/overlap_1b.txt)
             int lo, hi;
             SW_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
             SW_CUDA(cudaStreamCreateWithPriority(&s_prefill_full_, cudaStreamNonBlocking, lo));
+            for (int i = 0; i < lanes; ++i) {
+                cudaStream_t sf;
+                SW_CUDA(cudaStreamCreateWithPriority(&sf, cudaStreamNonBlocking, hi));
+                s_decode_full_.push_back(sf);
+            }
             return;
         }
         int lo, hi;
@@ -122,6 +130,10 @@ public:
         if (s_prefill_full_) {
             cudaStreamSynchronize(s_prefill_full_);
             cudaStreamDestroy(s_prefill_full_);
+        }
+        for (cudaStream_t s : s_decode_full_) {
+            cudaStreamSynchronize(s);
+            cudaStreamDestroy(s);
         }
         if (!own_streams_) return;
         for (cudaStream_t s : s_decode_)
@@ -228,13 +240,13 @@ public:
                 s += (j ? "|" : "") + std::to_string(table[static_cast<size_t>(slot) * kv_->max_pages + j]);
             s += "\n";
         }
-        char buf[320];
+        char buf[512];
         std::snprintf(buf, sizeof buf,
                       "#gpu launches=%zu;prefill_launches=%d;decode_launches=%d;split=%d;coalesce=%d;align=%d;decode_lanes=%zu;"
-                      "decode_sms=%d;prefill_sms=%d;prefill_full_gpu=%d;prefill_lean=%d;clock_skew_s=%.9g\n",
+                      "decode_sms=%d;prefill_sms=%d;prefill_full_gpu=%d;decode_full_gpu=%d;prefill_lean=%d;prefill_yield=%d;clock_skew_s=%.9g\n",
                       launches_.size(), n_prefill_, n_decode_, opt_.split ? 1 : 0, opt_.coalesce ? 1 : 0,
                       aligning() ? 1 : 0, s_decode_.size(), part_ ? part_->decode_sms : 0, part_ ? part_->prefill_sms : 0, n_prefill_full_,
-                      n_prefill_lean_, clock_skew_);
+                      n_decode_full_, n_prefill_lean_, n_prefill_yield_, clock_skew_);
         s += buf;
         return s;
     }
@@ -343,6 +355,11 @@ private:
                            [](const Entry& e) { return e.req.state == RequestState::Generating; });
     }
 
+    bool prompt_inflight() const {
+        return std::any_of(launches_.begin(), launches_.end(),
+                           [](const Launch& l) { return !l.done && l.kind == TaskKind::Prompt; });
+    }
+
     bool decode_inflight() const {
         return std::any_of(launches_.begin(), launches_.end(),
                            [](const Launch& l) { return !l.done && l.kind == TaskKind::TokenStep; });
@@ -402,7 +419,9 @@ private:
             const bool lean = opt_.split && opt_.lean_prefill && active;
             n_prefill_lean_ += lean ? 1 : 0;
             SW_CUDA(cudaEventRecord(events_[L.start_ev], ps));
-            prefill_forward(m_, kv_, b, ps, lean);
+            const int yield = opt_.split && active ? opt_.prefill_yield : 0;
+            n_prefill_yield_ += yield > 0 ? 1 : 0;
+            prefill_forward(m_, kv_, b, ps, lean, yield);
             SW_CUDA(cudaEventRecord(events_[L.end_ev], ps));
             ++n_prefill_;
         } else {
@@ -419,6 +438,10 @@ private:
             b.new_page = newp.data();
             b.out_index = oidx.data();
             cudaStream_t ds = s_decode_[static_cast<std::size_t>(L.lane)];
+            if (!s_decode_full_.empty() && !prompt_inflight()) {  // partition mode, decode alone: whole GPU
+                ds = s_decode_full_[static_cast<std::size_t>(L.lane)];
+                ++n_decode_full_;
+            }
             SW_CUDA(cudaEventRecord(events_[L.start_ev], ds));
             for (const auto& [se, ee] : L.merged_evs) SW_CUDA(cudaEventRecord(events_[se], ds));
             decode_forward(m_, kv_, b, ds, opt_.graphs, L.lane, static_cast<int>(s_decode_.size()));
@@ -436,8 +459,11 @@ private:
     std::vector<cudaStream_t> s_decode_;
     const SmPartition* part_ = nullptr;  // green-context partition (split mode, engine.decode_sms > 0)
     cudaStream_t s_prefill_full_ = nullptr;  // partition mode: whole-GPU prefill stream
+    std::vector<cudaStream_t> s_decode_full_;  // partition mode: whole-GPU decode streams (per lane)
+    int n_decode_full_ = 0;
     int n_prefill_full_ = 0;
     int n_prefill_lean_ = 0;
+    int n_prefill_yield_ = 0;
     bool own_streams_ = true;
     std::vector<cudaEvent_t> events_;
     int t0_ = -1;
@@ -466,6 +492,7 @@ extern "C" int sw_engine_run(sw_model* m, sw_kv* kv, const char* spec, char** ou
             else if (k == "engine.decode_lanes") opt.decode_lanes = std::stoi(v);
             else if (k == "engine.decode_sms") opt.decode_sms = std::stoi(v);
             else if (k == "engine.lean_prefill") opt.lean_prefill = v == "1" || v == "true";
+            else if (k == "engine.prefill_yield") opt.prefill_yield = std::stoi(v);
             else if (k == "engine.peak_flops") opt.peak_flops = std::stod(v);
             else if (k == "engine.peak_bytes") opt.peak_bytes = std::stod(v);
             else throw ConfigError("spec: unknown key '" + k + "'");

@@ -183,10 +183,11 @@ int decode_bucket(int n) {
 }
 
 // ------------------------------------------------------------------ prefill
-void prefill_forward(sw_model* m, sw_kv* kv, const sw_batch& b, cudaStream_t st, bool lean) {
+void prefill_forward(sw_model* m, sw_kv* kv, const sw_batch& b, cudaStream_t st, bool lean, int yield_tiles) {
     const sw_model_desc& d = m->desc;
-    auto lp = [lean](GemmProblem p) {
+    auto lp = [lean, yield_tiles](GemmProblem p) {
         p.lean = lean;
+        p.yield_tiles = yield_tiles;
         return p;
     };
     Workspace& w = m->pre;

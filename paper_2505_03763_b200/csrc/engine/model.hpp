@@ -115,7 +115,9 @@ namespace sw {
 constexpr int kMaxPositions = 32768;  // RoPE table extent (max context)
 // Forward passes (stream-ordered; host arrays staged internally).
 // lean: 128-wide prefill GEMM tiles in ~105 KB smem, so decode CTAs can share the SMs
-void prefill_forward(sw_model* m, sw_kv* kv, const sw_batch& b, cudaStream_t st, bool lean = false);
+// yield_tiles: > 0 caps the tiles per GEMM CTA (decode CTAs interleave at tile granularity)
+void prefill_forward(sw_model* m, sw_kv* kv, const sw_batch& b, cudaStream_t st, bool lean = false,
+                     int yield_tiles = 0);
 void decode_forward(sw_model* m, sw_kv* kv, const sw_batch& b, cudaStream_t st, bool use_graph, int lane = 0,
                     int lanes = 1);
 int decode_bucket(int n);

@@ -662,7 +662,8 @@ void gemm_run(const GemmProblem& p, cudaStream_t st) {
         a.N = p.features;
         a.stream_k = 0;
         const int tiles = cdiv(p.tokens, BM) * (p.features / bn);
-        const int ctas = std::min(grid_sms, tiles);
+        int ctas = std::min(grid_sms, tiles);
+        if (p.yield_tiles > 0) ctas = std::max(ctas, cdiv(tiles, p.yield_tiles));  // round robin over more CTAs
         const CUtensorMap& ta = tmap_cached(p.X, p.x_rows, p.K, BM);
         const CUtensorMap& tb = tmap_cached(p.W, p.w_rows, p.K, bn);
         switch (p.mode) {

@@ -82,6 +82,8 @@ struct GemmProblem {
     int n_counters = 0;
     DecodeFusion fx;  // swap-mode epilogue fusions
     bool lean = false;  // normal mode: 128-wide tiles in ~105 KB smem (co-resident with decode CTAs)
+    int yield_tiles = 0;  // normal mode: > 0 caps the tiles per CTA (grid = tiles / k): CTAs retire
+                          // every ~k tiles, so higher-priority decode CTAs get SMs between them
 };
 
 CUtensorMap make_tmap_bf16(const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows);
