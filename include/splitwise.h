@@ -95,6 +95,13 @@ void sw_transfer_bytes(unsigned long long* h2d, unsigned long long* d2h);
  * text: the event-log CSV, then `#report k=v;...`, then `#pages` lines. */
 int sw_sim_run(const char* spec, char** out);
 int sw_engine_run(sw_model* model, sw_kv* kv, const char* spec, char** out);
+/* Spec keys `output_dir=<dir>;emit_event_log=1` make both runs write the
+ * reference's experiment files there (splitsim/experiment.hpp:194-212
+ * write_experiment: report.json, requests.csv, timeseries.csv, events.csv).
+ * sw_replay: rebuild the report of a written events.csv, write
+ * replay_report.json next to it (experiment.hpp:290-296 replay_file +
+ * tools/splitsim.cpp:73-85), *out = the `#report` text. */
+int sw_replay(const char* events_path, char** out);
 
 /* ---- kernel level ---- */
 int sw_model_create(const sw_model_desc* desc, int device, sw_model** out);

@@ -10,6 +10,12 @@
 // nearest_rank (metrics.hpp:79-85) over its per-request records.
 //
 // Usage: refsim '<spec>'     (exit 2 config error, 4 contract violation)
+//
+// Built a second time as refwrite (-DREF_EXPERIMENT, needs nlohmann/json for
+// splitsim/experiment.hpp): `refwrite --write DIR '<spec>'` also writes the
+// reference's experiment files (write_experiment, experiment.hpp:194-212, with
+// the event log); `refwrite --replay events.csv` writes replay_report.json as
+// the reference CLI's replay does (tools/splitsim.cpp:73-85).
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -22,6 +28,9 @@
 #include "splitsim/event_log.hpp"
 #include "splitsim/metrics.hpp"
 #include "splitsim/schedulers.hpp"
+#ifdef REF_EXPERIMENT
+#include "splitsim/experiment.hpp"
+#endif
 
 using namespace splitsim;
 
@@ -79,6 +88,26 @@ int main(int argc, char** argv) {
         for (int i = 0, n = std::stoi(argv[3]); i < n; ++i) std::printf("%llu\n", (unsigned long long)rng.next_u64());
         return 0;
     }
+    std::string write_dir;
+#ifdef REF_EXPERIMENT
+    if (argc == 3 && std::string(argv[1]) == "--replay") {
+        try {
+            MetricsReport rep = replay_file(argv[2]);
+            std::filesystem::path dir = std::filesystem::path(argv[2]).parent_path();
+            if (dir.empty()) dir = ".";
+            write_file_atomic(dir / "replay_report.json", report_to_json(rep).dump(2) + "\n");
+            return 0;
+        } catch (const std::exception& e) {
+            std::fprintf(stderr, "error: %s\n", e.what());
+            return 3;
+        }
+    }
+    if (argc == 4 && std::string(argv[1]) == "--write") {
+        write_dir = argv[2];
+        argv[1] = argv[3];
+        argc = 2;
+    }
+#endif
     if (argc != 2) {
         std::fprintf(stderr, "usage: refsim '<spec>'\n");
         return 2;
@@ -144,6 +173,14 @@ int main(int argc, char** argv) {
         PolicyScheduler sched(in.requests, sc, in.cost.kv_handoff_s);
         EventLog log = run_simulation(in, sched);
         MetricsReport r = build_report(log);
+#ifdef REF_EXPERIMENT
+        if (!write_dir.empty()) {
+            ExperimentConfig cfg;
+            cfg.output_dir = write_dir;
+            cfg.emit_event_log = true;
+            write_experiment(cfg, RunResult{log, r});
+        }
+#endif
         std::vector<double> ttft, tbt;
         for (auto& q : r.requests) {
             ttft.push_back(q.ttft_s);

@@ -95,6 +95,7 @@ def lib() -> ctypes.CDLL:
         L.sw_transfer_bytes.restype = None
         for name, args in {
             "sw_engine_run": [c_void_p, c_void_p, c_char_p, ctypes.POINTER(c_void_p)],
+            "sw_replay": [c_char_p, ctypes.POINTER(c_void_p)],
             "sw_model_create": [ctypes.POINTER(ModelDesc), c_int, ctypes.POINTER(c_void_p)],
             "sw_model_destroy": [c_void_p],
             "sw_model_weight_checksum": [c_void_p, ctypes.POINTER(ctypes.c_uint64)],
@@ -120,7 +121,7 @@ def lib() -> ctypes.CDLL:
 
 
 EXPORTED_SYMBOLS = [
-    "sw_last_error", "sw_free", "sw_launch_count", "sw_transfer_bytes", "sw_sim_run", "sw_engine_run", "sw_model_create", "sw_model_destroy",
+    "sw_last_error", "sw_free", "sw_launch_count", "sw_transfer_bytes", "sw_sim_run", "sw_engine_run", "sw_replay", "sw_model_create", "sw_model_destroy",
     "sw_model_weight_checksum", "sw_model_tensor", "sw_kv_arena_create", "sw_kv_arena_destroy",
     "sw_kv_arena_views", "sw_prefill_enqueue", "sw_decode_enqueue", "sw_op_gemm", "sw_op_rmsnorm",
 ]
@@ -196,6 +197,13 @@ def sim_run(spec) -> RunResult:
     s = spec if isinstance(spec, str) else spec_string(spec)
     out = ctypes.c_void_p()
     check(lib().sw_sim_run(s.encode(), ctypes.byref(out)))
+    return parse_run_text(_take_text(out))
+
+
+def replay(events_path: str) -> RunResult:
+    """Rebuild the report of a written events.csv (writes replay_report.json next to it)."""
+    out = ctypes.c_void_p()
+    check(lib().sw_replay(str(events_path).encode(), ctypes.byref(out)))
     return parse_run_text(_take_text(out))
 
 

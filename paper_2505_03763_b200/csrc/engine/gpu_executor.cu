@@ -37,6 +37,7 @@
 #include "../host/spec.hpp"
 #include "../kernels/common.cuh"
 #include "model.hpp"
+#include "../host/experiment_files.hpp"
 #include "partition.hpp"
 
 namespace sw {
@@ -511,7 +512,9 @@ extern "C" int sw_engine_run(sw_model* m, sw_kv* kv, const char* spec, char** ou
         const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - w0).count();
         std::string text = serialize_event_log(log);
         try {
-            text += render_report(build_report(log));
+            const MetricsReport rep = build_report(log);
+            text += render_report(rep);
+            if (!rs.output_dir.empty()) write_experiment(rs.output_dir, rs.emit_event_log, log, rep);
         } catch (const ContractViolation& e) {
             g_last_error = std::string("ContractViolation: ") + e.what();
             text += std::string("#report_error ") + e.what() + "\n";

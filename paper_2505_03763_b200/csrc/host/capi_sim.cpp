@@ -6,6 +6,7 @@
 #include "../../../include/splitwise.h"
 #include "capi_util.hpp"
 #include "executor.hpp"
+#include "experiment_files.hpp"
 #include "report.hpp"
 #include "run_text.hpp"
 #include "spec.hpp"
@@ -33,6 +34,14 @@ extern "C" int sw_sim_run(const char* spec, char** out) {
         sw::VirtualClockExecutor ex(rs.inputs, sched);
         const sw::EventLog log = ex.run();
         const sw::MetricsReport rep = sw::build_report(log);
+        if (!rs.output_dir.empty()) sw::write_experiment(rs.output_dir, rs.emit_event_log, log, rep);
         *out = sw::dup_text(sw::serialize_event_log(log) + sw::render_report(rep) + sw::render_pages(ex.pages()));
+    });
+}
+
+extern "C" int sw_replay(const char* events_path, char** out) {
+    return sw::guarded([&] {
+        if (!events_path || !out) throw sw::ConfigError("sw_replay: null argument");
+        *out = sw::dup_text(sw::render_report(sw::replay_file(events_path)));
     });
 }

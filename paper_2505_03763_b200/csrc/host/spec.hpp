@@ -64,6 +64,8 @@ struct RunSpec {
     long long kv_capacity_override = 0;  // 0 = derive
     int shard_index = 0, shard_count = 1;  // request sharding across replicas (GPUs)
     SpecMap rest;                        // backend-specific keys (engine.*, model.*)
+    std::string output_dir;              // non-empty: write the experiment files there (experiment_files.hpp)
+    bool emit_event_log = false;         // ... including events.csv
 };
 
 // K = floor((budget - weights)/block_unit); duplicated weights cost
@@ -157,6 +159,8 @@ inline RunSpec build_spec(const SpecMap& m) {
                 throw ConfigError("shard: index must be in [0, count)");
         } else if (k.rfind("engine.", 0) == 0 || k.rfind("model.", 0) == 0) s.rest[k] = v;
         else if (k == "trace") s.rest[k] = v;
+        else if (k == "output_dir") s.output_dir = v;  // ExperimentConfig::output_dir (config.hpp:44)
+        else if (k == "emit_event_log") s.emit_event_log = v == "1" || v == "true";
         else throw ConfigError("spec: unknown key '" + k + "'");
         have_ws = have_ws || k == "n";
     }

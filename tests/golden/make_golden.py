@@ -2,7 +2,9 @@
 
 Run here, where /root/reference exists:  python tests/golden/make_golden.py
 
-* sched_golden.json -- the UNMODIFIED reference simulator (oracle/_ref/refsim,
+* sched_golden.json -- (files:*) sha256 of the reference's experiment files
+  (oracle/_ref/refwrite: write_experiment) for 6 randomized specs; and
+  the UNMODIFIED reference simulator (oracle/_ref/refsim,
   compiled from /root/reference/proj/include by oracle/Makefile) run on the
   shipped configs (configs/*.json as specs) and on 40 randomized specs from
   tests/test_sched_parity.random_spec.  Small outputs are stored verbatim,
@@ -51,6 +53,12 @@ def sched_cases():
     return cases
 
 
+def random_spec_files(s):
+    from test_sched_parity import random_spec
+
+    return random_spec(3000 + s)
+
+
 def make_sched():
     out = {}
     for name, spec in sched_cases().items():
@@ -62,6 +70,17 @@ def make_sched():
         elif p.returncode == 0:
             rec["report"] = report_block(p.stdout)
         out[name] = rec
+    # the reference's experiment files (write_experiment) for a few specs: sha256 per file
+    import tempfile
+    refwrite = os.path.join(ROOT, "oracle", "_ref", "refwrite")
+    for i, spec in enumerate([random_spec_files(s) for s in range(6)]):
+        d = tempfile.mkdtemp()
+        p = subprocess.run([refwrite, "--write", d, spec], capture_output=True, text=True)
+        if p.returncode != 0:
+            continue
+        out[f"files:{i}"] = {"spec": spec, "sha256": {
+            f: hashlib.sha256(open(os.path.join(d, f)).read().encode()).hexdigest()
+            for f in ("report.json", "requests.csv", "timeseries.csv", "events.csv")}}
     with open(os.path.join(HERE, "sched_golden.json"), "w") as f:
         json.dump(out, f, indent=1, sort_keys=True)
     print(f"sched_golden.json: {len(out)} cases")

@@ -19,7 +19,7 @@ from oracle import model as M
 
 HERE = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 with open(os.path.join(HERE, "sched_golden.json")) as _f:
-    SCHED = json.load(_f)
+    SCHED = {k: v for k, v in json.load(_f).items() if not k.startswith("files:")}
 TINY = np.load(os.path.join(HERE, "tiny_cfg1.npz"))
 TOL = 1e-2
 

@@ -31,6 +31,8 @@ RUNS = {
     "pipelined_P2_green48": "policy=pipelined_splitwiser;P=2;max_batch=4;engine.split=1;engine.decode_lanes=2;"
                             "engine.decode_sms=48",
     "mixed_green64_arrivals": "policy=mixed_batching;arrival=fixed:0.003;engine.split=1;engine.decode_sms=64",
+    # prefill GEMMs capped at one tile per CTA while decode work exists (tile-granular interleaving)
+    "pipelined_P2_yield1": "policy=pipelined_splitwiser;P=2;max_batch=4;engine.split=1;engine.prefill_yield=1",
 }
 
 
