@@ -307,7 +307,7 @@ private:
     }
 
     void schedule_pass() {
-        const std::vector<TaskRequest> trs = sched_.next_tasks(*this);
+        const std::vector<TaskRequest> trs = pass_tasks();
         if (trs.empty()) return;
         // group: coalesced -> one launch per kind; else one per task
         std::vector<Launch> group;

@@ -32,6 +32,7 @@
 #include <limits>
 #include <map>
 #include <string>
+#include <deque>
 #include <vector>
 
 #include "event_log.hpp"
@@ -69,6 +70,13 @@ struct SimulationInputs {
     CostModel cost;
     int block_tokens = 16;
     SharingDiscipline discipline;
+    // New: one KV quota shared by every instance instead of
+    // the reference's even per-instance split (engine.hpp:65-72).  Each
+    // instance's pool reports the whole capacity and reserved_blocks() the sum
+    // over instances, so the unchanged admission rule (admit_fifo) admits
+    // against the shared quota; the worst-case reservations keep the sum of the
+    // instances' allocations within it.
+    bool shared_kv_pool = false;
 };
 
 // A timestamp that may only be known later (GPU events): `ev >= 0` names a
@@ -98,7 +106,7 @@ public:
             throw ConfigError("discipline.mode: exclusive requires a single-instance scheduler");
         const long long total = in_.gpu.kv_capacity_blocks;
         for (int i = 0; i < n; ++i) {
-            const long long cap = total / n + (i < total % n ? 1 : 0);
+            const long long cap = in_.shared_kv_pool ? total : total / n + (i < total % n ? 1 : 0);
             if (cap < 1) throw ConfigError("gpu.kv_capacity_blocks: too small for instance count");
             pools_.emplace_back(in_.block_tokens, cap);
             log_.kv_capacity.push_back(cap);
@@ -137,7 +145,14 @@ public:
     RequestState state(int id) const override { return entry(id).req.state; }
     int generated(int id) const override { return entry(id).generated; }
     const KvBlockPool& pool(int inst) const override { return pools_.at(static_cast<std::size_t>(inst)); }
-    long long reserved_blocks(int inst) const override { return reserved_.at(static_cast<std::size_t>(inst)); }
+    long long reserved_blocks(int inst) const override {
+        if (in_.shared_kv_pool) {
+            long long all = pending_reserve_;  // prompts accepted earlier in this pass
+            for (long long r : reserved_) all += r;
+            return all;
+        }
+        return reserved_.at(static_cast<std::size_t>(inst));
+    }
     long long footprint_blocks(int id) const override { return entry(id).footprint; }
     int active_count(int inst, TaskKind k) const override {
         return (k == TaskKind::Prompt ? n_prompt_ : n_step_).at(static_cast<std::size_t>(inst));
@@ -180,6 +195,42 @@ protected:
         sched_.on_arrival(e.req.id);
     }
 
+    // Shared KV quota: a lane admits against the quota without seeing what
+    // another lane admitted in the same pass (the unchanged reference lanes
+    // reserve at activation), so a prompt that no longer fits waits here, in
+    // order, until reservations are released; its TaskStart is logged when it
+    // activates.  Lanes that hold reservations are decoding and release them
+    // without needing a prompt, so the wait always ends.
+    bool fits(const TaskRequest& tr) const {
+        if (!in_.shared_kv_pool || tr.kind != TaskKind::Prompt) return true;
+        long long need = 0;
+        for (int rid : tr.batch) need += entry(rid).footprint;
+        return reserved_blocks(tr.instance_id) + need <= pools_.at(static_cast<std::size_t>(tr.instance_id)).capacity();
+    }
+    // The next pass's tasks: deferred prompts that fit now (in order), then the
+    // scheduler's new ones, deferring any prompt that does not fit.
+    std::vector<TaskRequest> pass_tasks() {
+        std::vector<TaskRequest> out;
+        while (!deferred_.empty() && fits(deferred_.front())) {
+            out.push_back(deferred_.front());
+            deferred_.pop_front();
+            reserve_pending(out.back());
+        }
+        for (const TaskRequest& tr : sched_.next_tasks(*this)) {
+            if (deferred_.empty() && fits(tr)) {
+                out.push_back(tr);
+                reserve_pending(tr);
+            } else if (tr.kind == TaskKind::Prompt) {
+                deferred_.push_back(tr);
+            } else {
+                out.push_back(tr);
+            }
+        }
+        pending_reserve_ = 0;
+        return out;
+    }
+    std::size_t deferred_count() const { return deferred_.size(); }
+
     // Validate, reserve, allocate and log one task; returns its index in active_.
     std::size_t activate(const TaskRequest& tr, Stamp at) {
         if (tr.instance_id < 0 || tr.instance_id >= static_cast<int>(pools_.size()))
@@ -195,7 +246,7 @@ protected:
                 prompt_batch.push_back(e.req);
                 need += e.footprint;
             }
-            if (reserved_[inst] + need > pools_[inst].capacity())
+            if (reserved_blocks(static_cast<int>(inst)) + need > pools_[inst].capacity())
                 throw ContractViolation("scheduler: prompt batch exceeds KV reservation capacity");
             for (int rid : tr.batch) {
                 Entry& e = entry(rid);
@@ -335,6 +386,12 @@ protected:
     std::vector<KvBlockPool> pools_;
     PagePool pages_;
     std::vector<long long> reserved_;
+    std::deque<TaskRequest> deferred_;  // shared KV quota: prompts waiting for reservations
+    long long pending_reserve_ = 0;     // shared KV quota: footprints accepted in the current pass
+    void reserve_pending(const TaskRequest& tr) {
+        if (!in_.shared_kv_pool || tr.kind != TaskKind::Prompt) return;
+        for (int rid : tr.batch) pending_reserve_ += entry(rid).footprint;
+    }
     std::vector<int> n_prompt_, n_step_;
     std::vector<Active> active_;
     double clock_ = 0.0;
@@ -432,8 +489,9 @@ public:
                     ++next_arrival;
                 }
             }
-            for (const TaskRequest& tr : sched_.next_tasks(*this)) activate(tr, {clock_});
+            for (const TaskRequest& tr : pass_tasks()) activate(tr, {clock_});
         }
+        if (deferred_count()) throw ContractViolation("engine: deferred prompt never fit the shared KV quota");
         check_all_finished();
         LogRecord end;
         end.kind = LogKind::RunEnd;

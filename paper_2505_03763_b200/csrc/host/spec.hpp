@@ -8,6 +8,8 @@
 //   seed, policy, max_batch, P, n_instances, inner, mode, kv_capacity_blocks,
 //   block_tokens, compute_capacity, mem_bandwidth, weight_mem_units,
 //   shared_weights, mem_budget_units, block_mem_unit, cost.* (a_p ... kv_handoff_s).
+// New keys: kv.shared (one KV quota for all instances, executor.hpp), output_dir /
+// emit_event_log (experiment files, experiment_files.hpp), engine.* (GPU executor).
 // Unknown keys are a ConfigError naming the key (config.hpp:83-91 behaviour).
 #pragma once
 
@@ -136,6 +138,7 @@ inline RunSpec build_spec(const SpecMap& m) {
             else throw ConfigError("discipline.mode: unknown mode '" + v + "'");
         } else if (k == "kv_capacity_blocks") s.kv_capacity_override = integer(k, v);
         else if (k == "block_tokens") s.inputs.block_tokens = static_cast<int>(integer(k, v));
+        else if (k == "kv.shared") s.inputs.shared_kv_pool = v == "1" || v == "true";
         else if (k == "compute_capacity") s.inputs.gpu.compute_capacity = num(k, v);
         else if (k == "mem_bandwidth") s.inputs.gpu.mem_bandwidth = num(k, v);
         else if (k == "weight_mem_units") s.inputs.gpu.weight_mem_units = num(k, v);
