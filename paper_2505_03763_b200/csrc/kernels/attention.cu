@@ -26,7 +26,7 @@ constexpr int kQRows = 64;
 constexpr int kKeys = 64;
 
 template <int HD>
-__global__ void __launch_bounds__(128) attn_prefill_kernel(const __nv_bfloat16* __restrict__ q,
+__global__ void __launch_bounds__(128, HD == 64 ? 4 : 2) attn_prefill_kernel(const __nv_bfloat16* __restrict__ q,
                                                            const __nv_bfloat16* __restrict__ kv_layer,
                                                            __nv_bfloat16* __restrict__ out, PrefillAttnArgs a) {
     extern __shared__ __align__(128) uint8_t smem_raw[];
@@ -114,14 +114,16 @@ __global__ void __launch_bounds__(128) attn_prefill_kernel(const __nv_bfloat16* 
                 mma_bf16(sc[2 * np + 1], qf[ks], b[2], b[3]);
             }
         }
-        // mask + online softmax (log2 domain)
+        // mask + online softmax (log2 domain).  The max runs on raw scores
+        // (scale > 0 keeps the order) and the scale folds into the exponent:
+        // p = 2^(s * scale - m) is one FFMA + one MUFU.EX2 per score.
         const bool edge = (blk + 1) * kKeys > q0 || (blk + 1) * kKeys > len;
         float mx[2] = {-INFINITY, -INFINITY};
 #pragma unroll
         for (int nb = 0; nb < 8; ++nb) {
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
-                float v = sc[nb][e] * a.scale_log2;
+                float v = sc[nb][e];
                 if (edge) {
                     const int key = blk * kKeys + nb * 8 + (lane & 3) * 2 + (e & 1);
                     const int qp = row_a + ((e >> 1) << 3);
@@ -136,9 +138,9 @@ __global__ void __launch_bounds__(128) attn_prefill_kernel(const __nv_bfloat16* 
         for (int r = 0; r < 2; ++r) {
             mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 1));
             mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 2));
-            const float m_new = fmaxf(m_run[r], mx[r]);
+            const float m_new = fmaxf(m_run[r], mx[r] * a.scale_log2);
             const float m_use = m_new == -INFINITY ? 0.f : m_new;
-            alpha[r] = exp2f(m_run[r] - m_use);
+            alpha[r] = fast_exp2(m_run[r] - m_use);
             m_run[r] = m_new;
             mx[r] = m_use;
         }
@@ -147,19 +149,22 @@ __global__ void __launch_bounds__(128) attn_prefill_kernel(const __nv_bfloat16* 
         for (int nb = 0; nb < 8; ++nb) {
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
-                const float p = exp2f(sc[nb][e] - mx[e >> 1]);
+                const float p = fast_exp2(fmaf(sc[nb][e], a.scale_log2, -mx[e >> 1]));
                 sc[nb][e] = p;
                 rs[e >> 1] += p;
             }
         }
 #pragma unroll
         for (int r = 0; r < 2; ++r) l_run[r] = l_run[r] * alpha[r] + rs[r];
+        // rescale O only when some row's max moved (most blocks past the first few leave it)
+        if (__any_sync(0xffffffffu, alpha[0] != 1.f || alpha[1] != 1.f)) {
 #pragma unroll
-        for (int i = 0; i < HD / 8; ++i) {
-            o[i][0] *= alpha[0];
-            o[i][1] *= alpha[0];
-            o[i][2] *= alpha[1];
-            o[i][3] *= alpha[1];
+            for (int i = 0; i < HD / 8; ++i) {
+                o[i][0] *= alpha[0];
+                o[i][1] *= alpha[0];
+                o[i][2] *= alpha[1];
+                o[i][3] *= alpha[1];
+            }
         }
         // O += P V
 #pragma unroll

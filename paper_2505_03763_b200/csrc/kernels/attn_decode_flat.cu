@@ -298,13 +298,13 @@ __global__ void __launch_bounds__(NWARP * 32)
         mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
         mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
         const float m_new = fmaxf(m_run, mx);  // finite: key 0 of every page is valid
-        const float alpha = exp2f(m_run - m_new);
+        const float alpha = fast_exp2(m_run - m_new);
         m_run = m_new;
         float rs = 0.f;
 #pragma unroll
         for (int nb = 0; nb < 2; ++nb) {
-            sc[nb][0] = exp2f(sc[nb][0] - m_new);
-            sc[nb][1] = exp2f(sc[nb][1] - m_new);
+            sc[nb][0] = fast_exp2(sc[nb][0] - m_new);
+            sc[nb][1] = fast_exp2(sc[nb][1] - m_new);
             rs += sc[nb][0] + sc[nb][1];
         }
         l_run = l_run * alpha + rs;
@@ -406,7 +406,7 @@ __global__ void __launch_bounds__(NWARP * 32)
                         for (int j = 0; j < NB; ++j) {
                             if (c0 + j <= cb) {
                                 const float mn = fmaxf(Mx, ml[j].x);
-                                const float c_old = exp2f(Mx - mn), c_new = exp2f(ml[j].x - mn);
+                                const float c_old = fast_exp2(Mx - mn), c_new = fast_exp2(ml[j].x - mn);
                                 Mx = mn;
                                 Ls = Ls * c_old + ml[j].y * c_new;
 #pragma unroll

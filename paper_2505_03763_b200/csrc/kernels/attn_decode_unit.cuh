@@ -199,13 +199,13 @@ __device__ __forceinline__ void decode_unit(const DecodeAttnArgs& a, const __nv_
         mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
         mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
         const float m_new = fmaxf(m_run, mx);  // finite: the block's first key is valid
-        const float alpha = exp2f(m_run - m_new);
+        const float alpha = fast_exp2(m_run - m_new);
         m_run = m_new;
         float rs = 0.f;
 #pragma unroll
         for (int nb = 0; nb < KB / 8; ++nb) {
-            sc[nb][0] = exp2f(sc[nb][0] - m_new);
-            sc[nb][1] = exp2f(sc[nb][1] - m_new);
+            sc[nb][0] = fast_exp2(sc[nb][0] - m_new);
+            sc[nb][1] = fast_exp2(sc[nb][1] - m_new);
             sc[nb][2] = sc[nb][3] = 0.f;  // padding rows
             rs += sc[nb][0] + sc[nb][1];
         }
@@ -259,7 +259,7 @@ __device__ __forceinline__ void decode_unit(const DecodeAttnArgs& a, const __nv_
         float L = 0.f, O = 0.f;
 #pragma unroll
         for (int w = 0; w < 4; ++w) {
-            const float sc_w = cm[w * G + g] == -INFINITY ? 0.f : exp2f(cm[w * G + g] - M);
+            const float sc_w = cm[w * G + g] == -INFINITY ? 0.f : fast_exp2(cm[w * G + g] - M);
             L += cl[w * G + g] * sc_w;
             O += co[(w * G + g) * HD + d] * sc_w;
         }
@@ -295,7 +295,7 @@ __device__ __forceinline__ void decode_unit(const DecodeAttnArgs& a, const __nv_
             for (int sp = 0; sp < splits; ++sp) M = fmaxf(M, __ldcg(a.part_ml + ((base + sp) * G + g) * 2));
             float L = 0.f, O = 0.f;
             for (int sp = 0; sp < splits; ++sp) {
-                const float w = exp2f(__ldcg(a.part_ml + ((base + sp) * G + g) * 2) - M);
+                const float w = fast_exp2(__ldcg(a.part_ml + ((base + sp) * G + g) * 2) - M);
                 L += __ldcg(a.part_ml + ((base + sp) * G + g) * 2 + 1) * w;
                 O += __ldcg(a.part_o + (base + sp) * G * HD + idx) * w;
             }

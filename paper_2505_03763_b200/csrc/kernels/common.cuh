@@ -78,6 +78,15 @@ __device__ __forceinline__ uint32_t pack_bf2(float lo, float hi) {
     return *reinterpret_cast<uint32_t*>(&p);
 }
 
+// 2^x as one MUFU.EX2 (exp2f adds a denormal range fix-up: FSETP + two
+// predicated FMULs per call, a third of the softmax's issue slots in the
+// prefill attention).  Results below 2^-126 flush to zero, -inf -> 0.
+__device__ __forceinline__ float fast_exp2(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
