@@ -121,7 +121,8 @@ void ws_alloc(Workspace& w, const sw_model_desc& d, int rows, bool decode, int m
     } else {
         // header + tokens/pos/slot per token + per-seq arrays + tiles + page rows
         const size_t T = static_cast<size_t>(rows);
-        w.pmeta_bytes = (16 + 3 * T + 6 * (T + 1) + 2 * (T / 64 + T + 1) + (T / 16 + T + 1)) * sizeof(int32_t);
+        w.pmeta_bytes =
+            (16 + 3 * T + 6 * (T + 1) + 2 * (T / 64 + T + 1) + 2 * (T / 128 + T + 1) + (T / 16 + T + 1)) * sizeof(int32_t);
         w.pmeta = dalloc<int32_t>(w.pmeta_bytes / sizeof(int32_t));
     }
 }
@@ -216,10 +217,13 @@ void prefill_forward(sw_model* m, sw_kv* kv, const sw_batch& b, cudaStream_t st,
         int n_tiles = 0;
         for (int s = 0; s < S; ++s) n_tiles += cdiv(b.n_tokens[first + s], 64);
         int32_t *tseq = take(n_tiles), *tq0 = take(n_tiles);
+        int n_tiles128 = 0;  // 128-row tiles of the tcgen05 attention
+        for (int s = 0; s < S; ++s) n_tiles128 += cdiv(b.n_tokens[first + s], 128);
+        int32_t *tseq128 = take(n_tiles128), *tq0128 = take(n_tiles128);
         int n_pages_total = 0;
         for (int s = 0; s < S; ++s) n_pages_total += cdiv(b.n_tokens[first + s], B);
         int32_t* prow = take(n_pages_total);
-        int t = 0, ti = 0, pg = 0;
+        int t = 0, ti = 0, ti128 = 0, pg = 0;
         cu[0] = 0;
         poff[0] = 0;
         for (int s = 0; s < S; ++s) {
@@ -242,6 +246,10 @@ void prefill_forward(sw_model* m, sw_kv* kv, const sw_batch& b, cudaStream_t st,
                 tseq[ti] = s;
                 tq0[ti] = q0;
             }
+            for (int q0 = 0; q0 < n; q0 += 128, ++ti128) {
+                tseq128[ti128] = s;
+                tq0128[ti128] = q0;
+            }
             tok_off += n;
             page_off += np;
             t += n;
@@ -255,6 +263,7 @@ void prefill_forward(sw_model* m, sw_kv* kv, const sw_batch& b, cudaStream_t st,
         h[0] = T;
         h[1] = S;
         h[2] = n_tiles;
+        h[3] = n_tiles128;
         const size_t bytes = static_cast<size_t>(p - h) * sizeof(int32_t);
         if (bytes > w.pmeta_bytes || bytes > m->pre_ring.bytes) throw ContractViolation("prefill: metadata overflow");
         SW_CUDA(cudaMemcpyAsync(w.pmeta, h, bytes, cudaMemcpyHostToDevice, st));
@@ -282,6 +291,29 @@ void prefill_forward(sw_model* m, sw_kv* kv, const sw_batch& b, cudaStream_t st,
         aa.H = d.n_heads;
         aa.Hkv = d.n_kv_heads;
         aa.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(d.head_dim)));
+        // prefill attention on tcgen05 (SW_PREFILL_TC=0: the mma.sync kernel)
+        static const int tc_env = [] {
+            const char* v = std::getenv("SW_PREFILL_TC");
+            return v && *v ? std::atoi(v) : 1;
+        }();
+        const bool use_tc = tc_env && kv->tm_kv_ok;
+        PrefillTcArgs ta{};
+        CUtensorMap tm_q{};
+        if (use_tc) {
+            ta.n_tiles = w.pmeta + 3;
+            ta.tile_seq = dev(tseq128);
+            ta.tile_q0 = dev(tq0128);
+            ta.cu_seqlens = dev(cu);
+            ta.seq_slot = dev(sslot);
+            ta.page_table = kv->page_table;
+            ta.max_pages = kv->max_pages;
+            ta.H = d.n_heads;
+            ta.Hkv = d.n_kv_heads;
+            ta.scale_log2 = aa.scale_log2;
+            ta.page_rows = static_cast<int>(kv->page_stride / d.head_dim);
+            ta.v_rows = static_cast<int>(kv->page_stride / 2 / d.head_dim);
+            tm_q = make_tmap_heads(w.q, static_cast<uint64_t>(w.rows), d.n_heads, d.head_dim);
+        }
         for (int l = 0; l < d.n_layers; ++l) {
             const LayerWeights& L = m->layers[l];
             __nv_bfloat16* kvl = kv->pages + l * kv->layer_stride;
@@ -289,7 +321,12 @@ void prefill_forward(sw_model* m, sw_kv* kv, const sw_batch& b, cudaStream_t st,
             gemm_run(lp(gp(w.xn, w.rows, L.wqkv, qkv_w, T, qkv_w, d.d_model, EPI_STORE_F32, false, w.qkv, qkv_w)), st);
             rope_kv(w.qkv, w.q, kvl, dev(tpos), dev(tslot), kv->page_table, m->rope_cs, T, nullptr, d.n_heads,
                     d.n_kv_heads, d.head_dim, kv->max_pages, B, st);
-            attn_prefill(w.q, kvl, w.attn, aa, n_tiles, d.head_dim, st);
+            if (use_tc) {
+                ta.layer_row0 = static_cast<int>(l * kv->layer_stride / d.head_dim);
+                attn_prefill_tc(tm_q, kv->tm_kv, w.attn, ta, n_tiles128, d.head_dim, st);
+            } else {
+                attn_prefill(w.q, kvl, w.attn, aa, n_tiles, d.head_dim, st);
+            }
             gemm_run(lp(gp(w.attn, w.rows, L.wo, d.d_model, T, d.d_model, hdH, EPI_RESID, false, w.x, d.d_model)), st);
             rmsnorm(w.x, L.g_mlp, w.xn, T, d.d_model, d.norm_eps, nullptr, nullptr, st);
             gemm_run(lp(gp(w.xn, w.rows, L.wgu, 2 * d.ffn_dim, T, 2 * d.ffn_dim, d.d_model, EPI_SWIGLU, false, w.act,

@@ -44,6 +44,25 @@ struct DecodeAttnArgs {
     int max_ctx;         // longest context the arena holds (sizes the grid)
 };
 
+// Prefill on tcgen05 (attn_prefill_tc.cu): 128-row query tiles (host-built
+// list), Q through a 3-D TMA map over [tokens][H][hd], K/V through the arena map.
+struct PrefillTcArgs {
+    const int* n_tiles;        // device
+    const int32_t* tile_seq;   // device [tiles]
+    const int32_t* tile_q0;    // device [tiles]
+    const int32_t* cu_seqlens; // device [seqs + 1]
+    const int32_t* seq_slot;   // device [seqs]
+    const int32_t* page_table; // device [slots][max_pages]
+    int max_pages;
+    int H, Hkv;
+    float scale_log2;
+    int layer_row0;  // arena-map row of (layer, page 0, K, head 0)
+    int page_rows;   // arena-map rows per page
+    int v_rows;      // K -> V rows inside a page
+};
+void attn_prefill_tc(const CUtensorMap& tm_q, const CUtensorMap& tm_kv, __nv_bfloat16* out, const PrefillTcArgs& a,
+                     int max_tiles, int hd, cudaStream_t st);
+
 // Flat page-balanced decode attention (attn_decode_flat.cu): persistent grid,
 // TMA page-slice loads through a 2-D map of the whole KV arena (rows of hd
 // elements; K slice of (layer l, page p, kv head h) at row

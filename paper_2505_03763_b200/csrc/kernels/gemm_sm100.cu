@@ -558,6 +558,21 @@ CUtensorMap make_tmap_bf16(const void* base, uint64_t rows, uint64_t cols, uint3
     return m;
 }
 
+// [rows][heads][hd] bf16 as a 3-D map (hd, heads, rows), box 64 x 1 x 128,
+// SWIZZLE_128B: one head's 128-row x 64-column tile per load.
+CUtensorMap make_tmap_heads(const void* base, uint64_t rows, uint64_t heads, uint64_t hd) {
+    CUtensorMap m;
+    const cuuint64_t dims[3] = {hd, heads, rows};
+    const cuuint64_t strides[2] = {hd * 2, heads * hd * 2};
+    const cuuint32_t box[3] = {64, 1, 128};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides,
+                                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw_cuda("cuTensorMapEncodeTiled (3d)", cudaErrorInvalidValue, __FILE__, __LINE__);
+    return m;
+}
+
 const CUtensorMap& tmap_cached(const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
     static std::mutex mu;
     static std::map<std::tuple<const void*, uint64_t, uint64_t, uint32_t>, CUtensorMap> cache;

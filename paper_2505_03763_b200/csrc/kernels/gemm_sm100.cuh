@@ -87,6 +87,7 @@ struct GemmProblem {
 };
 
 CUtensorMap make_tmap_bf16(const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows);
+CUtensorMap make_tmap_heads(const void* base, uint64_t rows, uint64_t heads, uint64_t hd);
 const CUtensorMap& tmap_cached(const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows);
 void gemm_run(const GemmProblem& p, cudaStream_t st);
 // decode projections: split-K over a cluster (gemm_decode.cu)
