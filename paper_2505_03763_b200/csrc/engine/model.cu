@@ -296,7 +296,7 @@ void prefill_forward(sw_model* m, sw_kv* kv, const sw_batch& b, cudaStream_t st,
             const char* v = std::getenv("SW_PREFILL_TC");
             return v && *v ? std::atoi(v) : 1;
         }();
-        const bool use_tc = tc_env && kv->tm_kv_ok;
+        const bool use_tc = tc_env && kv->tm_kv_ok && (d.n_heads / d.n_kv_heads) % 2 == 0;  // head pairs share a kv head
         PrefillTcArgs ta{};
         CUtensorMap tm_q{};
         if (use_tc) {

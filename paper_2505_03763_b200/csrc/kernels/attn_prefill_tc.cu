@@ -1,8 +1,12 @@
 // Prefill attention on the 5th-generation tensor cores (sm_100a tcgen05/TMEM).
 //
 // Causal flash attention for a varlen batch of prompts over the paged KV cache
-// (GQA).  One CTA = 128 query rows of one head of one prompt, 128 threads,
-// thread t owns query row t (TMEM lane t).  Per 128-key block j:
+// (GQA).  One CTA = 128 query rows of one prompt for TWO query heads of the
+// same kv head: two independent 128-thread groups (warps 0-3 | 4-7), each with
+// its own S/O accumulators in TMEM, P buffer, MMA-issuing thread and barriers,
+// sharing the K/V blocks -- while one group runs its softmax the tensor core
+// works on the other group's MMAs.  Thread t of a group owns query row t (TMEM
+// lane t).  Per 128-key block j and group:
 //   S  = Q K_j^T        tcgen05.mma M=128 N=128 K=hd, Q and K from smem
 //                       (TMA SWIZZLE_128B, K-major), S fp32 in TMEM cols [0,128)
 //   softmax             each thread tcgen05.ld's its S row twice (max, then
@@ -16,9 +20,9 @@
 // Q (a 3-D TMA map over [tokens][H][hd]) and K/V (one 16-row TMA box per page
 // slice, the arena-wide map of the decode attention) are loaded by thread 0:
 // K double-buffered (block j+1 lands while block j's softmax runs), V single
-// (block j+1's V lands during the next S MMA and softmax).  Two CTAs fit per SM
-// at hd 64 (96 KB smem), so one CTA's softmax overlaps the other's MMAs; at
-// hd 128 (160 KB) one CTA per SM.
+// (block j+1's V lands during the next S MMA and softmax); a stage is reloaded
+// once both groups' MMAs released it (count-2 "empty" barriers).  smem: 144 KB
+// (hd 64) / 224 KB (hd 128), TMEM: 512 columns -- one CTA per SM.
 #include <cuda.h>
 
 #include <algorithm>
@@ -75,19 +79,20 @@ template <int HD>
 struct TcCfg {
     static constexpr int NH = HD / 64;                 // 64-wide column atoms of a head row
     static constexpr int kAtom = kRows * 128;          // one [128 rows][128 B] atom column
-    static constexpr int kQ = NH * kAtom;
+    static constexpr int kQ = NH * kAtom;              // one group's Q tile
     static constexpr int kKV = NH * kAtom;             // one K (or V) block of 128 keys
     static constexpr int kP = 2 * kAtom;               // P: 128 rows x 128 keys bf16
-    static constexpr int kOffK = kQ;                   // K: two stages
+    static constexpr int kOffK = 2 * kQ;               // K: two stages
     static constexpr int kOffV = kOffK + 2 * kKV;      // V: one stage
-    static constexpr int kOffP = kOffV + kKV;
-    static constexpr int kOffBar = kOffP + kP;
-    static constexpr int kSmem = 1024 + kOffBar + 64;
-    static constexpr uint32_t kTmemCols = 256;          // S [0,128) + O [128, 128+HD)
+    static constexpr int kOffP = kOffV + kKV;          // P: one per group
+    static constexpr int kOffBar = kOffP + 2 * kP;
+    static constexpr int kSmem = 1024 + kOffBar + 128;
+    static_assert(kSmem <= 227 * 1024, "smem budget");
+    static constexpr uint32_t kTmemCols = 512;          // group g: S [256g, 256g+128), O [256g+128, +HD)
 };
 
 template <int HD>
-__global__ void __launch_bounds__(128) attn_prefill_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
+__global__ void __launch_bounds__(256, 1) attn_prefill_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
                                                               const __grid_constant__ CUtensorMap tm_kv,
                                                               __nv_bfloat16* __restrict__ out, PrefillTcArgs a) {
     using C = TcCfg<HD>;
@@ -99,21 +104,25 @@ __global__ void __launch_bounds__(128) attn_prefill_tc_kernel(const __grid_const
     uint8_t* sP = smem + C::kOffP;
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + C::kOffBar);
     uint64_t* q_full = bar;
-    uint64_t* k_full = bar + 1;  // [2]
-    uint64_t* v_full = bar + 3;
-    uint64_t* s_done = bar + 4;
-    uint64_t* o_done = bar + 5;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 6);
+    uint64_t* k_full = bar + 1;   // [2]
+    uint64_t* k_empty = bar + 3;  // [2] both groups' S MMAs of the stage retired
+    uint64_t* v_full = bar + 5;
+    uint64_t* v_empty = bar + 6;  // both groups' PV MMAs retired
+    uint64_t* s_done_g = bar + 7;  // [2] per group
+    uint64_t* o_done_g = bar + 9;  // [2] per group
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 11);
 
     const int tile = blockIdx.x;
     if (tile >= *a.n_tiles) return;
-    const int h = blockIdx.y;
-    const int hk = h / (a.H / a.Hkv);
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const int g = warp >> 2;              // group: query head 2 * blockIdx.y + g
+    const int gt = tid & 127;             // thread within the group = query row
+    const int h = 2 * blockIdx.y + g;
+    const int hk = h / (a.H / a.Hkv);     // same for both groups (H / Hkv even)
     const int sq = a.tile_seq[tile];
     const int q0 = a.tile_q0[tile];
     const int start = a.cu_seqlens[sq];
     const int len = a.cu_seqlens[sq + 1] - start;
-    const int tid = threadIdx.x, warp = tid >> 5;
     const int kend = min(q0 + kRows, len);        // keys this tile attends to: [0, kend)
     const int nblk = (kend + kBlk - 1) / kBlk;
     const int npages = (len + kPg - 1) / kPg;
@@ -122,9 +131,14 @@ __global__ void __launch_bounds__(128) attn_prefill_tc_kernel(const __grid_const
         mbar_init(q_full, 1);
         mbar_init(&k_full[0], 1);
         mbar_init(&k_full[1], 1);
+        mbar_init(&k_empty[0], 2);
+        mbar_init(&k_empty[1], 2);
         mbar_init(v_full, 1);
-        mbar_init(s_done, 1);
-        mbar_init(o_done, 1);
+        mbar_init(v_empty, 2);
+        for (int q = 0; q < 2; ++q) {
+            mbar_init(&s_done_g[q], 1);
+            mbar_init(&o_done_g[q], 1);
+        }
         fence_mbar_init();
         tma_prefetch_desc(&tm_q);
         tma_prefetch_desc(&tm_kv);
@@ -137,7 +151,11 @@ __global__ void __launch_bounds__(128) attn_prefill_tc_kernel(const __grid_const
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
-    const uint32_t tS = tmem, tO = tmem + kBlk;
+    const uint32_t tS = tmem + 256 * g, tO = tS + kBlk;
+    uint64_t* s_done = &s_done_g[g];
+    uint64_t* o_done = &o_done_g[g];
+    uint8_t* sQg = sQ + g * C::kQ;
+    uint8_t* sPg = sP + g * C::kP;
 
     // K (v = 0) or V (v = 1) of key block j into `dst`, completing on `b` (thread 0).
     // Page ids past the prompt read page 0 (finite data, masked).
@@ -158,27 +176,32 @@ __global__ void __launch_bounds__(128) attn_prefill_tc_kernel(const __grid_const
         }
     };
     if (tid == 0) {
-        mbar_expect_tx(q_full, C::kQ);
+        mbar_expect_tx(q_full, 2 * C::kQ);
 #pragma unroll
-        for (int c = 0; c < C::NH; ++c) tma_load_3d(sQ + c * C::kAtom, &tm_q, q_full, c * 64, h, start + q0);
+        for (int q = 0; q < 2; ++q)
+#pragma unroll
+            for (int c = 0; c < C::NH; ++c)
+                tma_load_3d(sQ + q * C::kQ + c * C::kAtom, &tm_q, q_full, c * 64, 2 * blockIdx.y + q, start + q0);
         load_blk(0, 0, sK, &k_full[0]);
         load_blk(0, 1, sV, v_full);
     }
 
     constexpr uint32_t idesc_s = umma_idesc_bf16(kRows, kBlk);
     constexpr uint32_t idesc_o = umma_idesc_bf16(kRows, HD) | (1u << 16);  // B (V) MN-major
-    const uint32_t q_addr = smem_addr(sQ), k_addr = smem_addr(sK), v_addr = smem_addr(sV), p_addr = smem_addr(sP);
-    (void)npages;
-    const int row = tid;                       // query row of this thread (TMEM lane)
+    const uint32_t q_addr = smem_addr(sQg), k_addr = smem_addr(sK), v_addr = smem_addr(sV), p_addr = smem_addr(sPg);
+    const int row = gt;                        // query row of this thread (TMEM lane)
     const int qp = q0 + row;                   // its position in the prompt
-    const uint32_t lane_off = static_cast<uint32_t>(warp * 32) << 16;
+    const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
     float m_run = -INFINITY, l_run = 0.f;
 
     for (int j = 0; j < nblk; ++j) {
         const int s = j & 1;
-        // ---- S = Q K_j^T (K_{j+1} streams into the other stage meanwhile)
-        if (tid == 0) {
-            if (j + 1 < nblk) load_blk(j + 1, 0, sK + (s ^ 1) * C::kKV, &k_full[s ^ 1]);
+        // ---- S = Q K_j^T (K_{j+1} streams into the other stage once both groups' S_{j-1} retired)
+        if (tid == 0 && j + 1 < nblk) {
+            if (j >= 1) mbar_wait(&k_empty[s ^ 1], ((j - 1) >> 1) & 1);
+            load_blk(j + 1, 0, sK + (s ^ 1) * C::kKV, &k_full[s ^ 1]);
+        }
+        if (gt == 0) {
             if (j == 0) mbar_wait(q_full, 0);
             mbar_wait(&k_full[s], (j >> 1) & 1);
             tc_fence_after();
@@ -190,6 +213,7 @@ __global__ void __launch_bounds__(128) attn_prefill_tc_kernel(const __grid_const
                               umma_desc_sw128(k_addr + s * C::kKV + c * C::kAtom + k * 32), idesc_s,
                               (c | k) != 0 ? 1u : 0u);
             umma_commit(s_done);
+            umma_commit(&k_empty[s]);
         }
         mbar_wait(s_done, j & 1);
         tc_fence_after();
@@ -249,9 +273,9 @@ __global__ void __launch_bounds__(128) attn_prefill_tc_kernel(const __grid_const
         }
         fence_proxy_async_smem();  // P (generic-proxy stores) -> visible to the tensor core
         tc_fence_before();
-        __syncthreads();
+        asm volatile("bar.sync %0, 128;" ::"r"(1 + g) : "memory");  // this group's 128 threads
         // ---- O += P V_j
-        if (tid == 0) {
+        if (gt == 0) {
             mbar_wait(v_full, j & 1);
             tc_fence_after();
 #pragma unroll
@@ -259,10 +283,14 @@ __global__ void __launch_bounds__(128) attn_prefill_tc_kernel(const __grid_const
                 umma_bf16(tO, umma_desc_sw128(p_addr + (kc >> 2) * C::kAtom + (kc & 3) * 32),
                           umma_desc_sw128_mn(v_addr + kc * 2048, C::kAtom), idesc_o, (j | kc) != 0 ? 1u : 0u);
             umma_commit(o_done);
+            umma_commit(v_empty);
         }
-        mbar_wait(o_done, j & 1);  // P, V and O are free again
+        mbar_wait(o_done, j & 1);  // this group's P and O are free again
         tc_fence_after();
-        if (tid == 0 && j + 1 < nblk) load_blk(j + 1, 1, sV, v_full);
+        if (tid == 0 && j + 1 < nblk) {  // V_{j+1} once both groups' PV_j retired
+            mbar_wait(v_empty, j & 1);
+            load_blk(j + 1, 1, sV, v_full);
+        }
     }
 
     // ---- epilogue: O / l -> bf16 (TMEM loads are warp-collective: every lane loads, rows past the prompt
@@ -303,7 +331,7 @@ void tc_launch(const CUtensorMap& tq, const CUtensorMap& tkv, __nv_bfloat16* out
         SW_CUDA(cudaFuncSetAttribute(attn_prefill_tc_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
         cfg = true;
     }
-    launch_k(attn_prefill_tc_kernel<HD>, dim3(max_tiles, a.H), dim3(128), C::kSmem, st, tq, tkv, out, a);
+    launch_k(attn_prefill_tc_kernel<HD>, dim3(max_tiles, a.H / 2), dim3(256), C::kSmem, st, tq, tkv, out, a);
 }
 
 }  // namespace
