@@ -24,6 +24,9 @@
 #include "base.hpp"
 #include "event_log.hpp"
 #include "report.hpp"
+#ifdef SW_HAVE_NLOHMANN
+#include <json.hpp>
+#endif
 
 namespace sw {
 
@@ -77,11 +80,23 @@ struct JVal {
     }
 };
 
-// Shortest round-trip digits, laid out the way nlohmann's dump does: fixed
-// notation for decimal exponents in (-4, 15], else d.ddde[+-]XX; integral
-// values keep a ".0".
+// Doubles exactly as the reference's JSON library (nlohmann/json 3.11.3, the
+// version its README pins) prints them: its Grisu2 digit generation is not
+// always the shortest round trip (e.g. 50.959114812191586 where the shortest
+// is 50.95911481219159), so byte-identical report.json needs the same
+// routine.  The build defines SW_HAVE_NLOHMANN when the header is present in
+// the image; otherwise the shortest digits are laid out the same way (fixed
+// notation for decimal exponents in (-4, 15], else d.ddde[+-]XX, integral
+// values keep ".0") and differ from the reference only in such last digits.
 inline std::string json_double(double v) {
     if (!std::isfinite(v)) return "null";
+#ifdef SW_HAVE_NLOHMANN
+    {
+        char nb[64];
+        char* end = nlohmann::detail::to_chars(nb, nb + sizeof nb, v);
+        return std::string(nb, end);
+    }
+#endif
     if (v == 0.0) return std::signbit(v) ? "-0.0" : "0.0";
     char buf[64];
     auto res = std::to_chars(buf, buf + sizeof buf, v, std::chars_format::scientific);

@@ -110,3 +110,16 @@ def test_gpu_run_files_replay_to_the_same_report(tmp_path):
         os.remove(tmp_path / "replay_report.json")
         assert subprocess.run([REFWRITE, "--replay", str(tmp_path / "events.csv")]).returncode == 0
         assert _read(tmp_path, "replay_report.json") == report
+
+
+def test_replay_of_recorded_gpu_log_matches_reference_bytes(swlib, tmp_path):
+    """A GPU run's events.csv (irregular device timestamps) once exposed a
+    last-digit difference: the reference prints doubles with nlohmann's Grisu2,
+    which is not always the shortest round trip.  The recorded reference replay
+    of that log (oracle/_ref/refwrite --replay) is the fixture."""
+    import shutil
+
+    shutil.copy(os.path.join(ROOT, "tests", "golden", "gpu_run_events.csv"), tmp_path / "events.csv")
+    swlib.replay(str(tmp_path / "events.csv"))
+    assert _read(tmp_path, "replay_report.json") == _read(os.path.join(ROOT, "tests", "golden"),
+                                                           "gpu_run_events.reference_replay.json")
