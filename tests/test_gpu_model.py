@@ -172,3 +172,44 @@ def test_long_context_split_kv_and_split_k(shape):
         assert e32.max() < LOGIT_RTOL_FP32
     finally:
         eng.close()
+
+
+# Llama-8B's attention geometry (head_dim 128, 4 query heads per kv head) at a
+# size the oracle runs in seconds: exercises the hd-128 instantiations of the
+# tcgen05 prefill attention (head pairs), the decode attention kernels and the
+# 128-wide epilogues that the 8B bench uses.
+@pytest.mark.parametrize("flat", ["0", "1"])
+def test_hd128_gqa4_prefill_and_decode(flat):
+    import subprocess
+    import sys
+    import textwrap
+
+    # the decode-attention choice is read once per process: run each variant in a child
+    code = textwrap.dedent(f"""
+        import sys, numpy as np
+        sys.path.insert(0, {repr(str(__import__('pathlib').Path(__file__).resolve().parents[1]))})
+        from oracle import model as M
+        from paper_2505_03763_b200 import runtime
+        d = M.Desc(n_layers=2, d_model=512, n_heads=8, n_kv_heads=2, head_dim=128, ffn_dim=1024, vocab=4096)
+        eng = runtime.Engine(d, max_prefill_tokens=4096, max_decode_batch=8, n_pages=512, n_slots=8,
+                             max_pages_per_slot=40, max_out=8)
+        lens = [1, 127, 128, 129, 257, 600]
+        rows = [[i + 8 * j for j in range(40)] for i in range(len(lens))]
+        prompts = [M.prompt_tokens(d.seed, 700 + i, n, d.vocab) for i, n in enumerate(lens)]
+        lg = eng.prefill(list(range(len(lens))), prompts, [r[:(n + 15) // 16] for r, n in zip(rows, lens)])
+        o = M.OracleModel(d, emulate_bf16=True)
+        ref = o.prefill(prompts, [r[:(n + 15) // 16] for r, n in zip(rows, lens)])
+        rel = np.linalg.norm(lg - ref, axis=1) / np.linalg.norm(ref, axis=1)
+        toks = [int(np.argmax(x)) for x in ref]
+        newp = [rows[i][lens[i] // 16] if lens[i] % 16 == 0 else -1 for i in range(len(lens))]
+        lg2 = eng.decode(list(range(len(lens))), lens, tokens=toks, new_page=newp)
+        ref2 = o.decode(toks, lens, [r[:(n + 16) // 16] for r, n in zip(rows, lens)])
+        rel2 = np.linalg.norm(lg2 - ref2, axis=1) / np.linalg.norm(ref2, axis=1)
+        eng.close()
+        print(float(rel.max()), float(rel2.max()))
+    """)
+    env = dict(__import__("os").environ, SW_ATTN_FLAT=flat)
+    p = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, timeout=600)
+    assert p.returncode == 0, p.stderr[-2000:]
+    pre, dec = map(float, p.stdout.split()[-2:])
+    assert pre <= LOGIT_RTOL and dec <= LOGIT_RTOL, (pre, dec)
