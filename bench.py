@@ -38,7 +38,10 @@ WORKLOADS = {
     # serial = the SAME task stream under the one-task gate; best_serial = the fastest
     # serial policy on this closed batch (request-level batching of all 64), reported beside it
     "1b": dict(model="LLAMA_1B", n=64, input=512, output=128, arrival="zero", max_prefill=32768, max_decode=64,
-               split="policy=pipelined_splitwiser;P=2;max_batch=32;engine.split=1",
+               # prefill stream at the higher priority: on this closed batch the prompt sharing the GPU with
+               # the first lane's steps should finish first, so both lanes' steps merge sooner
+               # (profiles/r01c/priority_1b_8b.txt: 241.1 -> 231.8 ms per run)
+               split="policy=pipelined_splitwiser;P=2;max_batch=32;engine.split=1;engine.prefill_priority=1",
                serial="policy=pipelined_splitwiser;P=2;max_batch=32;engine.split=0",
                best_serial="policy=sequential;max_batch=64;engine.split=0"),
     # configs[2]: 8B shape, Poisson arrivals of mixed prompts, mixed batching vs continuous batching

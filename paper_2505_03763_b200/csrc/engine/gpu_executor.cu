@@ -48,6 +48,7 @@ struct GpuOptions {
     int decode_sms = 0;       // split mode: > 0 partitions the SMs with green contexts (decode | prefill)
     bool lean_prefill = false;  // split mode: prompts launched while decode work exists use co-resident GEMM tiles
     int prefill_yield = 0;      // split mode: prompts launched while decode work exists cap GEMM tiles per CTA
+    bool prefill_priority = false;  // split mode: prefill stream at the higher stream priority
     bool coalesce = true;     // one launch per kind per pass
     bool align = true;        // split mode: a token step requested while another is in flight waits for it and
                               // then runs merged with every other waiting step (one weight pass for all lanes)
@@ -116,10 +117,14 @@ public:
         }
         int lo, hi;
         SW_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-        SW_CUDA(cudaStreamCreateWithPriority(&s_prefill_, cudaStreamNonBlocking, lo));
+        // engine.prefill_priority=1: the prefill stream outranks the decode streams (a prompt
+        // that shares the GPU with token steps finishes first -- the lanes' steps then merge
+        // sooner); default: token steps outrank prompts (TBT first)
+        const int p_pre = opt_.prefill_priority ? hi : lo, p_dec = opt_.prefill_priority ? lo : hi;
+        SW_CUDA(cudaStreamCreateWithPriority(&s_prefill_, cudaStreamNonBlocking, p_pre));
         for (int i = 0; i < lanes; ++i) {
             cudaStream_t s = s_prefill_;
-            if (opt_.split) SW_CUDA(cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, hi));
+            if (opt_.split) SW_CUDA(cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, p_dec));
             s_decode_.push_back(s);
         }
     }
@@ -494,6 +499,7 @@ extern "C" int sw_engine_run(sw_model* m, sw_kv* kv, const char* spec, char** ou
             else if (k == "engine.decode_sms") opt.decode_sms = std::stoi(v);
             else if (k == "engine.lean_prefill") opt.lean_prefill = v == "1" || v == "true";
             else if (k == "engine.prefill_yield") opt.prefill_yield = std::stoi(v);
+            else if (k == "engine.prefill_priority") opt.prefill_priority = v == "1" || v == "true";
             else if (k == "engine.peak_flops") opt.peak_flops = std::stod(v);
             else if (k == "engine.peak_bytes") opt.peak_bytes = std::stod(v);
             else throw ConfigError("spec: unknown key '" + k + "'");

@@ -33,6 +33,8 @@ RUNS = {
     "mixed_green64_arrivals": "policy=mixed_batching;arrival=fixed:0.003;engine.split=1;engine.decode_sms=64",
     # prefill GEMMs capped at one tile per CTA while decode work exists (tile-granular interleaving)
     "pipelined_P2_yield1": "policy=pipelined_splitwiser;P=2;max_batch=4;engine.split=1;engine.prefill_yield=1",
+    "pipelined_P2_prefill_priority": "policy=pipelined_splitwiser;P=2;max_batch=4;engine.split=1;"
+                                     "engine.prefill_priority=1",
 }
 
 
