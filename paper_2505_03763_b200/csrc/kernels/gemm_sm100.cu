@@ -353,12 +353,25 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t r[32];
         while (it.next(sc, g)) {
             const int a = si & 1;
+            const int mt = g.tile / sc.tiles_n, nt = g.tile % sc.tiles_n;
+            const int m0 = mt * BM, n0 = nt * BN;
+            // prefill residual add: the residual row's first 32 columns load while the tile's MMAs
+            // still run, and every later chunk's load is in flight one chunk ahead (the epilogue
+            // was a chain of 8 dependent round trips per tile: wo ran at 26% tensor-pipe)
+            float4 res_cur[8];
+            const bool res_live = !SWAP && MODE == EPI_RESID && m0 + row < n_live;
+            float4* res_row = reinterpret_cast<float4*>(static_cast<float*>(args.out) +
+                                                        static_cast<size_t>(m0 + row) * args.ldo + n0);
+            if constexpr (!SWAP && MODE == EPI_RESID) {
+                if (res_live) {
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) res_cur[q] = __ldcg(res_row + q);
+                }
+            }
             mbar_wait(&acc_full[a], (si >> 1) & 1);
             tc_fence_after();
             ++si;
             const uint32_t tb = tmem + a * BN + (static_cast<uint32_t>(quarter * 32) << 16);
-            const int mt = g.tile / sc.tiles_n, nt = g.tile % sc.tiles_n;
-            const int m0 = mt * BM, n0 = nt * BN;
             const bool whole = g.lo == 0 && g.hi == sc.nk;
             if constexpr (!SWAP) {
                 // prefill: whole tiles only
@@ -391,6 +404,30 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 }
                             }
                         }
+                    }
+                } else if constexpr (MODE == EPI_RESID) {
+                    for (int c = 0; c < BN; c += 32) {
+                        float4 res_nxt[8];
+                        if (res_live && c + 32 < BN) {
+#pragma unroll
+                            for (int q = 0; q < 8; ++q) res_nxt[q] = __ldcg(res_row + (c + 32) / 4 + q);
+                        }
+                        tmem_ld32(tb + c, r);
+                        tmem_ld_wait();
+                        if (c == BN - 32) release_acc(a);
+                        if (res_live) {
+#pragma unroll
+                            for (int q = 0; q < 8; ++q) {
+                                float4 v = res_cur[q];
+                                v.x += __uint_as_float(r[4 * q + 0]);
+                                v.y += __uint_as_float(r[4 * q + 1]);
+                                v.z += __uint_as_float(r[4 * q + 2]);
+                                v.w += __uint_as_float(r[4 * q + 3]);
+                                res_row[c / 4 + q] = v;
+                            }
+                        }
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) res_cur[q] = res_nxt[q];
                     }
                 } else {
                     for (int c = 0; c < BN; c += 32) {
