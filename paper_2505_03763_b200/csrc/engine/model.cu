@@ -297,6 +297,12 @@ void prefill_forward(sw_model* m, sw_kv* kv, const sw_batch& b, cudaStream_t st,
             return v && *v ? std::atoi(v) : 1;
         }();
         const bool use_tc = tc_env && kv->tm_kv_ok && (d.n_heads / d.n_kv_heads) % 2 == 0;  // head pairs share a kv head
+        // RoPE + KV write fused into the QKV GEMM epilogue (SW_PREFILL_ROPE_FUSED=0: separate rope_kv pass)
+        static const int fuse_env = [] {
+            const char* v = std::getenv("SW_PREFILL_ROPE_FUSED");
+            return v && *v ? std::atoi(v) : 1;
+        }();
+        const bool fuse_rope = fuse_env != 0 && !lean;
         PrefillTcArgs ta{};
         CUtensorMap tm_q{};
         if (use_tc) {
@@ -318,9 +324,26 @@ void prefill_forward(sw_model* m, sw_kv* kv, const sw_batch& b, cudaStream_t st,
             const LayerWeights& L = m->layers[l];
             __nv_bfloat16* kvl = kv->pages + l * kv->layer_stride;
             rmsnorm(w.x, L.g_attn, w.xn, T, d.d_model, d.norm_eps, nullptr, nullptr, st);
-            gemm_run(lp(gp(w.xn, w.rows, L.wqkv, qkv_w, T, qkv_w, d.d_model, EPI_STORE_F32, false, w.qkv, qkv_w)), st);
-            rope_kv(w.qkv, w.q, kvl, dev(tpos), dev(tslot), kv->page_table, m->rope_cs, T, nullptr, d.n_heads,
-                    d.n_kv_heads, d.head_dim, kv->max_pages, B, st);
+            if (fuse_rope) {  // QKV GEMM with RoPE + q / paged-KV stores in its epilogue
+                GemmProblem pq = lp(gp(w.xn, w.rows, L.wqkv, qkv_w, T, qkv_w, d.d_model, EPI_QKV_ROPE, false, nullptr, 0));
+                pq.fx.pos = dev(tpos);
+                pq.fx.slot = dev(tslot);
+                pq.fx.page_table = kv->page_table;
+                pq.fx.max_pages = kv->max_pages;
+                pq.fx.page_tokens = B;
+                pq.fx.rope_cs = m->rope_cs;
+                pq.fx.q_out = w.q;
+                pq.fx.kv_layer = kvl;
+                pq.fx.page_stride = kv->page_stride;
+                pq.fx.H = d.n_heads;
+                pq.fx.Hkv = d.n_kv_heads;
+                pq.fx.hd = d.head_dim;
+                gemm_run(pq, st);
+            } else {
+                gemm_run(lp(gp(w.xn, w.rows, L.wqkv, qkv_w, T, qkv_w, d.d_model, EPI_STORE_F32, false, w.qkv, qkv_w)), st);
+                rope_kv(w.qkv, w.q, kvl, dev(tpos), dev(tslot), kv->page_table, m->rope_cs, T, nullptr, d.n_heads,
+                        d.n_kv_heads, d.head_dim, kv->max_pages, B, st);
+            }
             if (use_tc) {
                 ta.layer_row0 = static_cast<int>(l * kv->layer_stride / d.head_dim);
                 attn_prefill_tc(tm_q, kv->tm_kv, w.attn, ta, n_tiles128, d.head_dim, st);

@@ -408,6 +408,70 @@ __global__ void __launch_bounds__(kThreads, 1)
                             }
                         }
                     }
+                } else if constexpr (MODE == EPI_QKV_ROPE) {
+                    // prefill QKV projection with RoPE and the paged-KV write fused (the rope_kv
+                    // pass over an fp32 QKV buffer it replaces): the tile's BN columns are whole
+                    // heads; this thread's row is one token.  Same formula and rounding points as
+                    // rope_kv_kernel: fp32 rotate-half, one bf16 rounding.
+                    const int t = m0 + row;
+                    const bool live = t < n_live;
+                    int pos = 0;
+                    long long kv_off = 0;
+                    if (live) {
+                        pos = fx.pos[t];
+                        const int page = fx.page_table[static_cast<long long>(fx.slot[t]) * fx.max_pages +
+                                                       pos / fx.page_tokens];
+                        kv_off = static_cast<long long>(page) * fx.page_stride +
+                                 static_cast<long long>(pos % fx.page_tokens) * fx.hd;
+                    }
+                    const int hd = fx.hd, half = hd >> 1;
+                    const long long head_stride = static_cast<long long>(fx.page_tokens) * hd;
+                    for (int col0 = 0; col0 < BN; col0 += hd) {
+                        const int h = (n0 + col0) / hd;
+                        // one head: hd / 32 chunks; pair i is (i, i + half) = chunk c, lane-column j
+                        // with chunk c + hd / 64
+                        for (int c = 0; c < hd / 64; ++c) {
+                            uint32_t u[32];
+                            tmem_ld32(tb + col0 + c * 32, r);
+                            tmem_ld32(tb + col0 + half + c * 32, u);
+                            tmem_ld_wait();
+                            if (col0 + hd == BN && c == hd / 64 - 1) release_acc(a);
+                            if (!live) continue;
+                            uint32_t pa[16], pb[16];
+                            if (h < fx.H + fx.Hkv) {
+                                const float2* cs = fx.rope_cs + static_cast<long long>(pos) * half + c * 32;
+#pragma unroll
+                                for (int j = 0; j < 32; j += 2) {
+                                    const float2 c0 = cs[j], c1 = cs[j + 1];
+                                    const float a0 = __uint_as_float(r[j]), b0 = __uint_as_float(u[j]);
+                                    const float a1 = __uint_as_float(r[j + 1]), b1 = __uint_as_float(u[j + 1]);
+                                    pa[j / 2] = pack_bf2(a0 * c0.x - b0 * c0.y, a1 * c1.x - b1 * c1.y);
+                                    pb[j / 2] = pack_bf2(b0 * c0.x + a0 * c0.y, b1 * c1.x + a1 * c1.y);
+                                }
+                            } else {
+#pragma unroll
+                                for (int j = 0; j < 32; j += 2) {
+                                    pa[j / 2] = pack_bf2(__uint_as_float(r[j]), __uint_as_float(r[j + 1]));
+                                    pb[j / 2] = pack_bf2(__uint_as_float(u[j]), __uint_as_float(u[j + 1]));
+                                }
+                            }
+                            __nv_bfloat16* dst;
+                            if (h < fx.H) {
+                                dst = fx.q_out + static_cast<long long>(t) * fx.H * hd + static_cast<long long>(h) * hd;
+                            } else if (h < fx.H + fx.Hkv) {
+                                dst = fx.kv_layer + kv_off + (h - fx.H) * head_stride;
+                            } else {
+                                dst = fx.kv_layer + kv_off + fx.page_stride / 2 + (h - fx.H - fx.Hkv) * head_stride;
+                            }
+                            uint4* da = reinterpret_cast<uint4*>(dst + c * 32);
+                            uint4* db = reinterpret_cast<uint4*>(dst + half + c * 32);
+#pragma unroll
+                            for (int v = 0; v < 4; ++v) {
+                                da[v] = make_uint4(pa[4 * v], pa[4 * v + 1], pa[4 * v + 2], pa[4 * v + 3]);
+                                db[v] = make_uint4(pb[4 * v], pb[4 * v + 1], pb[4 * v + 2], pb[4 * v + 3]);
+                            }
+                        }
+                    }
                 } else if constexpr (MODE == EPI_RESID) {
                     for (int c = 0; c < BN; c += 32) {
                         float4 res_nxt[8];
@@ -726,6 +790,7 @@ void gemm_run(const GemmProblem& p, cudaStream_t st) {
             case EPI_RESID: dispatch_bn<false, EPI_RESID>(bn, ta, tb, a, ctas, st); break;
             case EPI_SWIGLU: dispatch_bn<false, EPI_SWIGLU>(bn, ta, tb, a, ctas, st); break;
             case EPI_STORE_F32: dispatch_bn<false, EPI_STORE_F32>(bn, ta, tb, a, ctas, st); break;
+            case EPI_QKV_ROPE: dispatch_bn<false, EPI_QKV_ROPE>(bn, ta, tb, a, ctas, st); break;
             default: throw_cuda("gemm: bad epilogue for normal mode", cudaErrorInvalidValue, __FILE__, __LINE__);
         }
     }
