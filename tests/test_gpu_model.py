@@ -174,12 +174,20 @@ def test_long_context_split_kv_and_split_k(shape):
         eng.close()
 
 
-# Llama-8B's attention geometry (head_dim 128, 4 query heads per kv head) at a
-# size the oracle runs in seconds: exercises the hd-128 instantiations of the
-# tcgen05 prefill attention (head pairs), the decode attention kernels and the
-# 128-wide epilogues that the 8B bench uses.
+# Llama-8B's attention geometry (head_dim 128, 4 query heads per kv head) and
+# Llama-1B's (head_dim 64) at a size the oracle runs in seconds: the tcgen05
+# prefill attention (head pairs), both decode-attention kernels (SW_ATTN_FLAT=0
+# forces the per-unit kernel, 1 the flat one; read once per process, hence a
+# child process) and the fused QKV/RoPE epilogue.
+DESCS = {
+    "hd128_g4": "n_layers=2, d_model=512, n_heads=8, n_kv_heads=2, head_dim=128, ffn_dim=1024, vocab=4096",
+    "hd64_g4": "n_layers=2, d_model=512, n_heads=8, n_kv_heads=2, head_dim=64, ffn_dim=1024, vocab=4096",
+}
+
+
+@pytest.mark.parametrize("shape", sorted(DESCS))
 @pytest.mark.parametrize("flat", ["0", "1"])
-def test_hd128_gqa4_prefill_and_decode(flat):
+def test_attention_geometries_prefill_and_decode(shape, flat):
     import subprocess
     import sys
     import textwrap
@@ -190,7 +198,7 @@ def test_hd128_gqa4_prefill_and_decode(flat):
         sys.path.insert(0, {repr(str(__import__('pathlib').Path(__file__).resolve().parents[1]))})
         from oracle import model as M
         from paper_2505_03763_b200 import runtime
-        d = M.Desc(n_layers=2, d_model=512, n_heads=8, n_kv_heads=2, head_dim=128, ffn_dim=1024, vocab=4096)
+        d = M.Desc({DESCS[shape]})
         eng = runtime.Engine(d, max_prefill_tokens=4096, max_decode_batch=8, n_pages=512, n_slots=8,
                              max_pages_per_slot=40, max_out=8)
         lens = [1, 127, 128, 129, 257, 600]
