@@ -365,21 +365,19 @@ __global__ void __launch_bounds__(NWARP * 32)
                     if ((lane & 3) == 0)
                         __stcg(reinterpret_cast<float2*>(a.part_ml + (slot * G + r) * 2), make_float2(m_run, l_tot));
                 }
-                __threadfence();
-                __syncwarp();
+                __syncwarp();  // every lane's partial stores happen-before lane 0's release below
                 const long long u0 = static_cast<long long>(pre[L.row]) * Hkv + static_cast<long long>(L.hk) * L.np;
                 const long long ca = warp_of(u0, W, NW), cb = warp_of(u0 + L.np - 1, W, NW);
                 unsigned last = 0;
                 if (lane == 0) {
-                    last = atomicAdd(a.counters + unit, 1u) == static_cast<unsigned>(cb - ca);
+                    last = atomic_add_acq_rel_gpu(a.counters + unit, 1u) == static_cast<unsigned>(cb - ca);
                     if (last) a.counters[unit] = 0u;
                 }
-                last = __shfl_sync(0xffffffffu, last, 0);
+                last = __shfl_sync(0xffffffffu, last, 0);  // lane 0's acquire, ordered to the warp
                 if (last) {
                     // merge the unit's partials in warp order (online rescale, one pass); each
                     // lane owns PER contiguous floats of the [G][HD] tile, loads for NB
                     // contributors in flight together
-                    __threadfence();
                     constexpr int PER = G * HD / 32;
                     static_assert(PER % 4 == 0, "vector merge");
                     const int e0 = lane * PER, g = e0 / HD;

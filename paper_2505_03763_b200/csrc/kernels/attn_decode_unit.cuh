@@ -277,17 +277,16 @@ __device__ __forceinline__ void decode_unit(const DecodeAttnArgs& a, const __nv_
         sync();  // cm/cl/co and s_pages are reused by the runner's next unit
         return;
     }
-    // ---- last split to arrive merges all splits in order
-    __threadfence();
+    // ---- last split to arrive merges all splits in order (the barrier orders every thread's
+    // partial stores before thread 0's release; its acquire reaches the others through the next one)
     sync();
     if (tid == 0) {
         unsigned* cnt = a.counters + static_cast<int64_t>(row) * a.Hkv + hk;
-        *s_last = atomicAdd(cnt, 1u) == static_cast<unsigned>(splits - 1);
+        *s_last = atomic_add_acq_rel_gpu(cnt, 1u) == static_cast<unsigned>(splits - 1);
         if (*s_last) *cnt = 0u;
     }
     sync();
     if (*s_last) {
-        __threadfence();
         const int64_t base = (static_cast<int64_t>(row) * a.Hkv + hk) * kPartSplits;
         for (int idx = tid; idx < G * HD; idx += 128) {
             const int g = idx / HD;

@@ -87,6 +87,15 @@ __device__ __forceinline__ float fast_exp2(float x) {
     return y;
 }
 
+// Split-merge arrival: the warp's partial-result stores (ordered to lane 0 by
+// __syncwarp) are released and the other contributors' acquired by one
+// acq_rel atomic -- no MEMBAR.GL + L1 invalidate (__threadfence) per partial.
+__device__ __forceinline__ unsigned atomic_add_acq_rel_gpu(unsigned* p, unsigned v) {
+    unsigned old;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+    return old;
+}
+
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
