@@ -57,11 +57,11 @@ constexpr int kMaxContrib = 8;  // stream-K: CTAs contributing to one tile (host
 // LEAN (prefill, BN = 128): ~105 KB of smem and 256 TMEM columns, so a decode
 // CTA (<= ~104 KB, <= 128 columns) fits on the same SM -- the co-resident
 // prefill the split executor launches while decode work exists.
-template <int BN, bool SWAP>
+template <int BN, bool SWAP, bool PAIR = false>
 struct GemmCfg {
     static constexpr bool kLean = !SWAP && BN == 128;
     static constexpr int kABytes = BM * BK * 2;
-    static constexpr int kBBytes = BN * BK * 2;
+    static constexpr int kBBytes = (PAIR ? BN / 2 : BN) * BK * 2;  // PAIR: this CTA's half of the N tile
     static constexpr int kStageBytes = kABytes + kBBytes;
     static constexpr int kBudget = kLean ? 96 * 1024 : 192 * 1024;
     static constexpr int kStagesRaw = kBudget / kStageBytes > 8 ? 8 : kBudget / kStageBytes;
@@ -122,10 +122,17 @@ struct SegIter {
     }
 };
 
-template <int BN, int MODE, bool SWAP>
+// PAIR (prefill, BN = 256): a CTA pair (cluster of 2) computes 256 x 256 tiles
+// with tcgen05.mma.cta_group::2 (M = 256): each CTA stages its 128 token rows
+// of A and its 128 feature rows of B (32 KB per stage instead of 48 KB for the
+// same FLOPs), both CTAs' TMA loads complete on the leader's full barrier, the
+// leader issues the MMAs and its commits arrive on both CTAs' barriers, and each
+// CTA's epilogue drains its own 128 accumulator rows.
+template <int BN, int MODE, bool SWAP, bool PAIR = false>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmArgs args) {
-    using C = GemmCfg<BN, SWAP>;
+    using C = GemmCfg<BN, SWAP, PAIR>;
+    static_assert(!PAIR || (!SWAP && BN == 256), "CTA pairs: prefill 256-wide tiles only");
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sA = smem;
@@ -146,12 +153,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
 
+    uint32_t rank = 0;  // PAIR: rank in the CTA pair (0 = leader)
+    if constexpr (PAIR) asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+    constexpr int BMe = PAIR ? 2 * BM : BM;  // token rows per tile
     Sched sc;
     sc.tiles_n = args.N / BN;
-    sc.tiles = cdiv(args.M, BM) * sc.tiles_n;
+    sc.tiles = cdiv(args.M, BMe) * sc.tiles_n;
     sc.nk = args.K / BK;
-    sc.C = gridDim.x;
-    sc.c = blockIdx.x;
+    sc.C = PAIR ? gridDim.x / 2 : gridDim.x;
+    sc.c = PAIR ? blockIdx.x / 2 : blockIdx.x;
     sc.stream_k = args.stream_k != 0;
     sc.I = static_cast<long long>(sc.tiles) * sc.nk;
 
@@ -162,20 +172,34 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&acc_full[a], 1);
-            mbar_init(&acc_empty[a], 4);  // one arrive per epilogue warp
+            mbar_init(&acc_empty[a], PAIR ? 8 : 4);  // one arrive per epilogue warp (of both CTAs: PAIR)
         }
         fence_mbar_init();
         tma_prefetch_desc(&tmA);
         tma_prefetch_desc(&tmB);
     }
     if (warp == 1) {
-        tmem_alloc(tmem_slot, C::kTmemCols);
-        tmem_relinquish();
+        if constexpr (PAIR) {
+            asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(tmem_slot)),
+                         "r"(static_cast<uint32_t>(C::kTmemCols)));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+        } else {
+            tmem_alloc(tmem_slot, C::kTmemCols);
+            tmem_relinquish();
+        }
     }
     tc_fence_before();
     __syncthreads();
+    if constexpr (PAIR)  // both CTAs' barriers exist before any remote arrive / multicast commit
+        asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    // PAIR: the leader's copy of a barrier (its shared::cluster address)
+    auto leader_bar = [&](uint64_t* b) {
+        uint32_t r = smem_addr(b);
+        if constexpr (PAIR) asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(r), "r"(0));
+        return r;
+    };
 
     if (warp == 2 || warp == 3) {
         // ------------------------------------------------------------ producers
@@ -187,8 +211,25 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint64_t pol_x = l2_policy_evict_last();
             auto coord = [&](const Seg& g, int& am, int& bn0) {
                 const int mt = g.tile / sc.tiles_n, nt = g.tile % sc.tiles_n;
-                am = mt * BM;
-                bn0 = nt * BN;
+                am = mt * BMe + static_cast<int>(rank) * BM;
+                bn0 = nt * BN + (PAIR ? static_cast<int>(rank) * (BN / 2) : 0);
+            };
+            // TMA into this CTA's smem, completing on `full[s]` (PAIR: the leader's)
+            auto load = [&](void* dst, const CUtensorMap* tm, int s, int x, int y, uint64_t pol) {
+                if constexpr (PAIR) {
+                    asm volatile(
+                        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+                        ".L2::cache_hint [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_addr(dst)),
+                        "l"(tm), "r"(leader_bar(&full[s])), "r"(x), "r"(y), "l"(pol)
+                        : "memory");
+                } else {
+                    tma_load_2d(dst, tm, &full[s], x, y, pol);
+                }
+            };
+            // the stage's expected bytes: PAIR -> both CTAs' loads, armed by the leader only
+            auto arm = [&](int s) {
+                if (!PAIR) mbar_expect_tx(&full[s], C::kStageBytes);
+                else if (rank == 0) mbar_expect_tx(&full[s], 2 * C::kStageBytes);
             };
             // Pass 1 (PDL): the first ring fill of the constant operand -- the
             // weights -- is issued before waiting on the predecessor kernel.
@@ -202,9 +243,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                     coord(g, am, bn0);
                     for (int kb = g.lo; kb < g.hi && gi < C::kStages; ++kb, ++gi) {
                         if (gi % kProducers != p) continue;
-                        mbar_expect_tx(&full[gi], C::kStageBytes);
-                        if (SWAP) tma_load_2d(sA + gi * C::kABytes, &tmA, &full[gi], kb * BK, am, pol_w);
-                        else tma_load_2d(sB + gi * C::kBBytes, &tmB, &full[gi], kb * BK, bn0, pol_w);
+                        arm(gi);
+                        if (SWAP) load(sA + gi * C::kABytes, &tmA, gi, kb * BK, am, pol_w);
+                        else load(sB + gi * C::kBBytes, &tmB, gi, kb * BK, bn0, pol_w);
                     }
                 }
             }
@@ -220,22 +261,32 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (gi % kProducers != p) continue;
                     const int s = gi % C::kStages;
                     if (gi < C::kStages) {  // weights already in flight: the activation half
-                        if (SWAP) tma_load_2d(sB + s * C::kBBytes, &tmB, &full[s], kb * BK, bn0, pol_x);
-                        else tma_load_2d(sA + s * C::kABytes, &tmA, &full[s], kb * BK, am, pol_x);
+                        if (SWAP) load(sB + s * C::kBBytes, &tmB, s, kb * BK, bn0, pol_x);
+                        else load(sA + s * C::kABytes, &tmA, s, kb * BK, am, pol_x);
                         continue;
                     }
                     mbar_wait(&empty[s], ((gi / C::kStages) & 1) ^ 1);
-                    mbar_expect_tx(&full[s], C::kStageBytes);
-                    tma_load_2d(sA + s * C::kABytes, &tmA, &full[s], kb * BK, am, SWAP ? pol_w : pol_x);
-                    tma_load_2d(sB + s * C::kBBytes, &tmB, &full[s], kb * BK, bn0, SWAP ? pol_x : pol_w);
+                    arm(s);
+                    load(sA + s * C::kABytes, &tmA, s, kb * BK, am, SWAP ? pol_w : pol_x);
+                    load(sB + s * C::kBBytes, &tmB, s, kb * BK, bn0, SWAP ? pol_x : pol_w);
                 }
             }
         }
         __syncwarp();
     } else if (warp == 1) {
         // ------------------------------------------------------------ MMA issuer
-        if (lane == 0) {
-            constexpr uint32_t idesc = umma_idesc_bf16(BM, BN);
+        if (lane == 0 && rank == 0) {
+            constexpr uint32_t idesc = umma_idesc_bf16(BMe, BN);
+            auto commit = [&](uint64_t* b) {  // PAIR: arrive on this barrier in both CTAs
+                if constexpr (PAIR)
+                    asm volatile(
+                        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 "
+                        "[%0], %1;" ::"r"(smem_addr(b)),
+                        "h"(static_cast<uint16_t>(3))
+                        : "memory");
+                else
+                    umma_commit(b);
+            };
             SegIter it;
             it.init(sc);
             Seg g;
@@ -252,12 +303,20 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const uint32_t a0 = smem_addr(sA + s * C::kABytes);
                     const uint32_t b0 = smem_addr(sB + s * C::kBBytes);
 #pragma unroll
-                    for (int k = 0; k < BK / 16; ++k)
-                        umma_bf16(acc, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32), idesc,
-                                  (kb > g.lo || k > 0) ? 1u : 0u);
-                    umma_commit(&empty[s]);
+                    for (int k = 0; k < BK / 16; ++k) {
+                        if constexpr (PAIR)
+                            asm volatile(
+                                "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                                "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(acc),
+                                "l"(umma_desc_sw128(a0 + k * 32)), "l"(umma_desc_sw128(b0 + k * 32)), "r"(idesc),
+                                "r"((kb > g.lo || k > 0) ? 1u : 0u));
+                        else
+                            umma_bf16(acc, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32), idesc,
+                                      (kb > g.lo || k > 0) ? 1u : 0u);
+                    }
+                    commit(&empty[s]);
                 }
-                umma_commit(&acc_full[a]);
+                commit(&acc_full[a]);
                 ++si;
             }
         }
@@ -343,7 +402,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             tmem_ld_wait();
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&acc_empty[a]);
+            if (lane == 0) {
+                if constexpr (PAIR)  // the leader's MMA warp waits on its own copy
+                    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(
+                                     leader_bar(&acc_empty[a]))
+                                 : "memory");
+                else
+                    mbar_arrive(&acc_empty[a]);
+            }
         };
 
         SegIter it;
@@ -354,7 +420,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         while (it.next(sc, g)) {
             const int a = si & 1;
             const int mt = g.tile / sc.tiles_n, nt = g.tile % sc.tiles_n;
-            const int m0 = mt * BM, n0 = nt * BN;
+            const int m0 = mt * BMe + static_cast<int>(rank) * BM, n0 = nt * BN;
             // prefill residual add: the residual row's first 32 columns load while the tile's MMAs
             // still run, and every later chunk's load is in flight one chunk ahead (the epilogue
             // was a chain of 8 dependent round trips per tile: wo ran at 26% tensor-pipe)
@@ -587,7 +653,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 1) {
+    if constexpr (PAIR) {  // both CTAs done: no remote arrive or multicast commit is still in flight
+        asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+        if (warp == 1) {
+            tc_fence_after();
+            asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                         "r"(static_cast<uint32_t>(C::kTmemCols)));
+        }
+    } else if (warp == 1) {
         tc_fence_after();
         tmem_dealloc(tmem, C::kTmemCols);
     }
@@ -634,6 +707,38 @@ void launch_one(const CUtensorMap& a, const CUtensorMap& b, const GemmArgs& args
         configured = true;
     }
     launch_k(gemm_tc_kernel<BN, MODE, SWAP>, dim3(ctas), dim3(kThreads), C::kSmem, st, a, b, args);
+}
+
+// CTA-pair prefill GEMM (BN = 256): clusters of 2, one pair per two SMs.
+template <int MODE>
+void launch_pair(const CUtensorMap& a, const CUtensorMap& b, const GemmArgs& args, int pairs, cudaStream_t st) {
+    using C = GemmCfg<256, false, true>;
+    static bool configured = false;
+    if (!configured) {
+        SW_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<256, MODE, false, true>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
+        configured = true;
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(2 * pairs);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = C::kSmem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    int na = 1;
+    if (pdl_mode() && pdl_allowed()) {
+        attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[1].val.programmaticStreamSerializationAllowed = 1;
+        na = 2;
+    }
+    cfg.attrs = attr;
+    cfg.numAttrs = na;
+    SW_CUDA(cudaLaunchKernelEx(&cfg, gemm_tc_kernel<256, MODE, false, true>, a, b, args));
+    count_launches(1);
 }
 
 template <bool SWAP, int MODE>
@@ -780,6 +885,22 @@ void gemm_run(const GemmProblem& p, cudaStream_t st) {
         a.M = p.tokens;
         a.N = p.features;
         a.stream_k = 0;
+        // CTA pairs (tcgen05 cta_group::2, 256 x 256 tiles): SW_GEMM_PAIR=1 (default) for 256-wide tiles
+        static const int pair_env = env_flag("SW_GEMM_PAIR", 1);
+        if (pair_env && bn == 256 && p.yield_tiles == 0 && grid_sms >= 2) {
+            const int tiles2 = cdiv(p.tokens, 2 * BM) * (p.features / 256);
+            const int pairs = std::min(grid_sms / 2, tiles2);
+            const CUtensorMap& ta = tmap_cached(p.X, p.x_rows, p.K, BM);
+            const CUtensorMap& tb = tmap_cached(p.W, p.w_rows, p.K, 128);
+            switch (p.mode) {
+                case EPI_STORE: launch_pair<EPI_STORE>(ta, tb, a, pairs, st); return;
+                case EPI_RESID: launch_pair<EPI_RESID>(ta, tb, a, pairs, st); return;
+                case EPI_SWIGLU: launch_pair<EPI_SWIGLU>(ta, tb, a, pairs, st); return;
+                case EPI_STORE_F32: launch_pair<EPI_STORE_F32>(ta, tb, a, pairs, st); return;
+                case EPI_QKV_ROPE: launch_pair<EPI_QKV_ROPE>(ta, tb, a, pairs, st); return;
+                default: break;
+            }
+        }
         const int tiles = cdiv(p.tokens, BM) * (p.features / bn);
         int ctas = std::min(grid_sms, tiles);
         if (p.yield_tiles > 0) ctas = std::max(ctas, cdiv(tiles, p.yield_tiles));  // round robin over more CTAs
