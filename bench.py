@@ -203,7 +203,7 @@ def roofline_decode_gemm(eng, desc, rows: int, peaks, reps: int = 20):
 
 
 def roofline_prefill_gemm(eng, desc, tokens: int, peaks, reps: int = 10):
-    """Prefill gate/up projection (normal-mode tcgen05 GEMM + SwiGLU), tensor-bound."""
+    """Prefill gate/up projection (normal-mode tcgen05 GEMM on CTA pairs + SwiGLU), tensor-bound."""
     import ctypes
     import torch
     import paper_2505_03763_b200 as sw
@@ -222,7 +222,8 @@ def roofline_prefill_gemm(eng, desc, tokens: int, peaks, reps: int = 10):
     flops = 2.0 * tokens * 2 * F * d
     achieved = flops / t / 1e12
     peak = float(peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"]))
-    return {"kernel": "gemm_tc_kernel<256,SWIGLU,normal> (prefill gate/up, tokens=%d)" % tokens, "bound": "tensor",
+    return {"kernel": "gemm_tc_kernel<256,SWIGLU,normal,pair> (prefill gate/up, CTA-pair cta_group::2, tokens=%d)" % tokens,
+            "bound": "tensor",
             "achieved": round(achieved, 1), "peak": peak, "unit": "TFLOP/s", "frac": round(achieved / peak, 4),
             "us_per_launch": round(t * 1e6, 1)}
 
