@@ -302,7 +302,7 @@ void prefill_forward(sw_model* m, sw_kv* kv, const sw_batch& b, cudaStream_t st,
             const char* v = std::getenv("SW_PREFILL_ROPE_FUSED");
             return v && *v ? std::atoi(v) : 1;
         }();
-        const bool fuse_rope = fuse_env != 0 && !lean;
+        const bool fuse_rope = fuse_env != 0;
         PrefillTcArgs ta{};
         CUtensorMap tm_q{};
         if (use_tc) {

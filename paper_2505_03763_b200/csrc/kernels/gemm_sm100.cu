@@ -57,9 +57,10 @@ constexpr int kMaxContrib = 8;  // stream-K: CTAs contributing to one tile (host
 // LEAN (prefill, BN = 128): ~105 KB of smem and 256 TMEM columns, so a decode
 // CTA (<= ~104 KB, <= 128 columns) fits on the same SM -- the co-resident
 // prefill the split executor launches while decode work exists.
-template <int BN, bool SWAP, bool PAIR = false>
+template <int BN, bool SWAP, bool PAIR = false, bool LEANP = false>
 struct GemmCfg {
-    static constexpr bool kLean = !SWAP && BN == 128;
+    // lean: ~100 KB of smem (and, for pairs, one 256-column accumulator) so a decode CTA fits beside
+    static constexpr bool kLean = (!SWAP && BN == 128) || LEANP;
     static constexpr int kABytes = BM * BK * 2;
     static constexpr int kBBytes = (PAIR ? BN / 2 : BN) * BK * 2;  // PAIR: this CTA's half of the N tile
     static constexpr int kStageBytes = kABytes + kBBytes;
@@ -67,7 +68,8 @@ struct GemmCfg {
     static constexpr int kStagesRaw = kBudget / kStageBytes > 8 ? 8 : kBudget / kStageBytes;
     static constexpr int kStages = kLean ? kStagesRaw : (kStagesRaw & ~1);
     static_assert(kStages >= (kLean ? 3 : 4), "stage ring too shallow");
-    static constexpr int kTmemCols = 2 * BN < 64 ? 64 : 2 * BN;  // two accumulators
+    static constexpr int kAccs = LEANP ? 1 : 2;  // TMEM accumulators (double-buffered unless lean pair)
+    static constexpr int kTmemCols = kAccs * BN < 64 ? 64 : kAccs * BN;
     static constexpr int kXchgBytes = SWAP ? 128 * 33 * 4 : 0;
     static constexpr int kTokBytes = 256 * 24;  // tok_inv, tok_pos, tok_kv, best
     static constexpr int kBarBytes = 512;
@@ -128,10 +130,11 @@ struct SegIter {
 // same FLOPs), both CTAs' TMA loads complete on the leader's full barrier, the
 // leader issues the MMAs and its commits arrive on both CTAs' barriers, and each
 // CTA's epilogue drains its own 128 accumulator rows.
-template <int BN, int MODE, bool SWAP, bool PAIR = false>
+template <int BN, int MODE, bool SWAP, bool PAIR = false, bool LEANP = false>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmArgs args) {
-    using C = GemmCfg<BN, SWAP, PAIR>;
+    using C = GemmCfg<BN, SWAP, PAIR, LEANP>;
+    static_assert(!LEANP || PAIR, "lean accumulators: pair kernel only");
     static_assert(!PAIR || (!SWAP && BN == 256), "CTA pairs: prefill 256-wide tiles only");
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -292,8 +295,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             Seg g;
             int gi = 0, si = 0;
             while (it.next(sc, g)) {
-                const int a = si & 1;
-                mbar_wait(&acc_empty[a], ((si >> 1) & 1) ^ 1);
+                const int a = si % C::kAccs;
+                mbar_wait(&acc_empty[a], ((si / C::kAccs) & 1) ^ 1);
                 tc_fence_after();
                 const uint32_t acc = tmem + a * BN;
                 for (int kb = g.lo; kb < g.hi; ++kb, ++gi) {
@@ -418,7 +421,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         int si = 0;
         uint32_t r[32];
         while (it.next(sc, g)) {
-            const int a = si & 1;
+            const int a = si % C::kAccs;
             const int mt = g.tile / sc.tiles_n, nt = g.tile % sc.tiles_n;
             const int m0 = mt * BMe + static_cast<int>(rank) * BM, n0 = nt * BN;
             // prefill residual add: the residual row's first 32 columns load while the tile's MMAs
@@ -437,7 +440,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     for (int q = 0; q < 8; ++q) res_cur[q] = __ldcg(res_row + q);
                 }
             }
-            mbar_wait(&acc_full[a], (si >> 1) & 1);
+            mbar_wait(&acc_full[a], (si / C::kAccs) & 1);
             tc_fence_after();
             ++si;
             const uint32_t tb = tmem + a * BN + (static_cast<uint32_t>(quarter * 32) << 16);
@@ -710,12 +713,12 @@ void launch_one(const CUtensorMap& a, const CUtensorMap& b, const GemmArgs& args
 }
 
 // CTA-pair prefill GEMM (BN = 256): clusters of 2, one pair per two SMs.
-template <int MODE>
+template <int MODE, bool LEANP = false>
 void launch_pair(const CUtensorMap& a, const CUtensorMap& b, const GemmArgs& args, int pairs, cudaStream_t st) {
-    using C = GemmCfg<256, false, true>;
+    using C = GemmCfg<256, false, true, LEANP>;
     static bool configured = false;
     if (!configured) {
-        SW_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<256, MODE, false, true>,
+        SW_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<256, MODE, false, true, LEANP>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
         configured = true;
     }
@@ -737,7 +740,7 @@ void launch_pair(const CUtensorMap& a, const CUtensorMap& b, const GemmArgs& arg
     }
     cfg.attrs = attr;
     cfg.numAttrs = na;
-    SW_CUDA(cudaLaunchKernelEx(&cfg, gemm_tc_kernel<256, MODE, false, true>, a, b, args));
+    SW_CUDA(cudaLaunchKernelEx(&cfg, gemm_tc_kernel<256, MODE, false, true, LEANP>, a, b, args));
     count_launches(1);
 }
 
@@ -887,11 +890,21 @@ void gemm_run(const GemmProblem& p, cudaStream_t st) {
         a.stream_k = 0;
         // CTA pairs (tcgen05 cta_group::2, 256 x 256 tiles): SW_GEMM_PAIR=1 (default) for 256-wide tiles
         static const int pair_env = env_flag("SW_GEMM_PAIR", 1);
-        if (pair_env && bn == 256 && p.yield_tiles == 0 && grid_sms >= 2) {
+        if (pair_env && (bn == 256 || p.lean) && p.yield_tiles == 0 && grid_sms >= 2) {
             const int tiles2 = cdiv(p.tokens, 2 * BM) * (p.features / 256);
             const int pairs = std::min(grid_sms / 2, tiles2);
             const CUtensorMap& ta = tmap_cached(p.X, p.x_rows, p.K, BM);
             const CUtensorMap& tb = tmap_cached(p.W, p.w_rows, p.K, 128);
+            if (p.lean) {  // co-resident with decode CTAs: 3 stages, one accumulator
+                switch (p.mode) {
+                    case EPI_STORE: launch_pair<EPI_STORE, true>(ta, tb, a, pairs, st); return;
+                    case EPI_RESID: launch_pair<EPI_RESID, true>(ta, tb, a, pairs, st); return;
+                    case EPI_SWIGLU: launch_pair<EPI_SWIGLU, true>(ta, tb, a, pairs, st); return;
+                    case EPI_STORE_F32: launch_pair<EPI_STORE_F32, true>(ta, tb, a, pairs, st); return;
+                    case EPI_QKV_ROPE: launch_pair<EPI_QKV_ROPE, true>(ta, tb, a, pairs, st); return;
+                    default: break;
+                }
+            }
             switch (p.mode) {
                 case EPI_STORE: launch_pair<EPI_STORE>(ta, tb, a, pairs, st); return;
                 case EPI_RESID: launch_pair<EPI_RESID>(ta, tb, a, pairs, st); return;

@@ -35,6 +35,8 @@ RUNS = {
     "pipelined_P2_yield1": "policy=pipelined_splitwiser;P=2;max_batch=4;engine.split=1;engine.prefill_yield=1",
     "pipelined_P2_prefill_priority": "policy=pipelined_splitwiser;P=2;max_batch=4;engine.split=1;"
                                      "engine.prefill_priority=1",
+    # prompts launched while decode work exists on lean CTA-pair GEMMs (co-resident with decode CTAs)
+    "pipelined_P2_lean": "policy=pipelined_splitwiser;P=2;max_batch=4;engine.split=1;engine.lean_prefill=1",
 }
 
 
