@@ -208,9 +208,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         // ------------------------------------------------------------ producers
         if (lane == 0) {
             const int p = warp - 2;
-            // weights stream once per launch (evict first); activations are
-            // re-read by every tile (evict last)
-            const uint64_t pol_w = l2_policy_evict_first();
+            // decode (swap): weights stream once per launch (evict first), activations are re-read by
+            // every tile (evict last).  Prefill: the weight panels are re-read by every token tile
+            // too -- evict first sent them back to HBM between tiles (the gate/up GEMM read 3.4 GB
+            // from HBM for 134 MB of operands)
+            const uint64_t pol_w = SWAP ? l2_policy_evict_first() : l2_policy_evict_last();
             const uint64_t pol_x = l2_policy_evict_last();
             auto coord = [&](const Seg& g, int& am, int& bn0) {
                 const int mt = g.tile / sc.tiles_n, nt = g.tile % sc.tiles_n;
