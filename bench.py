@@ -323,10 +323,9 @@ def main():
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    from oracle import model as M  # shapes only (Desc constants)
-    from paper_2505_03763_b200 import runtime
+    from paper_2505_03763_b200 import runtime, shapes
 
-    desc = getattr(M, w["model"])
+    desc = getattr(shapes, w["model"])
     n_local = w["n"]
     in_max = int(str(w["input"]).split("..")[-1])
     pages_per = (in_max + w["output"] + 15) // 16

@@ -1,0 +1,124 @@
+"""The `splitsim`-shaped CLI front end (paper_2505_03763_b200/cli.py).
+
+* the reference's JSON configs map onto run specs whose experiment files are
+  byte-identical to the reference writer's (oracle/_ref/refwrite) -- for the
+  shipped configs when /root/reference is present, and for inline configs;
+* --set overrides, sweep directories + sweep.csv, replay, exit codes 2/3;
+* GPU: the same config through the B200 engine (`--backend gpu`).
+"""
+import json
+import os
+import subprocess
+
+import pytest
+
+from conftest import ROOT
+from paper_2505_03763_b200 import cli
+
+REFWRITE = os.path.join(ROOT, "oracle", "_ref", "refwrite")
+REF_CONFIGS = "/root/reference/proj/configs"
+FILES = ("report.json", "requests.csv", "timeseries.csv", "events.csv")
+
+INLINE = {
+    "workload": {"n_requests": 24, "input_tokens": [64, 400], "output_tokens": [2, 20],
+                 "arrival": {"poisson_rate_per_s": 300.0}, "seed": 5},
+    "scheduler": {"policy": "mixed_batching", "max_batch": 8},
+    "cost": {"kv_handoff_s": 0.0005},
+    "output_dir": "unused",
+}
+
+
+def _read(d, f):
+    with open(os.path.join(d, f)) as fh:
+        return fh.read()
+
+
+def _check_against_reference(cfg, out):
+    if not os.path.exists(REFWRITE):
+        pytest.skip("oracle/_ref/refwrite not built")
+    spec = ";".join(kv for kv in cli.config_to_spec(cfg).split(";")
+                    if not kv.startswith(("output_dir=", "emit_event_log=")))
+    ref = str(out) + "_ref"
+    assert subprocess.run([REFWRITE, "--write", ref, spec], capture_output=True).returncode == 0
+    for f in FILES:
+        assert _read(out, f) == _read(ref, f), f
+
+
+def _run(tmp_path, cfg, *extra):
+    path = tmp_path / "cfg.json"
+    path.write_text(json.dumps(cfg))
+    out = tmp_path / "out"
+    code = cli.main(["run", "-c", str(path), "--output-dir", str(out), "--emit-events", *extra])
+    return code, out
+
+
+def test_inline_config_files_match_reference(tmp_path, capsys):
+    code, out = _run(tmp_path, INLINE)
+    assert code == 0
+    assert capsys.readouterr().out.startswith("makespan_s=")
+    cfg = dict(INLINE, output_dir=str(out), emit_event_log=True)
+    _check_against_reference(cfg, out)
+
+
+@pytest.mark.parametrize("name", ["hf_sequential", "hf_splitwiser", "vllm_sp", "vllm_mpsx2", "vllm_mpx2"])
+def test_shipped_configs_match_reference(tmp_path, name):
+    p = os.path.join(REF_CONFIGS, name + ".json")
+    if not os.path.exists(p):
+        pytest.skip("reference configs not present")
+    with open(p) as f:
+        cfg = json.load(f)
+    if cfg.get("discipline", {}).get("mode") == "time_sliced":
+        with pytest.raises(cli.ConfigError):
+            cli.config_to_spec(cfg)
+        return
+    if cfg["workload"].get("n_requests", 0) * cfg["workload"].get("output_tokens", 1) > 40000:
+        cfg["workload"]["n_requests"] = 16  # keep the CPU suite fast
+    code, out = _run(tmp_path, cfg)
+    assert code == 0
+    _check_against_reference(dict(cfg, output_dir=str(out), emit_event_log=True), out)
+
+
+def test_set_override_and_replay(tmp_path, capsys):
+    code, out = _run(tmp_path, INLINE, "--set", "scheduler.max_batch=2", "--set", "kv.shared=1")
+    assert code == 0
+    line = capsys.readouterr().out.strip()
+    assert cli.main(["replay", str(out / "events.csv")]) == 0
+    assert capsys.readouterr().out.strip() == line
+    assert _read(out, "replay_report.json") == _read(out, "report.json")
+
+
+def test_sweep_dirs_and_csv(tmp_path):
+    sweep = {"base": dict(INLINE, output_dir=str(tmp_path / "sw")), "axis": "workload.n_requests",
+             "values": [4, 12]}
+    p = tmp_path / "sweep.json"
+    p.write_text(json.dumps(sweep))
+    assert cli.main(["sweep", "-c", str(p)]) == 0
+    rows = _read(tmp_path / "sw", "sweep.csv").splitlines()
+    assert rows[0].startswith("value,status,makespan_s,tokens_per_s")
+    assert [r.split(",")[:2] for r in rows[1:]] == [["4", "ok"], ["12", "ok"]]
+    for v in ("4", "12"):
+        assert json.loads(_read(tmp_path / "sw" / v, "report.json"))["n_requests"] == int(v)
+
+
+def test_exit_codes(tmp_path):
+    bad = dict(INLINE, bogus=1)
+    p = tmp_path / "bad.json"
+    p.write_text(json.dumps(bad))
+    assert cli.main(["run", "-c", str(p)]) == 2
+    assert cli.main(["run", "-c", str(tmp_path / "missing.json")]) == 3
+    too_big = dict(INLINE, gpu={"kv_capacity_blocks": 3})
+    p.write_text(json.dumps(too_big))
+    assert cli.main(["run", "-c", str(p), "--output-dir", str(tmp_path / "o")]) == 4
+
+
+@pytest.mark.gpu
+def test_gpu_backend_run(tmp_path, capsys):
+    cfg = {"workload": {"n_requests": 8, "input_tokens": 64, "output_tokens": 8, "arrival": "all_at_zero"},
+           "scheduler": {"policy": "pipelined_splitwiser", "P": 2, "max_batch": 4},
+           "discipline": {"mode": "mps_concurrent"}, "engine": {"engine.split": 1}}
+    code, out = _run(tmp_path, cfg, "--backend", "gpu", "--model", "TINY")
+    assert code == 0
+    rep = json.loads(_read(out, "report.json"))
+    assert rep["total_output_tokens"] == 64
+    assert cli.main(["replay", str(out / "events.csv")]) == 0
+    assert _read(out, "replay_report.json") == _read(out, "report.json")
