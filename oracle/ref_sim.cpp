@@ -17,6 +17,8 @@
 // the event log); `refwrite --replay events.csv` writes replay_report.json as
 // the reference CLI's replay does (tools/splitsim.cpp:73-85).
 #include <cmath>
+#include <fstream>
+#include <sstream>
 #include <cstdio>
 #include <cstdlib>
 #include <iostream>
@@ -119,6 +121,7 @@ int main(int argc, char** argv) {
         SimulationInputs in;
         double budget = 22016.0, block_unit = 1.0;
         long long pinned = 0;
+        std::string trace_path;
         for (auto& [k, v] : m) {
             if (k == "n") w.n_requests = std::stoi(v);
             else if (k == "input") w.input_tokens = range_of(v);
@@ -155,10 +158,19 @@ int main(int argc, char** argv) {
             else if (k == "cost.prompt_overhead_s") in.cost.prompt_overhead_s = std::stod(v);
             else if (k == "cost.step_overhead_s") in.cost.step_overhead_s = std::stod(v);
             else if (k == "cost.kv_handoff_s") in.cost.kv_handoff_s = std::stod(v);
+            else if (k == "trace") trace_path = v;
             else throw ConfigError("unknown key " + k);
         }
         validate(sc);
-        in.requests = generate(w);
+        if (!trace_path.empty()) {  // config.hpp assemble: parse_trace (request.hpp:134-183)
+            std::ifstream f(trace_path);
+            if (!f) throw ConfigError("workload.trace: cannot open '" + trace_path + "'");
+            std::stringstream ss;
+            ss << f.rdbuf();
+            in.requests = parse_trace(ss.str());
+        } else {
+            in.requests = generate(w);
+        }
         // derive_kv_capacity (config.hpp:66-79), restated to avoid the json dependency.
         int n_inst = sc.policy == PolicyKind::PipelinedSplitwiser ? sc.splitwiser_processes
                      : sc.policy == PolicyKind::MultiInstance     ? sc.n_instances
@@ -213,6 +225,9 @@ int main(int argc, char** argv) {
         return 0;
     } catch (const ConfigError& e) {
         std::fprintf(stderr, "ConfigError: %s\n", e.what());
+        return 2;
+    } catch (const ParseError& e) {  // exit 2 like the reference CLI (tools/splitsim.cpp:124-139)
+        std::fprintf(stderr, "ParseError: %s\n", e.what());
         return 2;
     } catch (const ContractViolation& e) {
         std::fprintf(stderr, "ContractViolation: %s\n", e.what());

@@ -70,10 +70,13 @@ def config_to_spec(cfg: dict) -> str:
     w = cfg.get("workload")
     if w is None:
         raise ConfigError(-2, "workload: required")
-    if "trace" in w:
-        raise ConfigError(-2, "workload.trace: trace replay is not supported by this front end")
+    if "trace" in w:  # the workload from a trace CSV (config.hpp assemble)
+        _expect(w, "workload", {"trace"})
+        kv["trace"] = w["trace"]
+        w = {}
     _expect(w, "workload", {"n_requests", "input_tokens", "output_tokens", "arrival", "seed"})
-    kv["n"] = str(w.get("n_requests", 0))
+    if "trace" not in kv:
+        kv["n"] = str(w.get("n_requests", 0))
     if "input_tokens" in w:
         kv["input"] = _range(w["input_tokens"], "workload.input_tokens")
     if "output_tokens" in w:

@@ -8,12 +8,14 @@
 //   seed, policy, max_batch, P, n_instances, inner, mode, kv_capacity_blocks,
 //   block_tokens, compute_capacity, mem_bandwidth, weight_mem_units,
 //   shared_weights, mem_budget_units, block_mem_unit, cost.* (a_p ... kv_handoff_s).
-// New keys: kv.shared (one KV quota for all instances, executor.hpp), output_dir /
+// New keys: trace=<csv> (the reference's workload.trace), kv.shared (one KV quota for all instances, executor.hpp), output_dir /
 // emit_event_log (experiment files, experiment_files.hpp), engine.* (GPU executor).
 // Unknown keys are a ConfigError naming the key (config.hpp:83-91 behaviour).
 #pragma once
 
 #include <cmath>
+#include <fstream>
+#include <sstream>
 #include <map>
 #include <string>
 
@@ -66,6 +68,7 @@ struct RunSpec {
     long long kv_capacity_override = 0;  // 0 = derive
     int shard_index = 0, shard_count = 1;  // request sharding across replicas (GPUs)
     SpecMap rest;                        // backend-specific keys (engine.*, model.*)
+    std::string trace_path;              // workload from a trace CSV instead of the generator (config.hpp assemble)
     std::string output_dir;              // non-empty: write the experiment files there (experiment_files.hpp)
     bool emit_event_log = false;         // ... including events.csv
 };
@@ -161,14 +164,22 @@ inline RunSpec build_spec(const SpecMap& m) {
             if (s.shard_count < 1 || s.shard_index < 0 || s.shard_index >= s.shard_count)
                 throw ConfigError("shard: index must be in [0, count)");
         } else if (k.rfind("engine.", 0) == 0 || k.rfind("model.", 0) == 0) s.rest[k] = v;
-        else if (k == "trace") s.rest[k] = v;
+        else if (k == "trace") s.trace_path = v;
         else if (k == "output_dir") s.output_dir = v;  // ExperimentConfig::output_dir (config.hpp:44)
         else if (k == "emit_event_log") s.emit_event_log = v == "1" || v == "true";
         else throw ConfigError("spec: unknown key '" + k + "'");
         have_ws = have_ws || k == "n";
     }
     validate(s.scheduler);
-    s.inputs.requests = generate(s.workload);
+    if (!s.trace_path.empty()) {  // config.hpp assemble: the trace replaces the generated workload
+        std::ifstream f(s.trace_path);
+        if (!f) throw ConfigError("workload.trace: cannot open '" + s.trace_path + "'");
+        std::stringstream ss;
+        ss << f.rdbuf();
+        s.inputs.requests = parse_trace(ss.str());
+    } else {
+        s.inputs.requests = generate(s.workload);
+    }
     if (s.shard_count > 1) {
         // one replica's share of the trace: round robin by arrival order, the
         // reference's multi_instance_split rule (schedulers.hpp:86-92); ids stay global

@@ -122,3 +122,13 @@ def test_gpu_backend_run(tmp_path, capsys):
     assert rep["total_output_tokens"] == 64
     assert cli.main(["replay", str(out / "events.csv")]) == 0
     assert _read(out, "replay_report.json") == _read(out, "report.json")
+
+
+def test_trace_workload_config(tmp_path):
+    trace = tmp_path / "trace.csv"
+    trace.write_text("id,arrival_s,input_tokens,output_tokens\n0,0.0,100,5\n1,0.001,300,9\n2,0.001,50,2\n")
+    cfg = {"workload": {"trace": str(trace)}, "scheduler": {"policy": "mixed_batching"}}
+    code, out = _run(tmp_path, cfg)
+    assert code == 0
+    assert json.loads(_read(out, "report.json"))["n_requests"] == 3
+    _check_against_reference(dict(cfg, output_dir=str(out), emit_event_log=True), out)

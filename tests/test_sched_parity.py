@@ -89,3 +89,30 @@ def test_capacity_and_contract_errors_match(swlib):
     _compare(swlib, "n=2;input=1024;output=8;policy=continuous_batching;kv_capacity_blocks=10")
     # exclusive with several instances: ConfigError in both
     _compare(swlib, "n=2;input=16;output=2;policy=multi_instance;n_instances=2;mode=exclusive")
+
+
+TRACE = """id,arrival_s,input_tokens,output_tokens
+3,0.0,300,12
+0,0.0,64,4
+7,0.0015,900,30
+1,0.002,128,1
+5,0.002,2048,8
+2,0.0105,17,40
+"""
+
+
+@pytest.mark.parametrize("policy", ["policy=continuous_batching", "policy=mixed_batching;max_batch=2",
+                                    "policy=pipelined_splitwiser;P=2;max_batch=3;mode=mps_concurrent",
+                                    "policy=sequential;max_batch=4"])
+def test_trace_workload_matches_reference(swlib, tmp_path, policy):
+    """workload.trace (config.hpp assemble + request.hpp parse_trace): sorted by arrival, ties by id."""
+    p = tmp_path / "trace.csv"
+    p.write_text(TRACE)
+    _compare(swlib, f"trace={p};{policy}")
+
+
+def test_trace_errors_match_reference(swlib, tmp_path):
+    bad = tmp_path / "bad.csv"
+    bad.write_text("id,arrival_s,input_tokens,output_tokens\n1,0.0,10,2\n1,0.5,10,2\n")  # duplicate id
+    _compare(swlib, f"trace={bad};policy=continuous_batching")
+    _compare(swlib, f"trace={tmp_path / 'missing.csv'};policy=continuous_batching")
