@@ -7,7 +7,8 @@ for the virtual-clock backend (`--backend sim`, sw_sim_run) and the B200 engine
   python -m paper_2505_03763_b200.cli run -c configs/hf_splitwiser.json [--set scheduler.P=4] [--emit-events]
   python -m paper_2505_03763_b200.cli run -c cfg.json --backend gpu --model LLAMA_1B --set engine.split=1
   python -m paper_2505_03763_b200.cli sweep -c configs/sweep_batch.json
-  python -m paper_2505_03763_b200.cli replay out/run/events.csv
+  python -m paper_2505_03763_b200.cli replay out/run/events.csv [--out dir]
+  python -m paper_2505_03763_b200.cli validate -c cfg.json
 
 A config becomes the C-ABI's `key=value;...` run spec (config_to_spec); the
 run writes report.json / requests.csv / timeseries.csv (/ events.csv) under
@@ -220,6 +221,9 @@ def cmd_sweep(args) -> int:
         raise ConfigError(-2, "sweep.values: non-empty array required")
     root = base.get("output_dir", "out")
     os.makedirs(root, exist_ok=True)
+    for item in getattr(args, "set", None) or []:
+        k, _, v = item.partition("=")
+        set_path(base, k, _parse_value(v))
     rows: List[str] = ["value,status,makespan_s,tokens_per_s,requests_per_s,steady_tokens_per_s,"
                        "mean_ttft_s,mean_tbt_s,mean_e2e_s,p99_e2e_s,mean_batch_elapsed_s"]
     r = _Runner(args.backend, args.model)
@@ -235,19 +239,48 @@ def cmd_sweep(args) -> int:
                                          "mean_ttft_s", "mean_tbt_s", "mean_e2e_s", "p99_e2e_s",
                                          "mean_batch_elapsed_s")]
                 rows.append(_sanitize(v) + ",ok," + ",".join("%.17g" % x if not math.isnan(x) else "nan" for x in vals))
-            except SplitwiseError:
+                print(f"{axis}={_sanitize(v)}: {summary_line(rep)}")
+            except SplitwiseError as e:
                 ok = False
                 rows.append(_sanitize(v) + ",failed" + "," * 9)
+                print(f"{axis}={_sanitize(v)}: FAILED: {e}")
     finally:
         r.close()
-    with open(os.path.join(root, "sweep.csv"), "w") as f:
+    csv_path = os.path.join(root, "sweep.csv")
+    with open(csv_path, "w") as f:
         f.write("\n".join(rows) + "\n")
-    return 0 if ok else 4
+    print(f"sweep.csv: {csv_path}")
+    return 0 if ok else 1  # tools/splitsim.cpp sweep_cmd
 
 
 def cmd_replay(args) -> int:
-    res = replay(args.events)
+    res = replay(args.events)  # writes replay_report.json beside the log
+    if args.out:
+        import shutil
+
+        os.makedirs(args.out, exist_ok=True)
+        src = os.path.join(os.path.dirname(os.path.abspath(args.events)), "replay_report.json")
+        shutil.move(src, os.path.join(args.out, "replay_report.json"))
     print(summary_line(res.report))
+    return 0
+
+
+def cmd_validate(args) -> int:
+    """tools/splitsim.cpp validate_cmd: schema, policy/discipline and KV-budget checks, trace readable."""
+    with open(args.config) as f:
+        cfg = json.load(f)
+    for item in args.set or []:
+        k, _, v = item.partition("=")
+        set_path(cfg, k, _parse_value(v))
+    spec = config_to_spec(cfg)
+    if "trace" in cfg.get("workload", {}):
+        with open(cfg["workload"]["trace"]):
+            pass
+    # the C++ spec builder validates the rest; an empty workload makes it a no-op run
+    probe = ";".join(kv for kv in spec.split(";") if not kv.startswith(("output_dir=", "emit_event_log=", "n=",
+                                                                          "trace=", "engine.")))
+    sim_run(probe + ";n=0")
+    print("ok")
     return 0
 
 
@@ -263,11 +296,17 @@ def main(argv=None) -> int:
             p.add_argument("--set", action="append", help="override a config field: key.path=value")
             p.add_argument("--emit-events", action="store_true")
             p.add_argument("--output-dir", default="")
+        if name == "sweep":
+            p.add_argument("--set", action="append", help="override a base-config field: key.path=value")
+    p = sub.add_parser("validate")
+    p.add_argument("-c", "--config", required=True)
+    p.add_argument("--set", action="append")
     p = sub.add_parser("replay")
     p.add_argument("events")
+    p.add_argument("--out", default="", help="directory for replay_report.json")
     args = ap.parse_args(argv)
     try:
-        return {"run": cmd_run, "sweep": cmd_sweep, "replay": cmd_replay}[args.cmd](args)
+        return {"run": cmd_run, "sweep": cmd_sweep, "replay": cmd_replay, "validate": cmd_validate}[args.cmd](args)
     except (ConfigError, json.JSONDecodeError) as e:
         print(f"config error: {e}", file=sys.stderr)
         return 2

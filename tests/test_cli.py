@@ -132,3 +132,15 @@ def test_trace_workload_config(tmp_path):
     assert code == 0
     assert json.loads(_read(out, "report.json"))["n_requests"] == 3
     _check_against_reference(dict(cfg, output_dir=str(out), emit_event_log=True), out)
+
+
+def test_validate(tmp_path, capsys):
+    p = tmp_path / "cfg.json"
+    p.write_text(json.dumps(INLINE))
+    assert cli.main(["validate", "-c", str(p)]) == 0
+    assert capsys.readouterr().out.strip() == "ok"
+    p.write_text(json.dumps(dict(INLINE, scheduler={"policy": "nope"})))
+    assert cli.main(["validate", "-c", str(p)]) == 2
+    p.write_text(json.dumps(dict(INLINE, scheduler={"policy": "multi_instance", "n_instances": 2},
+                                 discipline={"mode": "exclusive"})))
+    assert cli.main(["validate", "-c", str(p)]) == 2
