@@ -305,6 +305,11 @@ void prefill_forward(sw_model* m, sw_kv* kv, const sw_batch& b, cudaStream_t st,
         const bool fuse_rope = fuse_env != 0;
         PrefillTcArgs ta{};
         CUtensorMap tm_q{};
+        // persistent prefill attention for short prompts (1B 32 x 512 layer: 165 -> 153 us); prompts of
+        // many 128-row tiles keep one item per CTA (8B 4 x 8192: 4.37 vs 4.63 ms persistent)
+        int max_prompt = 0;
+        for (int s = 0; s < S; ++s) max_prompt = std::max(max_prompt, b.n_tokens[first + s]);
+        const bool tc_persist = max_prompt <= 1024;
         if (use_tc) {
             ta.n_tiles = w.pmeta + 3;
             ta.tile_seq = dev(tseq128);
@@ -346,7 +351,7 @@ void prefill_forward(sw_model* m, sw_kv* kv, const sw_batch& b, cudaStream_t st,
             }
             if (use_tc) {
                 ta.layer_row0 = static_cast<int>(l * kv->layer_stride / d.head_dim);
-                attn_prefill_tc(tm_q, kv->tm_kv, w.attn, ta, n_tiles128, d.head_dim, st);
+                attn_prefill_tc(tm_q, kv->tm_kv, w.attn, ta, n_tiles128, d.head_dim, tc_persist, st);
             } else {
                 attn_prefill(w.q, kvl, w.attn, aa, n_tiles, d.head_dim, st);
             }

@@ -60,8 +60,10 @@ struct PrefillTcArgs {
     int page_rows;   // arena-map rows per page
     int v_rows;      // K -> V rows inside a page
 };
+// persistent: one CTA per SM looping over (tile, head pair) items -- amortises the CTA
+// prologue for short prompts; long prompts (uneven causal items) keep one item per CTA
 void attn_prefill_tc(const CUtensorMap& tm_q, const CUtensorMap& tm_kv, __nv_bfloat16* out, const PrefillTcArgs& a,
-                     int max_tiles, int hd, cudaStream_t st);
+                     int max_tiles, int hd, bool persistent, cudaStream_t st);
 
 // Flat page-balanced decode attention (attn_decode_flat.cu): persistent grid,
 // TMA page-slice loads through a 2-D map of the whole KV arena (rows of hd

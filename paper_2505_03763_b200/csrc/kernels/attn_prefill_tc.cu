@@ -26,11 +26,14 @@
 #include <cuda.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "attention.cuh"
 #include "common.cuh"
 
 namespace sw {
+int stream_sm_count(cudaStream_t st);  // engine/partition.cu
+
 namespace {
 
 constexpr int kRows = 128;     // query rows per CTA
@@ -112,21 +115,9 @@ __global__ void __launch_bounds__(256, 1) attn_prefill_tc_kernel(const __grid_co
     uint64_t* o_done_g = bar + 9;  // [2] per group
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 11);
 
-    const int tile = blockIdx.x;
-    if (tile >= *a.n_tiles) return;
     const int tid = threadIdx.x, warp = tid >> 5;
-    const int g = warp >> 2;              // group: query head 2 * blockIdx.y + g
+    const int g = warp >> 2;              // group: query head 2 * pair + g
     const int gt = tid & 127;             // thread within the group = query row
-    const int h = 2 * blockIdx.y + g;
-    const int hk = h / (a.H / a.Hkv);     // same for both groups (H / Hkv even)
-    const int sq = a.tile_seq[tile];
-    const int q0 = a.tile_q0[tile];
-    const int start = a.cu_seqlens[sq];
-    const int len = a.cu_seqlens[sq + 1] - start;
-    const int kend = min(q0 + kRows, len);        // keys this tile attends to: [0, kend)
-    const int nblk = (kend + kBlk - 1) / kBlk;
-    const int npages = (len + kPg - 1) / kPg;
-    const int32_t* ptab = a.page_table + static_cast<long long>(a.seq_slot[sq]) * a.max_pages;
     if (tid == 0) {
         mbar_init(q_full, 1);
         mbar_init(&k_full[0], 1);
@@ -157,6 +148,24 @@ __global__ void __launch_bounds__(256, 1) attn_prefill_tc_kernel(const __grid_co
     uint8_t* sQg = sQ + g * C::kQ;
     uint8_t* sPg = sP + g * C::kP;
 
+    // Persistent: work items (128-row query tile, head pair) round robin over the CTAs.  Barrier
+    // phases run on the CTA's global key-block count gb (K stage gb & 1) and item count it.
+    const int pairs = a.H / 2;
+    const int n_items = *a.n_tiles * pairs;
+    int gb = 0, it = 0;
+    for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
+    const int tile = item / pairs, pair = item % pairs;
+    const int h = 2 * pair + g;
+    const int hk = h / (a.H / a.Hkv);     // same for both groups (H / Hkv even)
+    const int sq = a.tile_seq[tile];
+    const int q0 = a.tile_q0[tile];
+    const int start = a.cu_seqlens[sq];
+    const int len = a.cu_seqlens[sq + 1] - start;
+    const int kend = min(q0 + kRows, len);        // keys this tile attends to: [0, kend)
+    const int nblk = (kend + kBlk - 1) / kBlk;
+    const int npages = (len + kPg - 1) / kPg;
+    const int32_t* ptab = a.page_table + static_cast<long long>(a.seq_slot[sq]) * a.max_pages;
+
     // K (v = 0) or V (v = 1) of key block j into `dst`, completing on `b` (thread 0).
     // Page ids past the prompt read page 0 (finite data, masked).
     auto load_blk = [&](int j, int v, uint8_t* dst, uint64_t* b) {
@@ -176,13 +185,17 @@ __global__ void __launch_bounds__(256, 1) attn_prefill_tc_kernel(const __grid_co
         }
     };
     if (tid == 0) {
+        // the previous item's S MMAs (both groups) retired: Q and that K stage are free
+        if (gb >= 1) mbar_wait(&k_empty[(gb - 1) & 1], ((gb - 1) >> 1) & 1);
         mbar_expect_tx(q_full, 2 * C::kQ);
 #pragma unroll
         for (int q = 0; q < 2; ++q)
 #pragma unroll
             for (int c = 0; c < C::NH; ++c)
-                tma_load_3d(sQ + q * C::kQ + c * C::kAtom, &tm_q, q_full, c * 64, 2 * blockIdx.y + q, start + q0);
-        load_blk(0, 0, sK, &k_full[0]);
+                tma_load_3d(sQ + q * C::kQ + c * C::kAtom, &tm_q, q_full, c * 64, 2 * pair + q, start + q0);
+        if (gb >= 2) mbar_wait(&k_empty[gb & 1], ((gb - 2) >> 1) & 1);
+        load_blk(0, 0, sK + (gb & 1) * C::kKV, &k_full[gb & 1]);
+        if (gb >= 1) mbar_wait(v_empty, (gb - 1) & 1);  // both groups' last PV retired: V is free
         load_blk(0, 1, sV, v_full);
     }
 
@@ -195,15 +208,16 @@ __global__ void __launch_bounds__(256, 1) attn_prefill_tc_kernel(const __grid_co
     float m_run = -INFINITY, l_run = 0.f;
 
     for (int j = 0; j < nblk; ++j) {
-        const int s = j & 1;
-        // ---- S = Q K_j^T (K_{j+1} streams into the other stage once both groups' S_{j-1} retired)
+        const int G = gb + j;  // global key-block index: barrier phases
+        const int s = G & 1;
+        // ---- S = Q K_j^T (K_{j+1} streams into the other stage once both groups' S_{G-1} retired)
         if (tid == 0 && j + 1 < nblk) {
-            if (j >= 1) mbar_wait(&k_empty[s ^ 1], ((j - 1) >> 1) & 1);
+            if (G >= 1) mbar_wait(&k_empty[s ^ 1], ((G - 1) >> 1) & 1);
             load_blk(j + 1, 0, sK + (s ^ 1) * C::kKV, &k_full[s ^ 1]);
         }
         if (gt == 0) {
-            if (j == 0) mbar_wait(q_full, 0);
-            mbar_wait(&k_full[s], (j >> 1) & 1);
+            if (j == 0) mbar_wait(q_full, it & 1);
+            mbar_wait(&k_full[s], (G >> 1) & 1);
             tc_fence_after();
 #pragma unroll
             for (int c = 0; c < C::NH; ++c)
@@ -215,7 +229,7 @@ __global__ void __launch_bounds__(256, 1) attn_prefill_tc_kernel(const __grid_co
             umma_commit(s_done);
             umma_commit(&k_empty[s]);
         }
-        mbar_wait(s_done, j & 1);
+        mbar_wait(s_done, G & 1);
         tc_fence_after();
         // ---- softmax of this thread's row (two passes over TMEM: max, then exp/sum/P)
         const int kbase = j * kBlk;
@@ -276,7 +290,7 @@ __global__ void __launch_bounds__(256, 1) attn_prefill_tc_kernel(const __grid_co
         asm volatile("bar.sync %0, 128;" ::"r"(1 + g) : "memory");  // this group's 128 threads
         // ---- O += P V_j
         if (gt == 0) {
-            mbar_wait(v_full, j & 1);
+            mbar_wait(v_full, G & 1);
             tc_fence_after();
 #pragma unroll
             for (int kc = 0; kc < kBlk / 16; ++kc)
@@ -285,10 +299,10 @@ __global__ void __launch_bounds__(256, 1) attn_prefill_tc_kernel(const __grid_co
             umma_commit(o_done);
             umma_commit(v_empty);
         }
-        mbar_wait(o_done, j & 1);  // this group's P and O are free again
+        mbar_wait(o_done, G & 1);  // this group's P and O are free again
         tc_fence_after();
         if (tid == 0 && j + 1 < nblk) {  // V_{j+1} once both groups' PV_j retired
-            mbar_wait(v_empty, j & 1);
+            mbar_wait(v_empty, G & 1);
             load_blk(j + 1, 1, sV, v_full);
         }
     }
@@ -314,6 +328,9 @@ __global__ void __launch_bounds__(256, 1) attn_prefill_tc_kernel(const __grid_co
             }
         }
     }
+    tc_fence_before();  // this item's O loads precede the group's next PV (ordered by its next bar.sync)
+    gb += nblk;
+    }  // items
     tc_fence_before();
     __syncthreads();
     if (warp == 0) {
@@ -324,22 +341,30 @@ __global__ void __launch_bounds__(256, 1) attn_prefill_tc_kernel(const __grid_co
 
 template <int HD>
 void tc_launch(const CUtensorMap& tq, const CUtensorMap& tkv, __nv_bfloat16* out, const PrefillTcArgs& a, int max_tiles,
-               cudaStream_t st) {
+               bool persistent, cudaStream_t st) {
     using C = TcCfg<HD>;
     static bool cfg = false;
     if (!cfg) {
         SW_CUDA(cudaFuncSetAttribute(attn_prefill_tc_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
         cfg = true;
     }
-    launch_k(attn_prefill_tc_kernel<HD>, dim3(max_tiles, a.H / 2), dim3(256), C::kSmem, st, tq, tkv, out, a);
+    // persistent: one CTA per SM of the stream's partition (smem and TMEM allow one), items round robin
+    static const int persist_env = [] {  // SW_PREFILL_TC_PERSIST=0/1 forces (A/B); default: the caller's choice
+        const char* v = std::getenv("SW_PREFILL_TC_PERSIST");
+        return v && *v ? std::atoi(v) : -1;
+    }();
+    const bool persist = persist_env >= 0 ? persist_env != 0 : persistent;
+    const int items = max_tiles * (a.H / 2);
+    const int grid = std::max(1, persist ? std::min(items, stream_sm_count(st)) : items);
+    launch_k(attn_prefill_tc_kernel<HD>, dim3(grid), dim3(256), C::kSmem, st, tq, tkv, out, a);
 }
 
 }  // namespace
 
 void attn_prefill_tc(const CUtensorMap& tm_q, const CUtensorMap& tm_kv, __nv_bfloat16* out, const PrefillTcArgs& a,
-                     int max_tiles, int hd, cudaStream_t st) {
-    if (hd == 64) tc_launch<64>(tm_q, tm_kv, out, a, max_tiles, st);
-    else if (hd == 128) tc_launch<128>(tm_q, tm_kv, out, a, max_tiles, st);
+                     int max_tiles, int hd, bool persistent, cudaStream_t st) {
+    if (hd == 64) tc_launch<64>(tm_q, tm_kv, out, a, max_tiles, persistent, st);
+    else if (hd == 128) tc_launch<128>(tm_q, tm_kv, out, a, max_tiles, persistent, st);
     else throw_cuda("attn_prefill_tc: head_dim must be 64 or 128", cudaErrorInvalidValue, __FILE__, __LINE__);
 }
 
