@@ -208,6 +208,10 @@ __global__ void __launch_bounds__(128, HD == 64 ? 4 : 2) attn_prefill_kernel(con
 // One CTA = one unit (row, kv head, split of the context); see attn_decode_unit.cuh.
 // NS-stage per-warp K/V rings: NS = 3 keeps 2 blocks per warp in flight at two
 // CTAs per SM (more bytes in flight per SM than 3 CTAs x double buffers).
+// SW_ATTN_LASTWAVE_TRIGGER=0 disables the last-wave early trigger (A/B)
+__device__ __constant__ bool kEarlyTrigger_c = true;
+#define kEarlyTrigger kEarlyTrigger_c
+
 template <int HD, int G, int KB, int NS>
 __global__ void __launch_bounds__(128, NS == 2 ? 3 : (NS == 3 ? 2 : 1))
     attn_decode_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ kv_layer,
@@ -215,8 +219,6 @@ __global__ void __launch_bounds__(128, NS == 2 ? 3 : (NS == 3 ? 2 : 1))
     extern __shared__ __align__(128) uint8_t dsm[];
     __shared__ uint32_t s_last;
     __shared__ int32_t s_pages[kMaxChunkPages];
-    // No early launch_dependents: the successor GEMM's CTAs (~112 KB smem) would
-    // take the SM slots this kernel's later waves need; it launches as we exit.
     griddep_wait();
     const int n_rows = a.meta->n;
     const int row = blockIdx.z;
@@ -225,10 +227,27 @@ __global__ void __launch_bounds__(128, NS == 2 ? 3 : (NS == 3 ? 2 : 1))
     // splits chosen at run time: only as many as it takes to reach
     // a.target_ctas CTAs, each warp keeping >= 1 key block
     const SplitPlan plan = decode_split_plan<KB>(ctx, cdiv(a.target_ctas, n_rows * a.Hkv), static_cast<int>(gridDim.x));
+    // The successor GEMM (~112 KB CTAs) may only launch once this kernel's last wave is resident
+    // (earlier, its CTAs would take the slots later waves need): the CTAs of the last
+    // ~target_ctas units trigger at their start, the others count as triggered when they exit.
+    // Measured (tools/step_time.py): Llama-1B b=64 step 1.030 -> 1.006 ms; Llama-8B b=128 ctx 1024
+    // 6.78 -> 7.17 ms (its attention streams at HBM peak and the GEMM's prefetch competes) -> hd 64 only.
+    if (HD == 64 && kEarlyTrigger && row >= n_rows - cdiv(a.target_ctas, a.Hkv * max(1, plan.splits)))
+        griddep_launch_dependents();
     const int split = blockIdx.x;
     if (split >= plan.splits) return;
     decode_unit<HD, G, KB, NS>(a, q, kv_layer, out, row, blockIdx.y, split, plan, ctx, dsm, s_pages, &s_last,
                                threadIdx.x, [] { __syncthreads(); });
+}
+
+void set_early_trigger_once() {
+    static bool done = [] {
+        const char* v = std::getenv("SW_ATTN_LASTWAVE_TRIGGER");
+        const bool on = !(v && *v && std::atoi(v) == 0);
+        SW_CUDA(cudaMemcpyToSymbol(kEarlyTrigger_c, &on, sizeof(on)));
+        return true;
+    }();
+    (void)done;
 }
 
 template <int HD, int G, int NS>
@@ -244,6 +263,7 @@ void decode_launch_ns(const __nv_bfloat16* q, const __nv_bfloat16* kv_layer, __n
     }
     // grid x: the most splits any row can take at this bucket size (the kernel
     // picks <= gridDim.x per row at run time), plus what the smem page list needs
+    set_early_trigger_once();
     DecodeAttnArgs args = a;
     const int want = std::max(1, std::min(a.max_splits, cdiv(a.target_ctas, max_rows * a.Hkv)));
     args.max_splits = std::max(want, cdiv(a.max_ctx, kMaxChunkPages * kPage));
