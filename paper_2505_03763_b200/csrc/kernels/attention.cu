@@ -219,7 +219,7 @@ __global__ void __launch_bounds__(128, NS == 2 ? 3 : (NS == 3 ? 2 : 1))
     extern __shared__ __align__(128) uint8_t dsm[];
     __shared__ uint32_t s_last;
     __shared__ int32_t s_pages[kMaxChunkPages];
-    griddep_wait();
+    // the step's metadata was copied before its first kernel: readable before the wait
     const int n_rows = a.meta->n;
     const int row = blockIdx.z;
     if (row >= n_rows) return;
@@ -237,7 +237,7 @@ __global__ void __launch_bounds__(128, NS == 2 ? 3 : (NS == 3 ? 2 : 1))
     const int split = blockIdx.x;
     if (split >= plan.splits) return;
     decode_unit<HD, G, KB, NS>(a, q, kv_layer, out, row, blockIdx.y, split, plan, ctx, dsm, s_pages, &s_last,
-                               threadIdx.x, [] { __syncthreads(); });
+                               threadIdx.x, [] { __syncthreads(); }, [] { griddep_wait(); });
 }
 
 void set_early_trigger_once() {

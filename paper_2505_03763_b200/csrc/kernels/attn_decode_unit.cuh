@@ -84,12 +84,16 @@ __device__ __forceinline__ SplitPlan decode_split_plan(int ctx, int want, int ca
 // One unit.  `tid` in [0, 128); `sync()` synchronises exactly the 128
 // threads running the unit.  smem: dsm (decode_unit_smem bytes), s_pages
 // (kMaxChunkPages ints), s_last (one word).
-template <int HD, int G, int KB, int NS = 2, class Sync>
+// `wait_pred()` is called once, after the ring fill of key blocks older than this
+// step's token (KV written by earlier steps, page ids installed earlier) and before
+// anything the predecessor kernel produces (q, the new K/V entry, a page installed
+// this step) is read: the unit's HBM stream starts while the QKV GEMM drains.
+template <int HD, int G, int KB, int NS = 2, class Sync, class Wait>
 __device__ __forceinline__ void decode_unit(const DecodeAttnArgs& a, const __nv_bfloat16* __restrict__ q,
                                             const __nv_bfloat16* __restrict__ kv_layer,
                                             __nv_bfloat16* __restrict__ out, int row, int hk, int split,
                                             const SplitPlan& plan, int ctx, uint8_t* dsm, int32_t* s_pages,
-                                            uint32_t* s_last, int tid, Sync sync) {
+                                            uint32_t* s_last, int tid, Sync sync, Wait wait_pred) {
     static_assert(G <= 8, "query rows live in the first 8 mma rows");
     constexpr int CH = HD / 8;
     const int warp = tid >> 5, lane = tid & 31;
@@ -108,19 +112,6 @@ __device__ __forceinline__ void decode_unit(const DecodeAttnArgs& a, const __nv_
     }
     const int page_base = k_begin / kPage;
     const int n_blocks = cdiv(k_end - k_begin, KB);
-
-    // Q fragment (A operand, rows = query heads of this kv head)
-    const int r = lane >> 2;
-    uint32_t qf[HD / 16][4];
-    const __nv_bfloat16* qrow = q + static_cast<int64_t>(row) * a.H * HD + static_cast<int64_t>(hk * G + r) * HD;
-#pragma unroll
-    for (int ks = 0; ks < HD / 16; ++ks) {
-        const int c = ks * 16 + (lane & 3) * 2;
-        qf[ks][0] = r < G ? *reinterpret_cast<const uint32_t*>(qrow + c) : 0u;
-        qf[ks][1] = 0u;
-        qf[ks][2] = r < G ? *reinterpret_cast<const uint32_t*>(qrow + c + 8) : 0u;
-        qf[ks][3] = 0u;
-    }
 
     // A block is KB / kPage whole pages (blocks start page aligned); a (layer,
     // page, kv head) K or V slice is one contiguous kPage x HD run, so lane l
@@ -156,11 +147,48 @@ __device__ __forceinline__ void decode_unit(const DecodeAttnArgs& a, const __nv_
     sync();  // s_pages
     // warp w streams blocks w, w + 4, ... through an NS-stage ring (NS - 1 in flight while one is computed)
     const int my_blocks = n_blocks > warp ? (n_blocks - warp + 3) / 4 : 0;
+    // ring fill before the wait: blocks that end before this step's token (the last key, ctx - 1) --
+    // in issue order, one commit per slot exactly as the in-order fill would make them
+    int filled = 0;
 #pragma unroll
     for (int i = 0; i < NS - 1; ++i) {
-        if (i < my_blocks) load(warp + 4 * i, i);
-        cp_async_commit();
+        const bool old_block = k_begin + (warp + 4 * i + 1) * KB < ctx;  // ends before key ctx - 1
+        if (filled == i && (i >= my_blocks || old_block)) {
+            if (i < my_blocks) load(warp + 4 * i, i);
+            cp_async_commit();
+            ++filled;
+        }
     }
+    wait_pred();
+    if (k_end == ctx) {  // this split holds the token's page: its id may have been installed by this step
+        sync();
+        if (tid == 0) {
+            const int32_t* ptab = a.page_table + static_cast<int64_t>(a.meta->slot[row]) * a.max_pages;
+            s_pages[(ctx - 1) / kPage - page_base] = ptab[(ctx - 1) / kPage];
+        }
+        sync();
+    }
+#pragma unroll
+    for (int i = 0; i < NS - 1; ++i) {
+        if (i >= filled) {
+            if (i < my_blocks) load(warp + 4 * i, i);
+            cp_async_commit();
+        }
+    }
+    // Q fragment (A operand, rows = query heads of this kv head)
+    const int r = lane >> 2;
+    uint32_t qf[HD / 16][4];
+    const __nv_bfloat16* qrow = q + static_cast<int64_t>(row) * a.H * HD + static_cast<int64_t>(hk * G + r) * HD;
+#pragma unroll
+    for (int ks = 0; ks < HD / 16; ++ks) {
+        const int c = ks * 16 + (lane & 3) * 2;
+        qf[ks][0] = r < G ? *reinterpret_cast<const uint32_t*>(qrow + c) : 0u;
+        qf[ks][1] = 0u;
+        qf[ks][2] = r < G ? *reinterpret_cast<const uint32_t*>(qrow + c + 8) : 0u;
+        qf[ks][3] = 0u;
+    }
+
+
     for (int it = 0; it < my_blocks; ++it) {
         const int blk = warp + 4 * it;
         const int buf = it % NS;
