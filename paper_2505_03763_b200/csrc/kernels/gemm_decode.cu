@@ -26,6 +26,7 @@
 #include <cuda.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "gemm_epilogue.cuh"
@@ -75,8 +76,37 @@ struct TokCtx {
 // a warp covers the tile's 128 features of the token contiguously.  Pairs of
 // features that meet in an epilogue (SwiGLU gate/up, RoPE rotate-half
 // partners) are lanes apart and exchanged by shuffles.  t is warp uniform.
+// Global inputs of emit_tok that do not depend on the accumulator (residual
+// row, RoPE cos/sin), loaded one token ahead so their latency overlaps the
+// previous token's epilogue.
+struct TokPre {
+    float4 a, b;
+};
+
 template <int MODE>
-__device__ __forceinline__ void emit_tok(const TokCtx& c, int t, int lane, float4 v) {
+__device__ __forceinline__ TokPre pre_tok(const TokCtx& c, int t, int lane) {
+    const GemmArgs& args = *c.a;
+    const int f0 = c.m0 + 4 * lane;
+    TokPre p{};
+    if constexpr (MODE == EPI_RESID) {
+        p.a = __ldcg(reinterpret_cast<const float4*>(static_cast<const float*>(args.out) +
+                                                     static_cast<size_t>(t) * args.ldo + f0));
+    } else if constexpr (MODE == EPI_QKV_ROPE) {
+        const DecodeFusion& fx = args.fx;
+        const int hd = fx.hd, half = hd >> 1;
+        const int head = f0 / hd, d0 = f0 - head * hd;
+        if (head < fx.H + fx.Hkv) {
+            const float4* cs4 = reinterpret_cast<const float4*>(fx.rope_cs + static_cast<int64_t>(c.tok_pos[t]) * half +
+                                                                (d0 & (half - 1)));
+            p.a = __ldg(cs4);
+            p.b = __ldg(cs4 + 1);
+        }
+    }
+    return p;
+}
+
+template <int MODE>
+__device__ __forceinline__ void emit_tok(const TokCtx& c, int t, int lane, float4 v, const TokPre& pre) {
     const GemmArgs& args = *c.a;
     const DecodeFusion& fx = args.fx;
     const int i0 = 4 * lane;
@@ -95,7 +125,7 @@ __device__ __forceinline__ void emit_tok(const TokCtx& c, int t, int lane, float
         *reinterpret_cast<float4*>(static_cast<float*>(args.out) + static_cast<size_t>(t) * args.ldo + f0) = v;
     } else if constexpr (MODE == EPI_RESID) {
         float4* px = reinterpret_cast<float4*>(static_cast<float*>(args.out) + static_cast<size_t>(t) * args.ldo + f0);
-        float4 x = __ldcg(px);
+        float4 x = pre.a;
         x.x += v.x;
         x.y += v.y;
         x.z += v.z;
@@ -132,9 +162,7 @@ __device__ __forceinline__ void emit_tok(const TokCtx& c, int t, int lane, float
         const bool is_v = head >= fx.H + fx.Hkv;
         float4 o = v;
         if (!is_v) {
-            const float4* cs4 = reinterpret_cast<const float4*>(fx.rope_cs + static_cast<int64_t>(c.tok_pos[t]) * half +
-                                                                (d0 & (half - 1)));
-            const float4 ca = cs4[0], cb = cs4[1];  // (cos, sin) of d0, d0+1 | d0+2, d0+3
+            const float4 ca = pre.a, cb = pre.b;  // (cos, sin) of d0, d0+1 | d0+2, d0+3
             const float sg = d0 < half ? -1.f : 1.f;
             o.x = v.x * ca.x + sg * p.x * ca.y;
             o.y = v.y * ca.z + sg * p.y * ca.w;
@@ -295,7 +323,8 @@ __global__ void __launch_bounds__(kThreads, 2)
                 asm volatile("bar.sync 1, 128;" ::: "memory");
                 const int cnt = min(32, n_live - c);
                 for (int j = ew; j < cnt; j += 4)
-                    emit_tok<MODE>(tc, c + j, lane, *reinterpret_cast<const float4*>(T + j * kTs + 4 * lane));
+                    emit_tok<MODE>(tc, c + j, lane, *reinterpret_cast<const float4*>(T + j * kTs + 4 * lane),
+                                   pre_tok<MODE>(tc, c + j, lane));
             }
         } else {
             // park this rank's partial token-major (a warp stores 128 contiguous bytes per token)
@@ -312,27 +341,42 @@ __global__ void __launch_bounds__(kThreads, 2)
     }
     if (S > 1) {
         cluster_sync_all();  // every rank's partial is in L2
-        if (warp >= kEpiWarp0) {
-            // rank r owns tokens [r*n/S, (r+1)*n/S): add the S partials in rank order (deterministic)
-            const int t0 = rank * n_live / S, t1 = (rank + 1) * n_live / S;
-            for (int t = t0 + ew; t < t1; t += 4) {
-                float4 in[kMaxSplit];
+        // rank r owns tokens [r*n/S, (r+1)*n/S): add the S partials in rank order
+        // (deterministic).  All warps of the CTA take part (the producer and MMA
+        // warps are idle by now; the cluster barrier published the epilogue
+        // warps' shared token tables to them), and the next token's loads
+        // are issued before this token's stores, so a warp has two tokens of
+        // L2 reads in flight instead of one dependent round trip per token.
+        if (warp < kEpiWarp0) {
+            griddep_wait();  // no-op by now; orders the live-token read after the predecessor
+            n_live = args.live_tokens ? min(args.valid_tokens, *args.live_tokens) : args.valid_tokens;
+        }
+        const int t0 = rank * n_live / S, t1 = (rank + 1) * n_live / S;
+        constexpr int kWarps = kThreads / 32;
+        float4 in[kMaxSplit];
+        TokPre pre{};
+        auto load = [&](int t) {
 #pragma unroll
-                for (int k = 0; k < kMaxSplit; ++k)
-                    if (k < S)
-                        in[k] = __ldcg(reinterpret_cast<const float4*>(ws_tile + (static_cast<size_t>(k) * BN + t) * BM) +
-                                       lane);
-                float4 v = in[0];
+            for (int k = 0; k < kMaxSplit; ++k)
+                if (k < S)
+                    in[k] = __ldcg(reinterpret_cast<const float4*>(ws_tile + (static_cast<size_t>(k) * BN + t) * BM) + lane);
+            pre = pre_tok<MODE>(tc, t, lane);
+        };
+        int t = t0 + warp;
+        if (t < t1) load(t);
+        for (; t < t1; t += kWarps) {
+            float4 v = in[0];
 #pragma unroll
-                for (int k = 1; k < kMaxSplit; ++k)
-                    if (k < S) {
-                        v.x += in[k].x;
-                        v.y += in[k].y;
-                        v.z += in[k].z;
-                        v.w += in[k].w;
-                    }
-                emit_tok<MODE>(tc, t, lane, v);
-            }
+            for (int k = 1; k < kMaxSplit; ++k)
+                if (k < S) {
+                    v.x += in[k].x;
+                    v.y += in[k].y;
+                    v.z += in[k].z;
+                    v.w += in[k].w;
+                }
+            const TokPre cur = pre;
+            if (t + kWarps < t1) load(t + kWarps);
+            emit_tok<MODE>(tc, t, lane, v, cur);
         }
     }
     __syncthreads();
@@ -393,12 +437,20 @@ void dispatch_mode(int mode, const CUtensorMap& a, const CUtensorMap& b, const G
 
 // Split factor from the weight shape and the device only (never the batch, so
 // the summation order is the same at every batch size): as many CTAs per tile
-// as keep tiles * S within `ctas`, each CTA with >= 2 K-blocks.  Clusters are
-// independent, so a cluster that does not fit in the first wave only costs
-// time (measured: capping S to co-resident clusters was 3-5% slower per step).
+// as keep tiles * S within `ctas`, each CTA with >= 2 K-blocks.  A cluster is
+// placed inside one GPC, so up to S - 1 CTA slots per GPC can stay unused;
+// a grid that only fits the SM count exactly leaves clusters for a second
+// wave (Llama-8B QKV: 48 clusters of 6 = 288 of 296 slots).  The budget keeps
+// kGpcs * (S - 1) slots of headroom.  (cudaOccupancyMaxActiveClusters is far
+// more conservative -- it allowed S = 2 there -- and was 2-5% slower.)
 int gemm_decode_splits(int tiles, int nk, int ctas) {
+    constexpr int kGpcs = 8;
+    static const bool fit = [] {
+        const char* v = std::getenv("SW_DEC_FIT");
+        return !(v && *v == '0');
+    }();
     int s = 1;
-    while (s < kMaxSplit && tiles * (s + 1) <= ctas && nk / (s + 1) >= 2) ++s;
+    while (s < kMaxSplit && tiles * (s + 1) <= ctas - (fit ? kGpcs * s : 0) && nk / (s + 1) >= 2) ++s;
     return s;
 }
 
