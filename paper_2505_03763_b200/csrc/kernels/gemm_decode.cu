@@ -441,16 +441,15 @@ void dispatch_mode(int mode, const CUtensorMap& a, const CUtensorMap& b, const G
 // placed inside one GPC, so up to S - 1 CTA slots per GPC can stay unused;
 // a grid that only fits the SM count exactly leaves clusters for a second
 // wave (Llama-8B QKV: 48 clusters of 6 = 288 of 296 slots).  The budget keeps
-// kGpcs * (S - 1) slots of headroom.  (cudaOccupancyMaxActiveClusters is far
+// 8 x (S - 1) slots of headroom (B200: 8 GPCs).  (cudaOccupancyMaxActiveClusters is far
 // more conservative -- it allowed S = 2 there -- and was 2-5% slower.)
 int gemm_decode_splits(int tiles, int nk, int ctas) {
-    constexpr int kGpcs = 8;
-    static const bool fit = [] {
+    static const int gpcs = [] {  // SW_DEC_FIT: headroom in GPCs (0 = none)
         const char* v = std::getenv("SW_DEC_FIT");
-        return !(v && *v == '0');
+        return v && *v ? std::atoi(v) : 8;
     }();
     int s = 1;
-    while (s < kMaxSplit && tiles * (s + 1) <= ctas - (fit ? kGpcs * s : 0) && nk / (s + 1) >= 2) ++s;
+    while (s < kMaxSplit && tiles * (s + 1) <= ctas - gpcs * s && nk / (s + 1) >= 2) ++s;
     return s;
 }
 
