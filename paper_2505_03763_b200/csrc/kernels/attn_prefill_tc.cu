@@ -148,12 +148,21 @@ __global__ void __launch_bounds__(256, 1) attn_prefill_tc_kernel(const __grid_co
     uint8_t* sQg = sQ + g * C::kQ;
     uint8_t* sPg = sP + g * C::kP;
 
-    // Persistent: work items (128-row query tile, head pair) round robin over the CTAs.  Barrier
-    // phases run on the CTA's global key-block count gb (K stage gb & 1) and item count it.
+    // Persistent: work items (128-row query tile, head pair) dealt to the CTAs last tile first
+    // (a prompt's later query tiles attend to more keys) in a snake order -- round k runs
+    // left to right when k is even, right to left when odd -- so the heavy and light items
+    // of consecutive rounds pair up on one CTA.  With one CTA per item (non-persistent) the
+    // same mapping makes the hardware's in-order block issue longest-first (8B 4 x 8192:
+    // 4.36 -> 4.26 ms per layer).  Barrier phases run on the CTA's global key-block count
+    // gb (K stage gb & 1) and item count it.
     const int pairs = a.H / 2;
     const int n_items = *a.n_tiles * pairs;
+    const int G = static_cast<int>(gridDim.x), bx = static_cast<int>(blockIdx.x);
     int gb = 0, it = 0;
-    for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
+    for (int k = 0;; ++k, ++it) {
+    const int idx = k * G + ((k & 1) ? G - 1 - bx : bx);
+    if (idx >= n_items) break;
+    const int item = n_items - 1 - idx;
     const int tile = item / pairs, pair = item % pairs;
     const int h = 2 * pair + g;
     const int hk = h / (a.H / a.Hkv);     // same for both groups (H / Hkv even)
