@@ -836,7 +836,10 @@ void gemm_run(const GemmProblem& p, cudaStream_t st) {
             // two CTAs per SM fit (<= 112 KB smem each); measured: 2 x SMs beats 1 x SMs
             // on the Llama-1B step (tools/profile_step.py)
             static const int dec_ctas = env_flag("SW_DEC_CTAS", 0);
-            const int S = gemm_decode_splits(tiles, p.K / BK, dec_ctas > 0 ? dec_ctas : 2 * sms);
+            static const int s_qkv = env_flag("SW_DEC_S_QKV", 0);  // experiment: fixed split for the QKV projection
+            const int S = p.mode == EPI_QKV_ROPE && s_qkv > 0
+                              ? s_qkv
+                              : gemm_decode_splits(tiles, p.K / BK, dec_ctas > 0 ? dec_ctas : 2 * sms);
             static const int dec_log = env_flag("SW_DEC_LOG", 0);
             if (dec_log) {
                 static std::mutex mu;
