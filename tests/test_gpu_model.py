@@ -138,19 +138,26 @@ def _long_ctx_engine(desc, pages):
                           max_pages_per_slot=pages, max_out=16)
 
 
-@pytest.mark.parametrize("shape", ["TINY", "LLAMA_1B_2L"])
+@pytest.mark.parametrize("shape", ["TINY", "LLAMA_1B_2L", "LLAMA_8B_1L"])
 def test_long_context_split_kv_and_split_k(shape):
     """Contexts long enough for several split-KV chunks (multi-split merge) and,
-    at the 1B shape, split-K decode GEMMs with the last-CTA fixup."""
+    at the 1B and 8B widths, the cluster split-K decode GEMMs: 1B runs S = 8
+    (QKV, Wo, Wd) and 2 (gate/up); 8B (one layer, small vocabulary) runs the
+    GPC-headroom factors S = 5 (QKV) and 7 (Wo, Wd) and S = 1 (gate/up)."""
     import dataclasses
 
-    d = M.TINY if shape == "TINY" else dataclasses.replace(M.LLAMA_1B, n_layers=2)
+    if shape == "TINY":
+        d = M.TINY
+    elif shape == "LLAMA_1B_2L":
+        d = dataclasses.replace(M.LLAMA_1B, n_layers=2)
+    else:
+        d = dataclasses.replace(M.LLAMA_8B, n_layers=1, vocab=4096)
     pages = 80
     eng = _long_ctx_engine(d, pages)
     try:
         o = M.OracleModel(d)
         emu = M.OracleModel(d, emulate_bf16=True, share_weights_with=o)
-        lens = [700, 1030]
+        lens = [700, 1030] if shape != "LLAMA_8B_1L" else [300, 530]
         prompts = [M.prompt_tokens(d.seed, 500 + i, n, d.vocab) for i, n in enumerate(lens)]
         rows = [list(range(i * pages, (i + 1) * pages)) for i in range(2)]
         lg = eng.prefill([0, 1], prompts, [r[:(n + 15) // 16] for r, n in zip(rows, lens)])
