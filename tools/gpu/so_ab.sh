@@ -1,4 +1,5 @@
-# A/B two builds of libsplitwise.so on one box: bash tools/gpu/so_ab.sh  (abso/old.so vs abso/new.so)
+# A/B two builds of libsplitwise.so on one box: bash tools/gpu/so_ab.sh  (abso/old.so vs abso/new.so;
+# build each with `make -C paper_2505_03763_b200/csrc` and copy ../libsplitwise.so into abso/, git-ignored)
 mkdir -p gpurun_out
 for V in old new old new; do
   cp abso/$V.so paper_2505_03763_b200/libsplitwise.so
