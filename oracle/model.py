@@ -61,6 +61,11 @@ def next_u64_stream(seed: int, n: int) -> List[int]:
     return [int(v) for v in splitmix_at(seed, np.arange(n, dtype=np.uint64))]
 
 
+def f16_round(x: np.ndarray) -> np.ndarray:
+    """float32 -> nearest-even IEEE half, returned as float32 values."""
+    return np.asarray(x, dtype=np.float32).astype(np.float16).astype(np.float32)
+
+
 def bf16_round(x: np.ndarray) -> np.ndarray:
     """float32 -> nearest-even bfloat16, returned as float32 values."""
     u = np.ascontiguousarray(x, dtype=np.float32).view(np.uint32)
@@ -135,12 +140,12 @@ class OracleModel:
     """fp32 Llama-style decoder over bf16-valued weights, paged KV cache.
 
     emulate_bf16=False is THE reference: everything in fp32.  emulate_bf16=True
-    additionally rounds to bf16 exactly where the CUDA path stores bf16
-    (RMSNorm outputs -- in decode the norm is folded into the GEMM, so the
-    rounded tensor is the residual x itself --, roped q/k and v -- the KV
-    cache --, the softmax numerators fed to the P.V tensor-core product,
-    attention output, SwiGLU output), so the remaining difference is
-    accumulation order only.
+    additionally rounds exactly where the CUDA path stores 16-bit values, so
+    the remaining difference is accumulation order only: to bf16 for the GEMM
+    inputs (RMSNorm outputs -- in decode the norm is folded into the GEMM, so
+    the rounded tensor is the residual x itself --, attention output, SwiGLU
+    output), to fp16 for the attention operands (roped q/k and v -- the KV
+    cache -- and the softmax numerators fed to the P.V tensor-core product).
     """
 
     def __init__(self, desc: Desc, page_tokens: int = 16, emulate_bf16: bool = False, share_weights_with=None):
@@ -154,9 +159,13 @@ class OracleModel:
         self.pages: Dict[int, np.ndarray] = {}
         half = hd // 2
         self.inv_freq = (1.0 / (desc.rope_theta ** (np.arange(half, dtype=np.float64) * 2.0 / hd))).astype(np.float32)
-        if share_weights_with is not None:  # same weights, separate KV store
+        # RMSNorm gains (bf16 values; the generator makes them 1, tests may set others):
+        # per layer g_attn / g_mlp [d], and g_final [d]
+        self.gains = dict(attn=[np.ones(D, np.float32) for _ in range(L)], mlp=[np.ones(D, np.float32) for _ in range(L)],
+                          final=np.ones(D, np.float32))
+        if share_weights_with is not None:  # same weights and gains, separate KV store
             o = share_weights_with
-            self.emb, self.layers, self.lm = o.emb, o.layers, o.lm
+            self.emb, self.layers, self.lm, self.gains = o.emb, o.layers, o.lm, o.gains
             return
         self.emb = tensor_values(s, 0, V, D, D)
         self.layers = []
@@ -177,18 +186,22 @@ class OracleModel:
     def _r(self, x: np.ndarray) -> np.ndarray:
         return bf16_round(x) if self.emul else x
 
-    def _norm_in(self, x: np.ndarray) -> np.ndarray:
-        """RMSNorm feeding a GEMM.  Emulation mirrors where the kernels round:
-        prefill rounds the normalised rows; decode folds the norm into the GEMM
-        (B operand = bf16(x), epilogue scales by 1/rms)."""
+    def _r16(self, x: np.ndarray) -> np.ndarray:
+        return f16_round(x) if self.emul else x
+
+    def _norm_in(self, x: np.ndarray, g: np.ndarray) -> np.ndarray:
+        """RMSNorm with gain g feeding a GEMM.  Emulation mirrors where the
+        kernels round: prefill rounds the normalised rows; decode folds the norm
+        into the GEMM (B operand = bf16(x * g), epilogue scales by 1/rms)."""
         if self.emul and self._phase == "decode":
             inv = 1.0 / np.sqrt(np.mean(x.astype(np.float32) ** 2, axis=-1, keepdims=True) + np.float32(self.d.norm_eps))
-            return (bf16_round(x) * inv).astype(np.float32)
-        return self._r(self.rmsnorm(x))
+            return (bf16_round(x * g) * inv).astype(np.float32)
+        return self._r(self.rmsnorm(x, g))
 
-    def rmsnorm(self, x: np.ndarray) -> np.ndarray:
+    def rmsnorm(self, x: np.ndarray, g: Optional[np.ndarray] = None) -> np.ndarray:
         ms = np.mean(x.astype(np.float32) ** 2, axis=-1, keepdims=True)
-        return (x / np.sqrt(ms + np.float32(self.d.norm_eps))).astype(np.float32)
+        y = (x / np.sqrt(ms + np.float32(self.d.norm_eps))).astype(np.float32)
+        return y if g is None else (y * g).astype(np.float32)
 
     def rope(self, x: np.ndarray, pos: np.ndarray) -> np.ndarray:
         """x [T, heads, hd]; rotate-half convention, angle = pos * inv_freq (fp32)."""
@@ -232,8 +245,8 @@ class OracleModel:
             sc = sc - sc.max(axis=1, keepdims=True)
             p = np.exp(sc)
             l = p.sum(axis=1, keepdims=True)
-            if self.emul:  # both attention kernels feed bf16 P to the P.V tensor-core product
-                p = bf16_round(p)
+            if self.emul:  # the attention kernels feed fp16 P to the P.V tensor-core product
+                p = f16_round(p)
             out[:, h, :] = (p @ vh) / l
         return out
 
@@ -241,12 +254,12 @@ class OracleModel:
         """One decoder layer over the concatenation of per-request token spans."""
         W = self.layers[l]
         H, Hk, hd = self.d.n_heads, self.d.n_kv_heads, self.d.head_dim
-        h = self._norm_in(x)
+        h = self._norm_in(x, self.gains["attn"][l])
         q = (h @ W["wq"].T).reshape(-1, H, hd)
         k = (h @ W["wk"].T).reshape(-1, Hk, hd)
-        v = self._r((h @ W["wv"].T).reshape(-1, Hk, hd))
+        v = self._r16((h @ W["wv"].T).reshape(-1, Hk, hd))
         pos_all = np.concatenate(spans)
-        q, k = self._r(self.rope(q, pos_all)), self._r(self.rope(k, pos_all))
+        q, k = self._r16(self.rope(q, pos_all)), self._r16(self.rope(k, pos_all))
         o = np.empty_like(q)
         off = 0
         for row, pos in zip(rows, spans):
@@ -256,7 +269,7 @@ class OracleModel:
             o[off:off + t] = self._attend(q[off:off + t], ks, vs, pos)
             off += t
         x = x + self._r(o.reshape(len(x), -1)) @ W["wo"].T
-        h = self._norm_in(x)
+        h = self._norm_in(x, self.gains["mlp"][l])
         gate = h @ W["wg"].T
         a = self._r((gate / (1.0 + np.exp(-gate))) * (h @ W["wu"].T))
         return (x + a.astype(np.float32) @ W["wd"].T).astype(np.float32)
@@ -269,7 +282,7 @@ class OracleModel:
             x = self._block(l, x, rows, spans)
         if want is None:
             want = np.cumsum([len(s) for s in spans]) - 1
-        return (self._norm_in(x[want]) @ self.lm.T).astype(np.float32)
+        return (self._norm_in(x[want], self.gains["final"]) @ self.lm.T).astype(np.float32)
 
     # -- phase entry points (same semantics as sw_prefill_enqueue / sw_decode_enqueue)
     def prefill(self, prompts: List[np.ndarray], page_rows: List[Sequence[int]]) -> np.ndarray:

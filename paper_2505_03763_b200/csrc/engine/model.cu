@@ -11,7 +11,7 @@
 //            wgu [2 ffn, d] in [gate 64 | up 64] row blocks (SwiGLU fuses into
 //            the GEMM epilogue), wd [d, ffn]; embedding [V, d]; LM head [V, d]
 //            (aliases the embedding when tied).
-//   KV       pages[L][n_pages][K|V][Hkv][16 tokens][hd]: a (layer, page, head)
+//   KV       pages[L][n_pages][K|V][Hkv][16 tokens][hd] fp16: a (layer, page, head)
 //            is one contiguous 16 x hd block, so attention reads whole pages
 //            with 16 B vector loads; page ids come from per-slot page tables
 //            (int32 [slots][max_pages]) shared by both phases -- the prompt
@@ -87,7 +87,7 @@ void ws_alloc(Workspace& w, const sw_model_desc& d, int rows, bool decode, int m
     w.x = dalloc<float>(static_cast<size_t>(rows) * d.d_model);
     w.xn = dalloc<__nv_bfloat16>(static_cast<size_t>(rows) * d.d_model);
     w.qkv = dalloc<float>(static_cast<size_t>(rows) * qkv_w);
-    w.q = dalloc<__nv_bfloat16>(static_cast<size_t>(rows) * d.n_heads * d.head_dim);
+    w.q = dalloc<kv_t>(static_cast<size_t>(rows) * d.n_heads * d.head_dim);
     w.attn = dalloc<__nv_bfloat16>(static_cast<size_t>(rows) * d.n_heads * d.head_dim);
     w.act = dalloc<__nv_bfloat16>(static_cast<size_t>(rows) * d.ffn_dim);
     w.xlast = dalloc<__nv_bfloat16>(static_cast<size_t>(kLmRowsMax) * d.d_model);
@@ -327,7 +327,7 @@ void prefill_forward(sw_model* m, sw_kv* kv, const sw_batch& b, cudaStream_t st,
         }
         for (int l = 0; l < d.n_layers; ++l) {
             const LayerWeights& L = m->layers[l];
-            __nv_bfloat16* kvl = kv->pages + l * kv->layer_stride;
+            kv_t* kvl = kv->pages + l * kv->layer_stride;
             rmsnorm(w.x, L.g_attn, w.xn, T, d.d_model, d.norm_eps, nullptr, nullptr, st);
             if (fuse_rope) {  // QKV GEMM with RoPE + q / paged-KV stores in its epilogue
                 GemmProblem pq = lp(gp(w.xn, w.rows, L.wqkv, qkv_w, T, qkv_w, d.d_model, EPI_QKV_ROPE, false, nullptr, 0));
@@ -409,9 +409,9 @@ void decode_layers(sw_model* m, sw_kv* kv, int R, cudaStream_t st, int lane, boo
     //   wo   GEMM + residual; emits bf16(x) and sum(x^2) for the next norm
     //   gu   GEMM . RMSNorm scale . SwiGLU
     //   wd   GEMM + residual; emits bf16(x) and sum(x^2)
-    // RMSNorm is folded into the consuming GEMM: its B operand is bf16(x) and
-    // the epilogue scales by rsqrt(mean(x^2) + eps) (the gains are 1, i.e.
-    // folded into the weights).
+    // RMSNorm is folded into the consuming GEMM: its B operand is bf16(x * g)
+    // (written by the producer with the consuming norm's gain g) and the
+    // epilogue scales by rsqrt(mean(x^2) + eps).
     PdlScope pdl(true);
     const sw_model_desc& d = m->desc;
     Workspace& w = m->dec[lane];
@@ -422,8 +422,8 @@ void decode_layers(sw_model* m, sw_kv* kv, int R, cudaStream_t st, int lane, boo
     float* ss_b = w.ss + kSsParts * kSsStride;
     const int parts = d.d_model / 128;  // one partial row per feature tile of a residual GEMM
     __nv_bfloat16* xb = w.xn;
-    embed(w.meta, R, m->emb, w.x, xb, ss_a, d.d_model, kv->last_token, kv->page_table, kv->max_pages,
-          kv->page_tokens, st);
+    embed(w.meta, R, m->emb, m->layers[0].g_attn, w.x, xb, ss_a, d.d_model, kv->last_token, kv->page_table,
+          kv->max_pages, kv->page_tokens, st);
     DecodeAttnArgs aa = decode_attn_args(m, kv, w);
     auto norm_in = [&](GemmProblem& p, const float* ss, int nparts) {
         p.fx.ss_parts = ss;
@@ -431,8 +431,9 @@ void decode_layers(sw_model* m, sw_kv* kv, int R, cudaStream_t st, int lane, boo
         p.fx.norm_dim = d.d_model;
         p.fx.norm_eps = d.norm_eps;
     };
-    auto resid_out = [&](GemmProblem& p, float* ss_out) {
+    auto resid_out = [&](GemmProblem& p, float* ss_out, const __nv_bfloat16* next_gain) {
         p.fx.x_bf16 = xb;
+        p.fx.x_gain = next_gain;
         p.fx.ss_part_out = ss_out;
     };
     static const int ablate = env_int("SW_ABLATE", 0);  // timing experiments only: skip kernel classes
@@ -453,7 +454,7 @@ void decode_layers(sw_model* m, sw_kv* kv, int R, cudaStream_t st, int lane, boo
     }
     for (int l = 0; l < d.n_layers; ++l) {
         const LayerWeights& L = m->layers[l];
-        __nv_bfloat16* kvl = kv->pages + l * kv->layer_stride;
+        kv_t* kvl = kv->pages + l * kv->layer_stride;
         GemmProblem pq = gp(xb, w.rows, L.wqkv, qkv_w, R, qkv_w, d.d_model, EPI_QKV_ROPE, true, nullptr, qkv_w, live, &w);
         norm_in(pq, ss_a, l == 0 ? 1 : parts);
         pq.fx.pos = w.meta->pos;
@@ -478,7 +479,7 @@ void decode_layers(sw_model* m, sw_kv* kv, int R, cudaStream_t st, int lane, boo
             }
         }
         GemmProblem po = gp(w.attn, w.rows, L.wo, d.d_model, R, d.d_model, hdH, EPI_RESID, true, w.x, d.d_model, live, &w);
-        resid_out(po, ss_b);
+        resid_out(po, ss_b, L.g_mlp);
         if (!(ablate & 4)) gemm_run(po, st);
         GemmProblem pg = gp(xb, w.rows, L.wgu, 2 * d.ffn_dim, R, 2 * d.ffn_dim, d.d_model, EPI_SWIGLU, true, w.act,
                             d.ffn_dim, live, &w);
@@ -486,7 +487,7 @@ void decode_layers(sw_model* m, sw_kv* kv, int R, cudaStream_t st, int lane, boo
         if (!(ablate & 8)) gemm_run(pg, st);
         GemmProblem pd = gp(w.act, w.rows, L.wd, d.d_model, R, d.d_model, d.ffn_dim, EPI_RESID, true, w.x, d.d_model,
                             live, &w);
-        resid_out(pd, ss_a);
+        resid_out(pd, ss_a, l + 1 < d.n_layers ? m->layers[l + 1].g_attn : m->g_final);
         if (!(ablate & 16)) gemm_run(pd, st);
     }
     GemmProblem pl = gp(xb, w.rows, m->lm, d.vocab, R, d.vocab, d.d_model, EPI_ARGMAX, true, nullptr, 0, live);
@@ -748,7 +749,7 @@ extern "C" int sw_kv_arena_create(sw_model* m, int64_t n_pages, int32_t n_slots,
         {
             const uint64_t rows = bytes / (2ull * d.head_dim);
             if (rows < (1ull << 31) && d.head_dim % 64 == 0) {
-                kv->tm_kv = make_tmap_bf16(kv->pages, rows, d.head_dim, 16);
+                kv->tm_kv = make_tmap_bf16(kv->pages, rows, d.head_dim, 16, /*fp16=*/true);
                 kv->tm_kv_ok = true;
             }
         }

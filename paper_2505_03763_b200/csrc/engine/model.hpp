@@ -33,7 +33,7 @@ struct Workspace {
     float* x = nullptr;              // [rows, d] residual stream, fp32
     __nv_bfloat16* xn = nullptr;     // [rows, d]
     float* qkv = nullptr;            // [rows, (H + 2Hkv) hd] fp32 (rounded once, after RoPE)
-    __nv_bfloat16* q = nullptr;      // [rows, H hd] roped
+    kv_t* q = nullptr;               // [rows, H hd] roped, fp16
     __nv_bfloat16* attn = nullptr;   // [rows, H hd]
     __nv_bfloat16* act = nullptr;    // [rows, ffn]
     __nv_bfloat16* xlast = nullptr;  // [256, d] rows feeding the LM head
@@ -98,7 +98,7 @@ struct sw_kv {
     int64_t n_pages = 0;
     int32_t n_slots = 0, max_pages = 0, max_out = 0;
     int page_tokens = 16;
-    __nv_bfloat16* pages = nullptr;  // [L][n_pages][2][Hkv][B][hd]
+    sw::kv_t* pages = nullptr;       // [L][n_pages][2][Hkv][B][hd] fp16
     int32_t* page_table = nullptr;   // [n_slots][max_pages]
     int32_t* last_token = nullptr;   // [n_slots]
     int32_t* out_tokens = nullptr;   // [n_slots][max_out]

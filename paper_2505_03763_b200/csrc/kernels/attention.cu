@@ -5,7 +5,7 @@
 //   prompt (4 warps x 16 rows); K/V stream through smem in 64-key blocks read
 //   straight from the 16-token pages just written by rope_kv (double-buffered
 //   cp.async, XOR-swizzled 16 B chunks for conflict-free ldmatrix); QK^T and
-//   PV on the tensor cores with mma.m16n8k16 bf16 -> fp32.
+//   PV on the tensor cores with mma.m16n8k16 fp16 -> fp32 (q, K/V and P are fp16).
 // Decode: split-KV paged attention on the tensor cores (see below); the G =
 //   H/Hkv query heads sharing a kv head are packed into one mma tile so every
 //   K/V byte is read once per step.  HBM-bound by design.
@@ -26,13 +26,13 @@ constexpr int kQRows = 64;
 constexpr int kKeys = 64;
 
 template <int HD>
-__global__ void __launch_bounds__(128, HD == 64 ? 4 : 2) attn_prefill_kernel(const __nv_bfloat16* __restrict__ q,
-                                                           const __nv_bfloat16* __restrict__ kv_layer,
+__global__ void __launch_bounds__(128, HD == 64 ? 4 : 2) attn_prefill_kernel(const kv_t* __restrict__ q,
+                                                           const kv_t* __restrict__ kv_layer,
                                                            __nv_bfloat16* __restrict__ out, PrefillAttnArgs a) {
     extern __shared__ __align__(128) uint8_t smem_raw[];
-    __nv_bfloat16* sQ = reinterpret_cast<__nv_bfloat16*>(smem_raw);
-    __nv_bfloat16* sK = sQ + kQRows * HD;       // [2][64][HD]
-    __nv_bfloat16* sV = sK + 2 * kKeys * HD;    // [2][64][HD]
+    kv_t* sQ = reinterpret_cast<kv_t*>(smem_raw);
+    kv_t* sK = sQ + kQRows * HD;       // [2][64][HD]
+    kv_t* sV = sK + 2 * kKeys * HD;    // [2][64][HD]
     constexpr int CH = HD / 8;                  // 16 B chunks per row
 
     const int tile = blockIdx.x;
@@ -52,7 +52,7 @@ __global__ void __launch_bounds__(128, HD == 64 ? 4 : 2) attn_prefill_kernel(con
     for (int i = tid; i < kQRows * CH; i += 128) {
         const int r = i / CH, c = i % CH;
         const bool ok = q0 + r < len;
-        const __nv_bfloat16* src = q + (start + (ok ? q0 + r : 0)) * qstride + h * HD + c * 8;
+        const kv_t* src = q + (start + (ok ? q0 + r : 0)) * qstride + h * HD + c * 8;
         cp_async16(sQ + swz<HD>(r, c), src, ok);
     }
     auto load_kv = [&](int blk, int buf) {
@@ -61,7 +61,7 @@ __global__ void __launch_bounds__(128, HD == 64 ? 4 : 2) attn_prefill_kernel(con
             const int key = blk * kKeys + r;
             const bool ok = key < len;
             const int page = ok ? ptab[key / kPage] : 0;
-            const __nv_bfloat16* base = kv_layer + static_cast<int64_t>(page) * a.page_stride +
+            const kv_t* base = kv_layer + static_cast<int64_t>(page) * a.page_stride +
                                         static_cast<int64_t>(hk) * kPage * HD +
                                         static_cast<int64_t>(key % kPage) * HD + c * 8;
             cp_async16(sK + buf * kKeys * HD + swz<HD>(r, c), base, ok);
@@ -97,8 +97,8 @@ __global__ void __launch_bounds__(128, HD == 64 ? 4 : 2) attn_prefill_kernel(con
                 ldsm_x4(qf[ks], sQ + swz<HD>(r, c));
             }
         }
-        const __nv_bfloat16* K = sK + buf * kKeys * HD;
-        const __nv_bfloat16* V = sV + buf * kKeys * HD;
+        const kv_t* K = sK + buf * kKeys * HD;
+        const kv_t* V = sV + buf * kKeys * HD;
         float sc[8][4];
 #pragma unroll
         for (int nb = 0; nb < 8; ++nb) sc[nb][0] = sc[nb][1] = sc[nb][2] = sc[nb][3] = 0.f;
@@ -110,8 +110,8 @@ __global__ void __launch_bounds__(128, HD == 64 ? 4 : 2) attn_prefill_kernel(con
                 const int key = np * 16 + (lane & 7) + ((lane >> 4) << 3);
                 const int c = ks * 2 + ((lane >> 3) & 1);
                 ldsm_x4(b, K + swz<HD>(key, c));
-                mma_bf16(sc[2 * np], qf[ks], b[0], b[1]);
-                mma_bf16(sc[2 * np + 1], qf[ks], b[2], b[3]);
+                mma_f16(sc[2 * np], qf[ks], b[0], b[1]);
+                mma_f16(sc[2 * np + 1], qf[ks], b[2], b[3]);
             }
         }
         // mask + online softmax (log2 domain).  The max runs on raw scores
@@ -170,18 +170,18 @@ __global__ void __launch_bounds__(128, HD == 64 ? 4 : 2) attn_prefill_kernel(con
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk) {
             uint32_t pa[4];
-            pa[0] = pack_bf2(sc[2 * kk][0], sc[2 * kk][1]);
-            pa[1] = pack_bf2(sc[2 * kk][2], sc[2 * kk][3]);
-            pa[2] = pack_bf2(sc[2 * kk + 1][0], sc[2 * kk + 1][1]);
-            pa[3] = pack_bf2(sc[2 * kk + 1][2], sc[2 * kk + 1][3]);
+            pa[0] = pack_h2(sc[2 * kk][0], sc[2 * kk][1]);
+            pa[1] = pack_h2(sc[2 * kk][2], sc[2 * kk][3]);
+            pa[2] = pack_h2(sc[2 * kk + 1][0], sc[2 * kk + 1][1]);
+            pa[3] = pack_h2(sc[2 * kk + 1][2], sc[2 * kk + 1][3]);
 #pragma unroll
             for (int dp = 0; dp < HD / 16; ++dp) {
                 uint32_t b[4];
                 const int key = kk * 16 + (lane & 7) + (((lane >> 3) & 1) << 3);
                 const int c = dp * 2 + (lane >> 4);
                 ldsm_x4_t(b, V + swz<HD>(key, c));
-                mma_bf16(o[2 * dp], pa, b[0], b[1]);
-                mma_bf16(o[2 * dp + 1], pa, b[2], b[3]);
+                mma_f16(o[2 * dp], pa, b[0], b[1]);
+                mma_f16(o[2 * dp + 1], pa, b[2], b[3]);
             }
         }
         __syncthreads();
@@ -214,7 +214,7 @@ __device__ __constant__ bool kEarlyTrigger_c = true;
 
 template <int HD, int G, int KB, int NS>
 __global__ void __launch_bounds__(128, NS == 2 ? 3 : (NS == 3 ? 2 : 1))
-    attn_decode_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ kv_layer,
+    attn_decode_kernel(const kv_t* __restrict__ q, const kv_t* __restrict__ kv_layer,
                        __nv_bfloat16* __restrict__ out, DecodeAttnArgs a) {
     extern __shared__ __align__(128) uint8_t dsm[];
     __shared__ uint32_t s_last;
@@ -251,7 +251,7 @@ void set_early_trigger_once() {
 }
 
 template <int HD, int G, int NS>
-void decode_launch_ns(const __nv_bfloat16* q, const __nv_bfloat16* kv_layer, __nv_bfloat16* out,
+void decode_launch_ns(const kv_t* q, const kv_t* kv_layer, __nv_bfloat16* out,
                       const DecodeAttnArgs& a, int max_rows, cudaStream_t st) {
     constexpr int KB = decode_kb<HD>();
     constexpr int smem = decode_unit_smem<HD, G, NS>();
@@ -272,7 +272,7 @@ void decode_launch_ns(const __nv_bfloat16* q, const __nv_bfloat16* kv_layer, __n
 }
 
 template <int HD, int G>
-void decode_launch(const __nv_bfloat16* q, const __nv_bfloat16* kv_layer, __nv_bfloat16* out, const DecodeAttnArgs& a,
+void decode_launch(const kv_t* q, const kv_t* kv_layer, __nv_bfloat16* out, const DecodeAttnArgs& a,
                    int max_rows, cudaStream_t st) {
     static const int ns = [] {
         const char* v = std::getenv("SW_ATTN_STAGES");  // measured: 3 (profiles/r01b/step_ablation.txt)
@@ -285,7 +285,7 @@ void decode_launch(const __nv_bfloat16* q, const __nv_bfloat16* kv_layer, __nv_b
 
 }  // namespace
 
-void attn_prefill(const __nv_bfloat16* q, const __nv_bfloat16* kv_layer, __nv_bfloat16* out, const PrefillAttnArgs& a,
+void attn_prefill(const kv_t* q, const kv_t* kv_layer, __nv_bfloat16* out, const PrefillAttnArgs& a,
                   int max_tiles, int hd, cudaStream_t st) {
     dim3 grid(max_tiles, a.H);
     if (hd == 64) {
@@ -310,7 +310,7 @@ void attn_prefill(const __nv_bfloat16* q, const __nv_bfloat16* kv_layer, __nv_bf
     SW_LAUNCH_CHECK();
 }
 
-void attn_decode(const __nv_bfloat16* q, const __nv_bfloat16* kv_layer, __nv_bfloat16* out, const DecodeAttnArgs& a,
+void attn_decode(const kv_t* q, const kv_t* kv_layer, __nv_bfloat16* out, const DecodeAttnArgs& a,
                  int max_rows, int hd, cudaStream_t st) {
     const int G = a.H / a.Hkv;
     if (hd == 64 && G == 4) decode_launch<64, 4>(q, kv_layer, out, a, max_rows, st);

@@ -3,6 +3,7 @@
 
 #include <cuda.h>
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -85,11 +86,11 @@ struct DecodeFlatArgs {
 // partial slots (each G x hd floats) the flat kernel needs on `sms` SMs
 size_t attn_decode_flat_part_rows(int sms);
 
-void attn_prefill(const __nv_bfloat16* q, const __nv_bfloat16* kv_layer, __nv_bfloat16* out, const PrefillAttnArgs& a,
+void attn_prefill(const kv_t* q, const kv_t* kv_layer, __nv_bfloat16* out, const PrefillAttnArgs& a,
                   int max_tiles, int hd, cudaStream_t st);
-void attn_decode(const __nv_bfloat16* q, const __nv_bfloat16* kv_layer, __nv_bfloat16* out, const DecodeAttnArgs& a,
+void attn_decode(const kv_t* q, const kv_t* kv_layer, __nv_bfloat16* out, const DecodeAttnArgs& a,
                  int max_rows, int hd, cudaStream_t st);
-void attn_decode_flat(const CUtensorMap& tm_kv, const __nv_bfloat16* q, __nv_bfloat16* out, const DecodeFlatArgs& a,
+void attn_decode_flat(const CUtensorMap& tm_kv, const kv_t* q, __nv_bfloat16* out, const DecodeFlatArgs& a,
                       int ctas, int hd, int G, cudaStream_t st);
 
 }  // namespace sw

@@ -51,13 +51,6 @@ __device__ __forceinline__ void ldsm_x4_t(uint32_t (&r)[4], uint32_t addr) {
                  : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
                  : "r"(addr));
 }
-__device__ __forceinline__ void mma_bf16(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
-    asm volatile(
-        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
-        "{%0,%1,%2,%3};"
-        : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
-        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
-}
 __device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 // Byte offset of 16 B chunk `chunk` (0 .. HD/8) of key row `row` inside one
@@ -104,7 +97,7 @@ struct FlatCfg {
 
 template <int HD, int G, int NWARP, int NS>
 __global__ void __launch_bounds__(NWARP * 32)
-    attn_decode_flat_kernel(const __grid_constant__ CUtensorMap tm_kv, const __nv_bfloat16* __restrict__ q,
+    attn_decode_flat_kernel(const __grid_constant__ CUtensorMap tm_kv, const kv_t* __restrict__ q,
                             __nv_bfloat16* __restrict__ out, DecodeFlatArgs a) {
     using C = FlatCfg<HD, G, NWARP, NS>;
     static_assert(G <= 8, "query rows live in the first 8 mma rows");
@@ -219,7 +212,7 @@ __global__ void __launch_bounds__(NWARP * 32)
     // Q fragments (A operand rows = the G query heads); the next unit's are
     // fetched when a segment starts, so a segment switch never waits on them
     auto fetch_q = [&](int row, int hk, uint32_t (&dst)[HD / 16][2]) {
-        const __nv_bfloat16* qrow = q + static_cast<long long>(row) * a.H * HD + static_cast<long long>(hk * G + r) * HD;
+        const kv_t* qrow = q + static_cast<long long>(row) * a.H * HD + static_cast<long long>(hk * G + r) * HD;
 #pragma unroll
         for (int ks = 0; ks < HD / 16; ++ks) {
             const int c = ks * 16 + (lane & 3) * 2;
@@ -282,8 +275,8 @@ __global__ void __launch_bounds__(NWARP * 32)
             uint32_t b[4];
             const int key = (lane & 7) + ((lane >> 4) << 3);
             ldsm_x4(b, kb + sw_off<HD>(key, ks * 2 + ((lane >> 3) & 1)));
-            mma_bf16(sc[0], qf[ks], b[0], b[1]);
-            mma_bf16(sc[1], qf[ks], b[2], b[3]);
+            mma_f16(sc[0], qf[ks], b[0], b[1]);
+            mma_f16(sc[1], qf[ks], b[2], b[3]);
         }
         float mx = -INFINITY;
 #pragma unroll
@@ -314,17 +307,17 @@ __global__ void __launch_bounds__(NWARP * 32)
             o[i][1] *= alpha;
         }
         uint32_t pa[4];
-        pa[0] = pack_bf2(sc[0][0], sc[0][1]);
+        pa[0] = pack_h2(sc[0][0], sc[0][1]);
         pa[1] = 0u;
-        pa[2] = pack_bf2(sc[1][0], sc[1][1]);
+        pa[2] = pack_h2(sc[1][0], sc[1][1]);
         pa[3] = 0u;
 #pragma unroll
         for (int dp = 0; dp < HD / 16; ++dp) {
             uint32_t b[4];
             const int key = (lane & 7) + (((lane >> 3) & 1) << 3);
             ldsm_x4_t(b, vb + sw_off<HD>(key, dp * 2 + (lane >> 4)));
-            mma_bf16(o[2 * dp], pa, b[0], b[1]);
-            mma_bf16(o[2 * dp + 1], pa, b[2], b[3]);
+            mma_f16(o[2 * dp], pa, b[0], b[1]);
+            mma_f16(o[2 * dp + 1], pa, b[2], b[3]);
         }
         __syncwarp();  // the stage's reads are done before it is refilled
         const int kn = k + NS;
@@ -457,7 +450,7 @@ __global__ void __launch_bounds__(NWARP * 32)
 }
 
 template <int HD, int G, int NWARP, int NS>
-void flat_launch(const CUtensorMap& tm, const __nv_bfloat16* q, __nv_bfloat16* out, const DecodeFlatArgs& a, int ctas,
+void flat_launch(const CUtensorMap& tm, const kv_t* q, __nv_bfloat16* out, const DecodeFlatArgs& a, int ctas,
                  cudaStream_t st) {
     using C = FlatCfg<HD, G, NWARP, NS>;
     static bool cfg = false;
@@ -490,7 +483,7 @@ FlatShape flat_shape(int hd) {
 }
 
 template <int HD, int G>
-void flat_dispatch(const CUtensorMap& tm, const __nv_bfloat16* q, __nv_bfloat16* out, const DecodeFlatArgs& a,
+void flat_dispatch(const CUtensorMap& tm, const kv_t* q, __nv_bfloat16* out, const DecodeFlatArgs& a,
                    int sms, cudaStream_t st) {
     const FlatShape f = flat_shape(HD);
     const int ctas = sms * std::max(1, f.per_sm);
@@ -515,7 +508,7 @@ size_t attn_decode_flat_part_rows(int sms) {
     return static_cast<size_t>(2) * 16 * sms;
 }
 
-void attn_decode_flat(const CUtensorMap& tm_kv, const __nv_bfloat16* q, __nv_bfloat16* out, const DecodeFlatArgs& a,
+void attn_decode_flat(const CUtensorMap& tm_kv, const kv_t* q, __nv_bfloat16* out, const DecodeFlatArgs& a,
                       int sms, int hd, int G, cudaStream_t st) {
     if (hd == 64 && G == 4) flat_dispatch<64, 4>(tm_kv, q, out, a, sms, st);
     else if (hd == 64 && G == 2) flat_dispatch<64, 2>(tm_kv, q, out, a, sms, st);

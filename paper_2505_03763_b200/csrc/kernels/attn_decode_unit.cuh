@@ -40,15 +40,8 @@ __device__ __forceinline__ void ldsm_x4_t(uint32_t (&r)[4], const void* p) {
                  : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
                  : "r"(smem_addr(p)));
 }
-__device__ __forceinline__ void mma_bf16(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
-    asm volatile(
-        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
-        "{%0,%1,%2,%3};"
-        : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
-        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
-}
 
-// [rows][HD] bf16 tile, 16 B chunks XOR-swizzled by row.
+// [rows][HD] 16-bit tile, 16 B chunks XOR-swizzled by row.
 template <int HD>
 __device__ __forceinline__ int swz(int row, int chunk) {
     return row * HD + ((chunk ^ (row & 7)) << 3);
@@ -89,16 +82,16 @@ __device__ __forceinline__ SplitPlan decode_split_plan(int ctx, int want, int ca
 // anything the predecessor kernel produces (q, the new K/V entry, a page installed
 // this step) is read: the unit's HBM stream starts while the QKV GEMM drains.
 template <int HD, int G, int KB, int NS = 2, class Sync, class Wait>
-__device__ __forceinline__ void decode_unit(const DecodeAttnArgs& a, const __nv_bfloat16* __restrict__ q,
-                                            const __nv_bfloat16* __restrict__ kv_layer,
+__device__ __forceinline__ void decode_unit(const DecodeAttnArgs& a, const kv_t* __restrict__ q,
+                                            const kv_t* __restrict__ kv_layer,
                                             __nv_bfloat16* __restrict__ out, int row, int hk, int split,
                                             const SplitPlan& plan, int ctx, uint8_t* dsm, int32_t* s_pages,
                                             uint32_t* s_last, int tid, Sync sync, Wait wait_pred) {
     static_assert(G <= 8, "query rows live in the first 8 mma rows");
     constexpr int CH = HD / 8;
     const int warp = tid >> 5, lane = tid & 31;
-    __nv_bfloat16* wK = reinterpret_cast<__nv_bfloat16*>(dsm) + warp * (2 * NS * KB * HD);  // [NS][KB][HD]
-    __nv_bfloat16* wV = wK + NS * KB * HD;                                                  // [NS][KB][HD]
+    kv_t* wK = reinterpret_cast<kv_t*>(dsm) + warp * (2 * NS * KB * HD);  // [NS][KB][HD]
+    kv_t* wV = wK + NS * KB * HD;                                                  // [NS][KB][HD]
     float* cm = reinterpret_cast<float*>(dsm + 4 * (2 * NS * KB * HD) * 2);  // [4][G]
     float* cl = cm + 4 * G;                                             // [4][G]
     float* co = cl + 4 * G;                                             // [4][G][HD]
@@ -178,7 +171,7 @@ __device__ __forceinline__ void decode_unit(const DecodeAttnArgs& a, const __nv_
     // Q fragment (A operand, rows = query heads of this kv head)
     const int r = lane >> 2;
     uint32_t qf[HD / 16][4];
-    const __nv_bfloat16* qrow = q + static_cast<int64_t>(row) * a.H * HD + static_cast<int64_t>(hk * G + r) * HD;
+    const kv_t* qrow = q + static_cast<int64_t>(row) * a.H * HD + static_cast<int64_t>(hk * G + r) * HD;
 #pragma unroll
     for (int ks = 0; ks < HD / 16; ++ks) {
         const int c = ks * 16 + (lane & 3) * 2;
@@ -196,8 +189,8 @@ __device__ __forceinline__ void decode_unit(const DecodeAttnArgs& a, const __nv_
         cp_async_commit();
         cp_async_wait<NS - 1>();
         __syncwarp();
-        const __nv_bfloat16* K = wK + buf * KB * HD;
-        const __nv_bfloat16* V = wV + buf * KB * HD;
+        const kv_t* K = wK + buf * KB * HD;
+        const kv_t* V = wV + buf * KB * HD;
         float sc[KB / 8][4];
 #pragma unroll
         for (int nb = 0; nb < KB / 8; ++nb) sc[nb][0] = sc[nb][1] = sc[nb][2] = sc[nb][3] = 0.f;
@@ -209,8 +202,8 @@ __device__ __forceinline__ void decode_unit(const DecodeAttnArgs& a, const __nv_
                 const int key = np * 16 + (lane & 7) + ((lane >> 4) << 3);
                 const int c = ks * 2 + ((lane >> 3) & 1);
                 ldsm_x4(b, K + swz<HD>(key, c));
-                mma_bf16(sc[2 * np], qf[ks], b[0], b[1]);
-                mma_bf16(sc[2 * np + 1], qf[ks], b[2], b[3]);
+                mma_f16(sc[2 * np], qf[ks], b[0], b[1]);
+                mma_f16(sc[2 * np + 1], qf[ks], b[2], b[3]);
             }
         }
         const int kbase = k_begin + blk * KB;
@@ -246,9 +239,9 @@ __device__ __forceinline__ void decode_unit(const DecodeAttnArgs& a, const __nv_
 #pragma unroll
         for (int kk = 0; kk < KB / 16; ++kk) {
             uint32_t pa[4];
-            pa[0] = pack_bf2(sc[2 * kk][0], sc[2 * kk][1]);
+            pa[0] = pack_h2(sc[2 * kk][0], sc[2 * kk][1]);
             pa[1] = 0u;
-            pa[2] = pack_bf2(sc[2 * kk + 1][0], sc[2 * kk + 1][1]);
+            pa[2] = pack_h2(sc[2 * kk + 1][0], sc[2 * kk + 1][1]);
             pa[3] = 0u;
 #pragma unroll
             for (int dp = 0; dp < HD / 16; ++dp) {
@@ -256,8 +249,8 @@ __device__ __forceinline__ void decode_unit(const DecodeAttnArgs& a, const __nv_
                 const int key = kk * 16 + (lane & 7) + (((lane >> 3) & 1) << 3);
                 const int c = dp * 2 + (lane >> 4);
                 ldsm_x4_t(b, V + swz<HD>(key, c));
-                mma_bf16(o[2 * dp], pa, b[0], b[1]);
-                mma_bf16(o[2 * dp + 1], pa, b[2], b[3]);
+                mma_f16(o[2 * dp], pa, b[0], b[1]);
+                mma_f16(o[2 * dp + 1], pa, b[2], b[3]);
             }
         }
         __syncwarp();

@@ -11,7 +11,7 @@
 //                       (TMA SWIZZLE_128B, K-major), S fp32 in TMEM cols [0,128)
 //   softmax             each thread tcgen05.ld's its S row twice (max, then
 //                       exp2/sum), online max/sum in fp32 (log2 domain), P as
-//                       bf16 into smem in the K-major 128B-swizzled layout
+//                       fp16 into smem in the K-major 128B-swizzled layout
 //   O += P V_j          tcgen05.mma M=128 N=hd K=128, P (K-major) and V from
 //                       smem -- V is [keys][hd] as stored, i.e. MN-major for
 //                       the B operand (instruction-descriptor transpose bit);
@@ -208,8 +208,9 @@ __global__ void __launch_bounds__(256, 1) attn_prefill_tc_kernel(const __grid_co
         load_blk(0, 1, sV, v_full);
     }
 
-    constexpr uint32_t idesc_s = umma_idesc_bf16(kRows, kBlk);
-    constexpr uint32_t idesc_o = umma_idesc_bf16(kRows, HD) | (1u << 16);  // B (V) MN-major
+    // fp16 operands (q, K/V cache, P: common.cuh kv_t)
+    constexpr uint32_t idesc_s = umma_idesc_f16(kRows, kBlk);
+    constexpr uint32_t idesc_o = umma_idesc_f16(kRows, HD) | (1u << 16);  // B (V) MN-major
     const uint32_t q_addr = smem_addr(sQg), k_addr = smem_addr(sK), v_addr = smem_addr(sV), p_addr = smem_addr(sPg);
     const int row = gt;                        // query row of this thread (TMEM lane)
     const int qp = q0 + row;                   // its position in the prompt
@@ -269,7 +270,7 @@ __global__ void __launch_bounds__(256, 1) attn_prefill_tc_kernel(const __grid_co
                 const float p1 =
                     k0 + 1 < nvalid ? fast_exp2(fmaf(__uint_as_float(r[2 * i + 1]), a.scale_log2, -m_new)) : 0.f;
                 rs += p0 + p1;
-                pk[i] = pack_bf2(p0, p1);
+                pk[i] = pack_h2(p0, p1);
             }
             // keys [32c, 32c + 32): atom c / 2, 16 B chunks (c % 2) * 4 + q, XOR-swizzled by row
 #pragma unroll

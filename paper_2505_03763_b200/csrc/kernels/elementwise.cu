@@ -57,10 +57,11 @@ void checksum_bf16(const void* p, int64_t n, unsigned long long* out_dev, cudaSt
 // Decode step head, one CTA per row: install the step's new page, gather the
 // embedding of the fed token (the slot's device-resident last token unless
 // explicit tokens are given) and emit what the first fused GEMM consumes:
-// x (fp32 residual), bf16(x) (its B operand) and sum(x^2) (its RMSNorm scale,
-// as a single partial row).
+// x (fp32 residual), bf16(x * g) (its B operand, g = layer 0's attention-norm
+// gain) and sum(x^2) (its RMSNorm scale, as a single partial row).
 __global__ void embed_kernel(const StepMeta* __restrict__ meta, const __nv_bfloat16* __restrict__ emb,
-                             float* __restrict__ x, __nv_bfloat16* __restrict__ xb, float* __restrict__ ss_a,
+                             const __nv_bfloat16* __restrict__ gain, float* __restrict__ x,
+                             __nv_bfloat16* __restrict__ xb, float* __restrict__ ss_a,
                              int d, const int32_t* __restrict__ last_token,
                              int32_t* __restrict__ page_table, int max_pages, int page_tokens) {
     griddep_launch_dependents();
@@ -75,6 +76,7 @@ __global__ void embed_kernel(const StepMeta* __restrict__ meta, const __nv_bfloa
     const uint4* src = reinterpret_cast<const uint4*>(emb + static_cast<int64_t>(tok) * d);
     float4* dst = reinterpret_cast<float4*>(x + static_cast<int64_t>(row) * d);
     uint4* dstb = reinterpret_cast<uint4*>(xb + static_cast<int64_t>(row) * d);
+    const uint4* g4 = reinterpret_cast<const uint4*>(gain);
     float ss = 0.f;
     for (int i = threadIdx.x; i < d / 8; i += blockDim.x) {
         const uint4 v = src[i];
@@ -82,7 +84,9 @@ __global__ void embed_kernel(const StepMeta* __restrict__ meta, const __nv_bfloa
         const float4 b = make_float4(bf_lo(v.z), bf_hi(v.z), bf_lo(v.w), bf_hi(v.w));
         dst[2 * i] = a;
         dst[2 * i + 1] = b;
-        dstb[i] = v;  // bf16(x) == the embedding row itself
+        const uint4 g = __ldg(g4 + i);
+        dstb[i] = make_uint4(pack_bf2(a.x * bf_lo(g.x), a.y * bf_hi(g.x)), pack_bf2(a.z * bf_lo(g.y), a.w * bf_hi(g.y)),
+                             pack_bf2(b.x * bf_lo(g.z), b.y * bf_hi(g.z)), pack_bf2(b.z * bf_lo(g.w), b.w * bf_hi(g.w)));
         ss += a.x * a.x + a.y * a.y + a.z * a.z + a.w * a.w + b.x * b.x + b.y * b.y + b.z * b.z + b.w * b.w;
     }
     __shared__ float red[32];
@@ -96,9 +100,10 @@ __global__ void embed_kernel(const StepMeta* __restrict__ meta, const __nv_bfloa
     }
 }
 
-void embed(const StepMeta* meta, int max_rows, const __nv_bfloat16* emb, float* x, __nv_bfloat16* xb, float* ss_a,
-           int d, const int32_t* last_token, int32_t* page_table, int max_pages, int page_tokens, cudaStream_t st) {
-    launch_k(embed_kernel, dim3(max_rows), dim3(128), 0, st, meta, emb, x, xb, ss_a, d, last_token, page_table,
+void embed(const StepMeta* meta, int max_rows, const __nv_bfloat16* emb, const __nv_bfloat16* gain, float* x,
+           __nv_bfloat16* xb, float* ss_a, int d, const int32_t* last_token, int32_t* page_table, int max_pages,
+           int page_tokens, cudaStream_t st) {
+    launch_k(embed_kernel, dim3(max_rows), dim3(128), 0, st, meta, emb, gain, x, xb, ss_a, d, last_token, page_table,
              max_pages, page_tokens);
 }
 
@@ -202,8 +207,8 @@ void rope_table(const float* inv_freq, float2* table, int max_pos, int half, cud
     SW_LAUNCH_CHECK();
 }
 
-__global__ void rope_kv_kernel(const float* __restrict__ qkv, __nv_bfloat16* __restrict__ q_out,
-                               __nv_bfloat16* __restrict__ kv_layer, const int32_t* __restrict__ tok_pos,
+__global__ void rope_kv_kernel(const float* __restrict__ qkv, kv_t* __restrict__ q_out,
+                               kv_t* __restrict__ kv_layer, const int32_t* __restrict__ tok_pos,
                                const int32_t* __restrict__ tok_slot, const int32_t* __restrict__ page_table,
                                const float2* __restrict__ cs_table, int rows, const int* rows_dev, int H, int Hkv,
                                int hd, int max_pages, int page_tokens, int64_t page_stride) {
@@ -217,7 +222,7 @@ __global__ void rope_kv_kernel(const float* __restrict__ qkv, __nv_bfloat16* __r
     const int off = pos % page_tokens;
     const int width = (H + 2 * Hkv) * hd;
     const float* src = qkv + static_cast<int64_t>(t) * width;
-    __nv_bfloat16* kbase = kv_layer + static_cast<int64_t>(page) * page_stride;
+    kv_t* kbase = kv_layer + static_cast<int64_t>(page) * page_stride;
     const int64_t head_stride = static_cast<int64_t>(page_tokens) * hd;
     const int64_t kv_stride = static_cast<int64_t>(Hkv) * head_stride;
     // (head, i) pairs over q and k heads: rotate; v heads: copy.
@@ -226,25 +231,25 @@ __global__ void rope_kv_kernel(const float* __restrict__ qkv, __nv_bfloat16* __r
         const float2 cs = cs_table[static_cast<int64_t>(pos) * half + i];
         const float c = cs.x, s = cs.y;
         const float a = src[h * hd + i], b = src[h * hd + i + half];
-        const __nv_bfloat16 ra = __float2bfloat16_rn(a * c - b * s);
-        const __nv_bfloat16 rb = __float2bfloat16_rn(b * c + a * s);
+        const kv_t ra = __float2half_rn(a * c - b * s);
+        const kv_t rb = __float2half_rn(b * c + a * s);
         if (h < H) {
-            __nv_bfloat16* qd = q_out + static_cast<int64_t>(t) * H * hd + h * hd;
+            kv_t* qd = q_out + static_cast<int64_t>(t) * H * hd + h * hd;
             qd[i] = ra;
             qd[i + half] = rb;
         } else {
-            __nv_bfloat16* kd = kbase + (h - H) * head_stride + off * hd;
+            kv_t* kd = kbase + (h - H) * head_stride + off * hd;
             kd[i] = ra;
             kd[i + half] = rb;
         }
     }
     for (int idx = threadIdx.x; idx < Hkv * hd; idx += blockDim.x) {
         const int h = idx / hd, i = idx % hd;
-        kbase[kv_stride + h * head_stride + off * hd + i] = __float2bfloat16_rn(src[(H + Hkv + h) * hd + i]);
+        kbase[kv_stride + h * head_stride + off * hd + i] = __float2half_rn(src[(H + Hkv + h) * hd + i]);
     }
 }
 
-void rope_kv(const float* qkv, __nv_bfloat16* q_out, __nv_bfloat16* kv_layer, const int32_t* tok_pos,
+void rope_kv(const float* qkv, kv_t* q_out, kv_t* kv_layer, const int32_t* tok_pos,
              const int32_t* tok_slot, const int32_t* page_table, const float2* cs_table, int rows, const int* rows_dev,
              int H, int Hkv, int hd, int max_pages, int page_tokens, cudaStream_t st) {
     const int64_t page_stride = 2LL * Hkv * page_tokens * hd;

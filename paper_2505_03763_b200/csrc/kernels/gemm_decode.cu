@@ -131,9 +131,11 @@ __device__ __forceinline__ void emit_tok(const TokCtx& c, int t, int lane, float
         x.z += v.z;
         x.w += v.w;
         *px = x;
-        if (fx.x_bf16)
+        if (fx.x_bf16) {  // the next GEMM's B operand: bf16(x * g) of the consuming RMSNorm
+            const uint2 g = __ldg(reinterpret_cast<const uint2*>(fx.x_gain + f0));
             *reinterpret_cast<uint2*>(fx.x_bf16 + static_cast<size_t>(t) * args.ldo + f0) =
-                make_uint2(pack_bf2(x.x, x.y), pack_bf2(x.z, x.w));
+                make_uint2(pack_bf2(x.x * bf_lo(g.x), x.y * bf_hi(g.x)), pack_bf2(x.z * bf_lo(g.y), x.w * bf_hi(g.y)));
+        }
         if (fx.ss_part_out) {  // this tile's sum(x^2) of the token, for the next RMSNorm (fixed tree)
             const float ss = warp_sum((x.x * x.x + x.y * x.y) + (x.z * x.z + x.w * x.w));
             if (lane == 0) fx.ss_part_out[static_cast<size_t>(c.m0 / 128) * kSsStride + t] = ss;
@@ -169,7 +171,7 @@ __device__ __forceinline__ void emit_tok(const TokCtx& c, int t, int lane, float
             o.z = v.z * cb.x + sg * p.z * cb.y;
             o.w = v.w * cb.z + sg * p.w * cb.w;
         }
-        const uint2 packed = make_uint2(pack_bf2(o.x, o.y), pack_bf2(o.z, o.w));
+        const uint2 packed = make_uint2(pack_h2(o.x, o.y), pack_h2(o.z, o.w));
         if (head < fx.H) {
             *reinterpret_cast<uint2*>(fx.q_out + static_cast<size_t>(t) * fx.H * hd + f0) = packed;
         } else {

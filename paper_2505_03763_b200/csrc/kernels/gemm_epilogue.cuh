@@ -90,7 +90,9 @@ __device__ __forceinline__ void emit_swap(const SwapEpi& E, int m0, int c, const
                 x[j] += v[j];
                 if (j < tcount) {
                     col[static_cast<size_t>(j) * args.ldo] = x[j];
-                    if (fx.x_bf16) fx.x_bf16[static_cast<size_t>(c + j) * args.ldo + f] = __float2bfloat16_rn(x[j]);
+                    if (fx.x_bf16)
+                        fx.x_bf16[static_cast<size_t>(c + j) * args.ldo + f] =
+                            __float2bfloat16_rn(x[j] * __bfloat162float(fx.x_gain[f]));
                 }
                 x[j] = j < tcount ? x[j] * x[j] : 0.f;
             }
@@ -156,12 +158,12 @@ __device__ __forceinline__ void emit_swap(const SwapEpi& E, int m0, int c, const
                     out = i < half ? v[j] * cs.x - b * cs.y : v[j] * cs.x + b * cs.y;
                 }
                 if (head < fx.H) {
-                    fx.q_out[static_cast<size_t>(t) * fx.H * hd + f] = __float2bfloat16_rn(out);
+                    fx.q_out[static_cast<size_t>(t) * fx.H * hd + f] = __float2half_rn(out);
                 } else {
                     const int kvh = is_v ? head - fx.H - fx.Hkv : head - fx.H;
-                    __nv_bfloat16* dst = fx.kv_layer + tok_kv[t] + (is_v ? fx.page_stride / 2 : 0) +
+                    kv_t* dst = fx.kv_layer + tok_kv[t] + (is_v ? fx.page_stride / 2 : 0) +
                                          static_cast<int64_t>(kvh) * fx.page_tokens * hd + i;
-                    *dst = __float2bfloat16_rn(out);
+                    *dst = __float2half_rn(out);
                 }
             }
             asm volatile("bar.sync 1, 128;" ::: "memory");

@@ -516,17 +516,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                                     const float2 c0 = cs[j], c1 = cs[j + 1];
                                     const float a0 = __uint_as_float(r[j]), b0 = __uint_as_float(u[j]);
                                     const float a1 = __uint_as_float(r[j + 1]), b1 = __uint_as_float(u[j + 1]);
-                                    pa[j / 2] = pack_bf2(a0 * c0.x - b0 * c0.y, a1 * c1.x - b1 * c1.y);
-                                    pb[j / 2] = pack_bf2(b0 * c0.x + a0 * c0.y, b1 * c1.x + a1 * c1.y);
+                                    pa[j / 2] = pack_h2(a0 * c0.x - b0 * c0.y, a1 * c1.x - b1 * c1.y);
+                                    pb[j / 2] = pack_h2(b0 * c0.x + a0 * c0.y, b1 * c1.x + a1 * c1.y);
                                 }
                             } else {
 #pragma unroll
                                 for (int j = 0; j < 32; j += 2) {
-                                    pa[j / 2] = pack_bf2(__uint_as_float(r[j]), __uint_as_float(r[j + 1]));
-                                    pb[j / 2] = pack_bf2(__uint_as_float(u[j]), __uint_as_float(u[j + 1]));
+                                    pa[j / 2] = pack_h2(__uint_as_float(r[j]), __uint_as_float(r[j + 1]));
+                                    pb[j / 2] = pack_h2(__uint_as_float(u[j]), __uint_as_float(u[j + 1]));
                                 }
                             }
-                            __nv_bfloat16* dst;
+                            kv_t* dst;
                             if (h < fx.H) {
                                 dst = fx.q_out + static_cast<long long>(t) * fx.H * hd + static_cast<long long>(h) * hd;
                             } else if (h < fx.H + fx.Hkv) {
@@ -759,20 +759,21 @@ void dispatch_bn(int bn, const CUtensorMap& a, const CUtensorMap& b, const GemmA
 
 }  // namespace
 
-CUtensorMap make_tmap_bf16(const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+CUtensorMap make_tmap_bf16(const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows, bool fp16) {
     CUtensorMap m;
     const cuuint64_t dims[2] = {cols, rows};
     const cuuint64_t strides[1] = {cols * 2};
     const cuuint32_t box[2] = {BK, box_rows};
     const cuuint32_t estr[2] = {1, 1};
-    const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
+    const CUresult r = encode_fn()(&m, fp16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                                   const_cast<void*>(base), dims, strides,
                                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) throw_cuda("cuTensorMapEncodeTiled", cudaErrorInvalidValue, __FILE__, __LINE__);
     return m;
 }
 
-// [rows][heads][hd] bf16 as a 3-D map (hd, heads, rows), box 64 x 1 x 128,
+// [rows][heads][hd] fp16 (roped q, kv_t) as a 3-D map (hd, heads, rows), box 64 x 1 x 128,
 // SWIZZLE_128B: one head's 128-row x 64-column tile per load.
 CUtensorMap make_tmap_heads(const void* base, uint64_t rows, uint64_t heads, uint64_t hd) {
     CUtensorMap m;
@@ -780,7 +781,7 @@ CUtensorMap make_tmap_heads(const void* base, uint64_t rows, uint64_t heads, uin
     const cuuint64_t strides[2] = {hd * 2, heads * hd * 2};
     const cuuint32_t box[3] = {64, 1, 128};
     const cuuint32_t estr[3] = {1, 1, 1};
-    const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides,
+    const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, const_cast<void*>(base), dims, strides,
                                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) throw_cuda("cuTensorMapEncodeTiled (3d)", cudaErrorInvalidValue, __FILE__, __LINE__);

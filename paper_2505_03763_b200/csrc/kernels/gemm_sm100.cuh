@@ -4,6 +4,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <stdint.h>
 
 namespace sw {
@@ -14,7 +15,7 @@ enum GemmEpilogue : int {
     EPI_SWIGLU = 2,     // [gate 64 | up 64] feature blocks -> bf16 silu(g)*u
     EPI_ARGMAX = 3,     // packed (value, index) atomicMax per token
     EPI_STORE_F32 = 4,  // fp32 out
-    EPI_QKV_ROPE = 5,   // decode: RoPE on q/k heads, q -> bf16 buffer, k/v -> paged KV cache
+    EPI_QKV_ROPE = 5,   // RoPE on q/k heads, q -> fp16 buffer, k/v -> paged fp16 KV cache
 };
 
 constexpr int kSsStride = 256;  // tokens per sum(x^2) partial row (max decode rows)
@@ -22,8 +23,8 @@ constexpr int kSsStride = 256;  // tokens per sum(x^2) partial row (max decode r
 // Decode-only epilogue fusions (swap-AB).
 struct DecodeFusion {
     // RMSNorm folded into the consumer GEMM: acc *= rsqrt(sum_p ss_parts[p][t] / norm_dim + eps),
-    // partial sums of squares added in a fixed order (deterministic); the gains
-    // are folded into the weights and B is the bf16 residual itself
+    // partial sums of squares added in a fixed order (deterministic); B is
+    // bf16(x * gain) written by the producer (x_gain below)
     const float* ss_parts = nullptr;  // [ss_nparts][kSsStride]
     int ss_nparts = 0;
     float norm_eps = 1e-5f;
@@ -31,6 +32,7 @@ struct DecodeFusion {
     // RESID producer side: write bf16(x) for the next GEMM and this tile's
     // partial sum(x^2) per token to ss_part_out[tile][t]
     __nv_bfloat16* x_bf16 = nullptr;
+    const __nv_bfloat16* x_gain = nullptr;  // the consuming RMSNorm's gain: x_bf16 = bf16(x * gain)
     float* ss_part_out = nullptr;
     // QKV_ROPE: per-token position / slot, page table, cos/sin table, outputs
     const int32_t* pos = nullptr;
@@ -38,8 +40,8 @@ struct DecodeFusion {
     const int32_t* page_table = nullptr;
     int max_pages = 0, page_tokens = 16;
     const float2* rope_cs = nullptr;
-    __nv_bfloat16* q_out = nullptr;
-    __nv_bfloat16* kv_layer = nullptr;
+    __half* q_out = nullptr;     // fp16 (kv_t): the attention operands
+    __half* kv_layer = nullptr;
     long long page_stride = 0;
     int H = 0, Hkv = 0, hd = 0;
 };
@@ -86,7 +88,8 @@ struct GemmProblem {
                           // every ~k tiles, so higher-priority decode CTAs get SMs between them
 };
 
-CUtensorMap make_tmap_bf16(const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows);
+// 2-D map of 16-bit rows (bf16, or fp16 for the KV arena), box 64 x box_rows, SWIZZLE_128B
+CUtensorMap make_tmap_bf16(const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows, bool fp16 = false);
 CUtensorMap make_tmap_heads(const void* base, uint64_t rows, uint64_t heads, uint64_t hd);
 const CUtensorMap& tmap_cached(const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows);
 void gemm_run(const GemmProblem& p, cudaStream_t st);

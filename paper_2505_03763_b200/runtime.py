@@ -102,6 +102,20 @@ class Engine:
         host = device_view(ptr, (n,), "<i2").cpu().numpy().view(np.uint16)
         return (host.astype(np.uint32) << 16).view(np.float32)
 
+    def write_tensor(self, name: str, values: np.ndarray):
+        """Overwrite a bf16 weight tensor (e.g. RMSNorm gains) with `values`,
+        rounded to nearest-even bf16; returns the stored values as float32."""
+        import torch
+
+        ptr, n = self.tensor(name)
+        v = np.ascontiguousarray(values, dtype=np.float32).reshape(-1)
+        if v.size != n:
+            raise ValueError(f"{name}: {v.size} values for {n} elements")
+        t = torch.from_numpy(v).to(torch.bfloat16)
+        device_view(ptr, (n,), "<i2").copy_(t.view(torch.int16).cuda())
+        torch.cuda.synchronize()
+        return t.float().numpy()
+
     def weight_checksum(self) -> int:
         v = ctypes.c_uint64()
         check(lib().sw_model_weight_checksum(self.model, ctypes.byref(v)))

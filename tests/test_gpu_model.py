@@ -1,15 +1,25 @@
 """Model-level parity of the CUDA path (through the C-ABI) with the CPU oracle.
 
-Bars:
-  * vs the oracle with the kernel's bf16 storage points emulated
-    (emulate_bf16=True): per-row relative L2 <= 1e-2 (the north-star bar;
-    what remains is accumulation order);
-  * vs the pure fp32 oracle: per-row relative L2 <= 2e-2 -- bf16 activation
-    rounding alone costs ~0.5-1% on these random-init models (DESIGN.md
-    "Parity"), so 1e-2 is reported, not asserted, there;
-  * greedy tokens identical to the fp32 oracle wherever its top-2 margin
-    exceeds 1e-2 * max|logit|; page tables bit exact.
+Bars (north star: "1e-2 relative for bf16 against the fp32 reference"; the
+row criterion of SURVEY.md §7), asserted against the PURE fp32 oracle:
+  * per-row relative L2 of the logits <= 1e-2, and
+  * elementwise |gpu - ref| <= 1e-2 * max|ref_row| for every row;
+  * greedy tokens identical wherever the oracle's top-2 margin exceeds
+    1e-2 * max|logit|;
+  * against the oracle with the kernels' 16-bit storage points emulated
+    (emulate_bf16=True) the same 1e-2 bars hold (what remains there is
+    accumulation order).
+The GEMM inputs are bf16 (RMSNorm outputs, attention output, SwiGLU output);
+the attention operands (q, the paged K/V cache, P) are fp16 -- a bf16 cache
+alone put tiny-model rows at 1.1-1.2% against fp32.
+Depth and shape coverage: the configs[0] tiny model; Llama-3.2-1B at full
+depth and vocabulary; Llama-3-8B at 4 layers with the full untied vocabulary;
+an 8192-token configs[4] prompt decoded past 8192; decode batches of 128-200
+live rows (the BN=128/256 decode GEMMs and the split-K reductions) and the
+batch invariance of one row's logits.
 """
+import dataclasses
+
 import numpy as np
 import pytest
 
@@ -19,16 +29,78 @@ from oracle import model as M
 
 pytestmark = pytest.mark.gpu
 
-LOGIT_RTOL = 1e-2       # vs emulated-format oracle
-LOGIT_RTOL_FP32 = 2e-2  # vs pure fp32 oracle
+LOGIT_RTOL = 1e-2
 
 
 def rel_rows(a, b):
     return np.linalg.norm(a - b, axis=-1) / np.linalg.norm(b, axis=-1)
 
 
+def elem_rows(a, b):
+    return np.abs(a - b).max(axis=-1) / np.abs(b).max(axis=-1)
+
+
 def margin_tol(ref_row):
     return LOGIT_RTOL * float(np.max(np.abs(ref_row)))
+
+
+class Bars:
+    """Accumulates per-row errors against the fp32 and the emulated oracle."""
+
+    def __init__(self, name):
+        self.name = name
+        self.r32, self.e32, self.rem, self.eem = [], [], [], []
+        self.tokens_checked = 0
+
+    def add(self, gpu, ref, emu=None):
+        self.r32.append(rel_rows(gpu, ref))
+        self.e32.append(elem_rows(gpu, ref))
+        if emu is not None:
+            self.rem.append(rel_rows(gpu, emu))
+            self.eem.append(elem_rows(gpu, emu))
+        for g, r in zip(gpu, ref):  # greedy token parity outside near-ties
+            if M.top2_margin(r) > margin_tol(r):
+                assert int(np.argmax(g)) == int(np.argmax(r)), self.name
+                self.tokens_checked += 1
+
+    def check(self):
+        r32, e32 = np.concatenate(self.r32), np.concatenate(self.e32)
+        msg = (f"\n{self.name}: vs fp32 rel-L2 max {r32.max():.4f} median {np.median(r32):.4f}, "
+               f"elementwise max {e32.max():.4f}; greedy tokens checked {self.tokens_checked}")
+        if self.rem:
+            rem, eem = np.concatenate(self.rem), np.concatenate(self.eem)
+            msg += f"; vs emulated rel-L2 max {rem.max():.4f} elementwise max {eem.max():.4f}"
+            assert rem.max() <= LOGIT_RTOL and eem.max() <= LOGIT_RTOL, msg
+        print(msg)
+        assert r32.max() <= LOGIT_RTOL, msg
+        assert e32.max() <= LOGIT_RTOL, msg
+
+
+def teacher_forced(eng, oracle, emu, lens, steps, name, rows=None, rid0=100, slots=None, pages_per=None):
+    """Prefill `lens`-token prompts, then `steps` decode steps fed with the
+    oracle's greedy tokens (teacher forcing), checking every logit row."""
+    d = eng.desc
+    n = len(lens)
+    slots = slots or list(range(n))
+    if rows is None:
+        per = pages_per or max((L + steps + 15) // 16 for L in lens)
+        rows = [[i * per + j for j in range(per)] for i in range(n)]
+    prompts = [M.prompt_tokens(d.seed, rid0 + i, L, d.vocab) for i, L in enumerate(lens)]
+    bars = Bars(name)
+    lg = eng.prefill(slots, prompts, [r[:(L + 15) // 16] for r, L in zip(rows, lens)])
+    ref = oracle.prefill(prompts, rows)
+    bars.add(lg, ref, emu.prefill(prompts, rows) if emu else None)
+    toks = [int(np.argmax(l)) for l in ref]
+    pos = list(lens)
+    for _ in range(steps):
+        newp = [rows[i][pos[i] // 16] if pos[i] % 16 == 0 else -1 for i in range(n)]
+        lg = eng.decode(slots, pos, tokens=toks, new_page=newp)
+        ref = oracle.decode(toks, pos, rows)
+        bars.add(lg, ref, emu.decode(toks, pos, rows) if emu else None)
+        toks = [int(np.argmax(l)) for l in ref]
+        pos = [p + 1 for p in pos]
+    bars.check()
+    return bars
 
 
 @pytest.fixture(scope="module")
@@ -68,52 +140,18 @@ def test_weights_bit_exact(tiny, tiny_oracle):
             assert np.array_equal(gu[128 * j + 64:128 * j + 128], W["wu"][64 * j:64 * j + 64])
         assert np.array_equal(tiny.tensor_numpy(f"layer{l}.wo").reshape(d.d_model, -1), W["wo"])
         assert np.array_equal(tiny.tensor_numpy(f"layer{l}.wd").reshape(d.d_model, F), W["wd"])
+        assert np.array_equal(tiny.tensor_numpy(f"layer{l}.g_attn"), np.ones(d.d_model, np.float32))
     assert np.array_equal(tiny.tensor_numpy("lm").reshape(d.vocab, d.d_model), o.lm)
 
 
 def test_prefill_then_decode_teacher_forced(tiny, tiny_oracle, tiny_emu):
-    d = M.TINY
-    o = tiny_oracle
-    errs_fp32, errs_emu = [], []
+    """configs[0] model: ragged prompts across page boundaries, 20 decode steps."""
     lens = [1, 15, 16, 17, 64, 100, 129]  # page-boundary edge cases, ragged batch
-    slots = list(range(10, 10 + len(lens)))
-    prompts = [M.prompt_tokens(d.seed, 100 + i, n, d.vocab) for i, n in enumerate(lens)]
     # disjoint page rows, deliberately non-contiguous ids
     rows = [[(i * 37 + j * 11) % 800 for j in range(16)] for i in range(len(lens))]
-    seen = set()
-    for r in rows:
-        for p in r:
-            assert p not in seen
-            seen.add(p)
-    lg = tiny.prefill(slots, prompts, [r[:(n + 15) // 16] for r, n in zip(rows, lens)])
-    ref = o.prefill(prompts, rows)
-    emu = tiny_emu.prefill(prompts, rows)
-    errs_fp32.append(rel_rows(lg, ref))
-    errs_emu.append(rel_rows(lg, emu))
-    toks = [int(np.argmax(l)) for l in ref]
-    for i, l in enumerate(ref):
-        if M.top2_margin(l) > margin_tol(l):
-            assert int(np.argmax(lg[i])) == toks[i]
-    pos = list(lens)
-    for step in range(20):
-        newp = [rows[i][pos[i] // 16] if pos[i] % 16 == 0 else -1 for i in range(len(lens))]
-        lg = tiny.decode(slots, pos, tokens=toks, new_page=newp)
-        ref = o.decode(toks, pos, rows)
-        emu = tiny_emu.decode(toks, pos, rows)
-        errs_fp32.append(rel_rows(lg, ref))
-        errs_emu.append(rel_rows(lg, emu))
-        nxt = []
-        for i, l in enumerate(ref):
-            if M.top2_margin(l) > margin_tol(l):
-                assert int(np.argmax(lg[i])) == int(np.argmax(l)), (step, i)
-            nxt.append(int(np.argmax(l)))  # teacher forcing with the oracle's token
-        toks = nxt
-        pos = [p + 1 for p in pos]
-    e32, eem = np.concatenate(errs_fp32), np.concatenate(errs_emu)
-    print(f"\nlogit rel-L2 vs fp32 oracle: max {e32.max():.4f} median {np.median(e32):.4f} "
-          f"frac<=1e-2 {np.mean(e32 <= 1e-2):.3f}; vs emulated-format oracle: max {eem.max():.4f}")
-    assert eem.max() < LOGIT_RTOL
-    assert e32.max() < LOGIT_RTOL_FP32
+    assert len({p for r in rows for p in r}) == 16 * len(lens)
+    teacher_forced(tiny, tiny_oracle, tiny_emu, lens, 20, "tiny teacher-forced", rows=rows,
+                   slots=list(range(10, 10 + len(lens))))
 
 
 def test_decode_uses_device_resident_token(tiny, tiny_oracle):
@@ -128,55 +166,152 @@ def test_decode_uses_device_resident_token(tiny, tiny_oracle):
     pos = [len(p) for p in prompts]
     lg_dev = tiny.decode(slots, pos, tokens=None, new_page=[-1] * 3)
     ref = tiny_oracle.decode(t1, pos, rows)
-    assert rel_rows(lg_dev, ref).max() < LOGIT_RTOL_FP32
+    assert rel_rows(lg_dev, ref).max() <= LOGIT_RTOL
+    assert elem_rows(lg_dev, ref).max() <= LOGIT_RTOL
 
 
-def _long_ctx_engine(desc, pages):
+def test_nonunit_rmsnorm_gains_prefill_and_decode():
+    """RMSNorm gains are read by both phases: prefill normalises with them, and
+    decode folds them into the B operand its residual GEMMs write
+    (bf16(x * g) for the consuming norm).  Random gains in [0.5, 1.5]; the
+    decode logits of token t at position p must match the prefill of the same
+    sequence through position p (prefill/decode agreement) and the oracle."""
     from paper_2505_03763_b200 import runtime
 
-    return runtime.Engine(desc, max_prefill_tokens=2048, max_decode_batch=8, n_pages=8 * pages + 8, n_slots=8,
-                          max_pages_per_slot=pages, max_out=16)
+    d = M.TINY
+    eng = runtime.Engine(d, max_prefill_tokens=2048, max_decode_batch=16, n_pages=512, n_slots=16,
+                         max_pages_per_slot=16, max_out=16)
+    try:
+        o = M.OracleModel(d)
+        rng = np.random.default_rng(7)
+        for l in range(d.n_layers):
+            o.gains["attn"][l] = eng.write_tensor(f"layer{l}.g_attn", rng.uniform(0.5, 1.5, d.d_model))
+            o.gains["mlp"][l] = eng.write_tensor(f"layer{l}.g_mlp", rng.uniform(0.5, 1.5, d.d_model))
+        o.gains["final"] = eng.write_tensor("g_final", rng.uniform(0.5, 1.5, d.d_model))
+        emu = M.OracleModel(d, emulate_bf16=True, share_weights_with=o)
+        bars = teacher_forced(eng, o, emu, [5, 31, 64, 90], 6, "tiny, non-unit gains", pages_per=8)
+        assert bars.tokens_checked > 0
+        # prefill of prompt + its first greedy token == the decode step that fed that token
+        p = M.prompt_tokens(d.seed, 900, 40, d.vocab)
+        lg = eng.prefill([8], [p], [[200, 201, 202]])
+        t1 = int(np.argmax(lg[0]))
+        dec = eng.decode([8], [40], tokens=[t1], new_page=[-1])
+        full = eng.prefill([9], [np.append(p, t1)], [[210, 211, 212]])
+        assert rel_rows(dec, full).max() <= LOGIT_RTOL
+        assert elem_rows(dec, full).max() <= LOGIT_RTOL
+    finally:
+        eng.close()
+
+
+def _engine(desc, pages_per, n_slots=8, max_decode=8, max_prefill=4096, n_pages=None):
+    from paper_2505_03763_b200 import runtime
+
+    return runtime.Engine(desc, max_prefill_tokens=max_prefill, max_decode_batch=max_decode,
+                          n_pages=n_pages or n_slots * pages_per + 8, n_slots=n_slots, max_pages_per_slot=pages_per,
+                          max_out=16)
 
 
 @pytest.mark.parametrize("shape", ["TINY", "LLAMA_1B_2L", "LLAMA_8B_1L"])
 def test_long_context_split_kv_and_split_k(shape):
     """Contexts long enough for several split-KV chunks (multi-split merge) and,
-    at the 1B and 8B widths, the cluster split-K decode GEMMs: 1B runs S = 8
-    (QKV, Wo, Wd) and 2 (gate/up); 8B (one layer, small vocabulary) runs the
-    GPC-headroom factors S = 5 (QKV) and 7 (Wo, Wd) and S = 1 (gate/up)."""
-    import dataclasses
-
+    at the 1B and 8B widths, the cluster split-K decode GEMMs."""
     if shape == "TINY":
         d = M.TINY
     elif shape == "LLAMA_1B_2L":
         d = dataclasses.replace(M.LLAMA_1B, n_layers=2)
     else:
         d = dataclasses.replace(M.LLAMA_8B, n_layers=1, vocab=4096)
-    pages = 80
-    eng = _long_ctx_engine(d, pages)
+    eng = _engine(d, 80)
     try:
         o = M.OracleModel(d)
         emu = M.OracleModel(d, emulate_bf16=True, share_weights_with=o)
         lens = [700, 1030] if shape != "LLAMA_8B_1L" else [300, 530]
-        prompts = [M.prompt_tokens(d.seed, 500 + i, n, d.vocab) for i, n in enumerate(lens)]
-        rows = [list(range(i * pages, (i + 1) * pages)) for i in range(2)]
-        lg = eng.prefill([0, 1], prompts, [r[:(n + 15) // 16] for r, n in zip(rows, lens)])
-        ref, em = o.prefill(prompts, rows), emu.prefill(prompts, rows)
-        e32, eem = [rel_rows(lg, ref)], [rel_rows(lg, em)]
+        teacher_forced(eng, o, emu, lens, 4, shape, pages_per=80, rid0=500)
+    finally:
+        eng.close()
+
+
+def test_llama1b_full_depth_full_vocab():
+    """Llama-3.2-1B shape at full depth (16 layers) and the full tied 128256-row
+    vocabulary: ragged prompts, 8 teacher-forced greedy steps."""
+    d = M.LLAMA_1B
+    eng = _engine(d, 40)
+    try:
+        o = M.OracleModel(d)
+        teacher_forced(eng, o, None, [1, 77, 256, 515], 8, "Llama-1B 16 layers", pages_per=40, rid0=1000)
+    finally:
+        eng.close()
+
+
+def test_llama8b_four_layers_full_untied_vocab():
+    """Llama-3-8B shape (hd 128, GQA 4, ffn 14336) at 4 layers with the full
+    untied 128256-row LM head: 8 teacher-forced greedy steps."""
+    d = dataclasses.replace(M.LLAMA_8B, n_layers=4)
+    eng = _engine(d, 40)
+    try:
+        o = M.OracleModel(d)
+        teacher_forced(eng, o, None, [3, 130, 333], 8, "Llama-8B 4 layers", pages_per=40, rid0=2000)
+    finally:
+        eng.close()
+
+
+def test_configs4_prompt_8192_decode_past_8192():
+    """configs[4] geometry: an 8192-token prompt (tcgen05 prefill attention over
+    64 key blocks) then decode at contexts 8193.. (flat decode attention over
+    >512 pages, split-KV), Llama-8B widths at 2 layers, full vocabulary."""
+    d = dataclasses.replace(M.LLAMA_8B, n_layers=2)
+    eng = _engine(d, 520, n_slots=2, max_prefill=8192)
+    try:
+        o = M.OracleModel(d)
+        teacher_forced(eng, o, None, [8192], 4, "8B 2 layers, prompt 8192", pages_per=520, rid0=3000)
+    finally:
+        eng.close()
+
+
+@pytest.mark.parametrize("shape,rows", [("LLAMA_1B_2L", 128), ("LLAMA_1B_2L", 200), ("LLAMA_8B_1L", 160)])
+def test_wide_decode_batch_and_batch_invariance(shape, rows):
+    """Decode batches of 128-200 live rows (BN = 128 / 256 decode GEMM tiles,
+    a warp taking several tokens in the split-K reduction) against the oracle,
+    and one row's logits alone (b=1) vs inside the wide batch: the split-K
+    factors depend on the weight shapes only, so the GEMM sums are batch
+    invariant; the attention kernel choice may change with the batch, so the
+    bar there is 1e-3 relative, not bit equality."""
+    if shape == "LLAMA_1B_2L":
+        d = dataclasses.replace(M.LLAMA_1B, n_layers=2, vocab=8192)
+    else:
+        d = dataclasses.replace(M.LLAMA_8B, n_layers=1, vocab=8192)
+    eng = _engine(d, 8, n_slots=rows + 1, max_decode=256, max_prefill=16384)
+    try:
+        o = M.OracleModel(d)
+        lens = [8 + (7 * i) % 57 for i in range(rows)]
+        prompts = [M.prompt_tokens(d.seed, 4000 + i, L, d.vocab) for i, L in enumerate(lens)]
+        prow = [list(range(i * 8, i * 8 + 8)) for i in range(rows)]
+        bars = Bars(f"{shape} b={rows}")
+        lg = eng.prefill(list(range(rows)), prompts, [r[:(L + 15) // 16] for r, L in zip(prow, lens)])
+        ref = o.prefill(prompts, prow)
+        bars.add(lg, ref)
         toks = [int(np.argmax(l)) for l in ref]
         pos = list(lens)
-        for _ in range(4):
-            newp = [rows[i][pos[i] // 16] if pos[i] % 16 == 0 else -1 for i in range(2)]
-            lg = eng.decode([0, 1], pos, tokens=toks, new_page=newp)
-            ref, em = o.decode(toks, pos, rows), emu.decode(toks, pos, rows)
-            e32.append(rel_rows(lg, ref))
-            eem.append(rel_rows(lg, em))
+        wide = None
+        for step in range(3):
+            newp = [prow[i][pos[i] // 16] if pos[i] % 16 == 0 else -1 for i in range(rows)]
+            lg = eng.decode(list(range(rows)), pos, tokens=toks, new_page=newp)
+            wide = lg if step == 0 else wide
+            ref = o.decode(toks, pos, prow)
+            bars.add(lg, ref)
             toks = [int(np.argmax(l)) for l in ref]
             pos = [p + 1 for p in pos]
-        e32, eem = np.concatenate(e32), np.concatenate(eem)
-        print(f"\n{shape}: rel-L2 vs fp32 max {e32.max():.4f}; vs emulated max {eem.max():.4f}")
-        assert eem.max() < LOGIT_RTOL
-        assert e32.max() < LOGIT_RTOL_FP32
+        bars.check()
+        assert bars.tokens_checked > rows
+        # row 0 again, alone, in a fresh slot and pages: the same first decode step
+        solo = list(range(rows * 8, rows * 8 + 8))
+        eng.prefill([rows], [prompts[0]], [solo[:(lens[0] + 15) // 16]])
+        t1 = int(np.argmax(o.prefill([prompts[0]], [solo])[0]))
+        newp = [solo[lens[0] // 16]] if lens[0] % 16 == 0 else [-1]
+        one = eng.decode([rows], [lens[0]], tokens=[t1], new_page=newp)
+        inv = rel_rows(one[0:1], wide[0:1]).max()
+        print(f"{shape}: row 0 at b=1 vs b={rows}: rel {inv:.2e}")
+        assert inv <= 1e-3
     finally:
         eng.close()
 
@@ -212,19 +347,24 @@ def test_attention_geometries_prefill_and_decode(shape, flat):
         rows = [[i + 8 * j for j in range(40)] for i in range(len(lens))]
         prompts = [M.prompt_tokens(d.seed, 700 + i, n, d.vocab) for i, n in enumerate(lens)]
         lg = eng.prefill(list(range(len(lens))), prompts, [r[:(n + 15) // 16] for r, n in zip(rows, lens)])
-        o = M.OracleModel(d, emulate_bf16=True)
-        ref = o.prefill(prompts, [r[:(n + 15) // 16] for r, n in zip(rows, lens)])
-        rel = np.linalg.norm(lg - ref, axis=1) / np.linalg.norm(ref, axis=1)
+        o = M.OracleModel(d)
+        e = M.OracleModel(d, emulate_bf16=True, share_weights_with=o)
+        pr = [r[:(n + 16) // 16] for r, n in zip(rows, lens)]
+        ref, em = o.prefill(prompts, pr), e.prefill(prompts, pr)
+        def bars(g, r):
+            return max((np.linalg.norm(g - r, axis=1) / np.linalg.norm(r, axis=1)).max(),
+                       (np.abs(g - r).max(axis=1) / np.abs(r).max(axis=1)).max())
         toks = [int(np.argmax(x)) for x in ref]
         newp = [rows[i][lens[i] // 16] if lens[i] % 16 == 0 else -1 for i in range(len(lens))]
         lg2 = eng.decode(list(range(len(lens))), lens, tokens=toks, new_page=newp)
-        ref2 = o.decode(toks, lens, [r[:(n + 16) // 16] for r, n in zip(rows, lens)])
-        rel2 = np.linalg.norm(lg2 - ref2, axis=1) / np.linalg.norm(ref2, axis=1)
+        ref2, em2 = o.decode(toks, lens, pr), e.decode(toks, lens, pr)
         eng.close()
-        print(float(rel.max()), float(rel2.max()))
+        print(bars(lg, ref), bars(lg2, ref2), bars(lg, em), bars(lg2, em2))
     """)
     env = dict(__import__("os").environ, SW_ATTN_FLAT=flat)
     p = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, timeout=600)
     assert p.returncode == 0, p.stderr[-2000:]
-    pre, dec = map(float, p.stdout.split()[-2:])
-    assert pre <= LOGIT_RTOL and dec <= LOGIT_RTOL, (pre, dec)
+    errs = list(map(float, p.stdout.split()[-4:]))
+    print(f"\n{shape} flat={flat}: prefill/decode vs fp32 {errs[0]:.4f}/{errs[1]:.4f}, vs emulated "
+          f"{errs[2]:.4f}/{errs[3]:.4f}")
+    assert max(errs) <= LOGIT_RTOL, errs
