@@ -18,10 +18,14 @@ semantics the reference does pin:
     entries = blocks_for(in+g) blocks (engine.hpp:316-319);
   * KV is paged in blocks of B=16 tokens (config.hpp:33) addressed through
     per-request page tables.
-Logit/token parity is therefore "parity unpinned" by any reference test; the
-weights/prompt generator IS pinned to the reference's SplitMix64
-(prng.hpp:10-35, checked against oracle/_ref/refsim --prng) and the page-table
-layout to the reference's KV ledger (gpu_model.hpp:79-135).
+No reference test pins logits or tokens; the weights/prompt generator IS
+pinned to the reference's SplitMix64 (prng.hpp:10-35, checked against
+oracle/_ref/refsim --prng) and the page-table layout to the reference's KV
+ledger (gpu_model.hpp:79-135).  The decoder math itself is pinned against an
+independent implementation instead: tests/test_oracle_hf.py loads the same
+weights (and non-unit norm gains) into HuggingFace transformers'
+LlamaForCausalLM and requires per-row logits within 2e-5 relative, prefill at
+every position and incremental paged decode.
 
 Synthetic inputs:
   tensor k, element i (row-major of its logical [out, in] shape):
