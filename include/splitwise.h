@@ -112,12 +112,23 @@ int sw_model_tensor(sw_model* model, const char* name, void** dev_ptr, int64_t* 
 int sw_kv_arena_create(sw_model* model, int64_t n_pages, int32_t n_slots, int32_t max_pages_per_slot,
                        int32_t max_out_tokens, sw_kv** out);
 int sw_kv_arena_destroy(sw_kv* kv);
+/* KV capacity of the device in pages (the reference's derive_kv_capacity,
+ * splitsim/config.hpp:66-79, with budget = cudaMemGetInfo free bytes -
+ * reserve_bytes; one page = 16 tokens x 2 (K,V) x n_layers x n_kv_heads x
+ * head_dim fp16 values, 2 MiB for Llama-3-8B).  Call after sw_model_create so
+ * the weights are already resident. */
+int sw_kv_capacity_pages(const sw_model_desc* desc, int device, int64_t reserve_bytes, int64_t* out);
 /* Device arrays of the arena (page table int32 [n_slots][max_pages_per_slot],
  * last_token int32 [n_slots], out_tokens int32 [n_slots][max_out_tokens],
  * pages bf16 [n_layers][n_pages][2][n_kv_heads][page_tokens][head_dim]). */
 int sw_kv_arena_views(sw_kv* kv, int32_t** page_table, int32_t** last_token, int32_t** out_tokens, void** pages);
 
 int sw_prefill_enqueue(sw_model* model, sw_kv* kv, const sw_batch* batch, void* stream);
+/* The co-scheduler's SM partition (green contexts, cached per device): a
+ * decode stream on `decode_sms` SMs (rounded to the driver's granularity) and
+ * a prefill stream on the rest; kernels enqueued on them stay on their SMs. */
+int sw_sm_partition(int device, int decode_sms, void** decode_stream, void** prefill_stream, int* decode_sms_out,
+                    int* prefill_sms_out);
 int sw_decode_enqueue(sw_model* model, sw_kv* kv, const sw_batch* batch, void* stream);
 
 /* ---- op level (kernel unit tests; device pointers, stream-ordered) ---- */

@@ -30,6 +30,7 @@
 #include <thread>
 #include <vector>
 
+#include "../../../include/splitwise_engine.hpp"
 #include "../host/capi_util.hpp"
 #include "../host/executor.hpp"
 #include "../host/report.hpp"
@@ -41,21 +42,6 @@
 #include "partition.hpp"
 
 namespace sw {
-
-struct GpuOptions {
-    bool split = true;        // two streams (prefill || decode) vs one
-    int decode_lanes = 1;     // split mode: concurrent decode streams (instance i -> lane i % lanes)
-    int decode_sms = 0;       // split mode: > 0 partitions the SMs with green contexts (decode | prefill)
-    bool lean_prefill = false;  // split mode: prompts launched while decode work exists use co-resident GEMM tiles
-    int prefill_yield = 0;      // split mode: prompts launched while decode work exists cap GEMM tiles per CTA
-    bool prefill_priority = false;  // split mode: prefill stream at the higher stream priority
-    bool coalesce = true;     // one launch per kind per pass
-    bool align = true;        // split mode: a token step requested while another is in flight waits for it and
-                              // then runs merged with every other waiting step (one weight pass for all lanes)
-    bool graphs = true;       // CUDA graphs for decode steps
-    double peak_flops = 1.6932e15;
-    double peak_bytes = 6.4469e12;
-};
 
 // Algorithmic work of the real forward passes.
 struct ModelWork {
@@ -225,8 +211,8 @@ public:
         return log_;
     }
 
-    std::string extras() const {
-        std::string s;
+    // Generated tokens, device page-table rows and launch statistics of the run.
+    void collect(RunOutputs& o) const {
         // generated tokens per request: x_1..x_out (device out_tokens[slot][0..out))
         std::vector<int32_t> host(static_cast<size_t>(kv_->n_slots) * kv_->max_out);
         SW_CUDA(cudaMemcpy(host.data(), kv_->out_tokens, host.size() * 4, cudaMemcpyDeviceToHost));
@@ -234,17 +220,13 @@ public:
         SW_CUDA(cudaMemcpy(table.data(), kv_->page_table, table.size() * 4, cudaMemcpyDeviceToHost));
         count_transfer(0, (host.size() + table.size()) * 4);
         for (const Entry& e : entries_) {
-            const int slot = slot_of_.at(e.req.id);
-            s += "#tokens " + std::to_string(e.req.id) + ":";
-            for (int j = 0; j < e.req.output_tokens; ++j)
-                s += (j ? "|" : "") + std::to_string(host[static_cast<size_t>(slot) * kv_->max_out + j]);
-            s += "\n";
+            const std::size_t slot = static_cast<std::size_t>(slot_of_.at(e.req.id));
+            const int32_t* t = host.data() + slot * static_cast<std::size_t>(kv_->max_out);
+            o.tokens[e.req.id].assign(t, t + e.req.output_tokens);
             const auto it = pages_.final_rows().find(e.req.id);
             const std::size_t np = it == pages_.final_rows().end() ? 0 : it->second.size();
-            s += "#devpages " + std::to_string(e.req.id) + ":";
-            for (std::size_t j = 0; j < np; ++j)
-                s += (j ? "|" : "") + std::to_string(table[static_cast<size_t>(slot) * kv_->max_pages + j]);
-            s += "\n";
+            const int32_t* r = table.data() + slot * static_cast<std::size_t>(kv_->max_pages);
+            o.page_rows[e.req.id].assign(r, r + np);
         }
         char buf[512];
         std::snprintf(buf, sizeof buf,
@@ -253,8 +235,8 @@ public:
                       launches_.size(), n_prefill_, n_decode_, opt_.split ? 1 : 0, opt_.coalesce ? 1 : 0,
                       aligning() ? 1 : 0, s_decode_.size(), part_ ? part_->decode_sms : 0, part_ ? part_->prefill_sms : 0, n_prefill_full_,
                       n_decode_full_, n_prefill_lean_, n_prefill_yield_, clock_skew_);
-        s += buf;
-        return s;
+        o.diagnostics = buf;
+        o.pages = pages_;
     }
 
 protected:
@@ -481,6 +463,44 @@ private:
     int n_prefill_ = 0, n_decode_ = 0;
 };
 
+EventLog run_split_engine(const SimulationInputs& inputs, Scheduler& scheduler, sw_model* model, sw_kv* kv,
+                          const GpuOptions& options, RunOutputs* outputs) {
+    if (!model || !kv) throw ConfigError("run_split_engine: null model or KV arena");
+    SW_CUDA(cudaSetDevice(model->device));
+    GpuExecutor ex(inputs, scheduler, model, kv, options);
+    EventLog log = ex.run();
+    if (outputs) ex.collect(*outputs);
+    return log;
+}
+
+int64_t derive_kv_capacity_pages(const sw_model_desc& d, int device, int64_t reserve_bytes) {
+    if (d.n_layers < 1 || d.n_kv_heads < 1 || d.head_dim < 1) throw ConfigError("kv capacity: bad model shape");
+    if (reserve_bytes < 0) throw ConfigError("kv capacity: reserve_bytes must be >= 0");
+    SW_CUDA(cudaSetDevice(device));
+    size_t free_b = 0, total_b = 0;
+    SW_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    // one page = page_tokens tokens of K and V for every layer and kv head, fp16 (kv_t)
+    constexpr int64_t kPageTokens = 16;  // sw_kv::page_tokens
+    const int64_t page_bytes = static_cast<int64_t>(d.n_layers) * 2 * d.n_kv_heads * kPageTokens * d.head_dim * 2;
+    const int64_t budget = static_cast<int64_t>(free_b) - reserve_bytes;
+    return budget > 0 ? budget / page_bytes : 0;
+}
+
+// The `#pages` / `#tokens` / `#devpages` / `#gpu` trailer of sw_engine_run's text.
+static std::string render_outputs(const EventLog&, const RunOutputs& o) {
+    std::string s;
+    for (const auto& [rid, toks] : o.tokens) {
+        s += "#tokens " + std::to_string(rid) + ":";
+        for (std::size_t j = 0; j < toks.size(); ++j) s += (j ? "|" : "") + std::to_string(toks[j]);
+        s += "\n";
+        s += "#devpages " + std::to_string(rid) + ":";
+        const auto& row = o.page_rows.at(rid);
+        for (std::size_t j = 0; j < row.size(); ++j) s += (j ? "|" : "") + std::to_string(row[j]);
+        s += "\n";
+    }
+    return s + o.diagnostics;
+}
+
 }  // namespace sw
 
 using namespace sw;
@@ -512,9 +532,9 @@ extern "C" int sw_engine_run(sw_model* m, sw_kv* kv, const char* spec, char** ou
             if (rs.inputs.discipline.mode == SharingDiscipline::Mode::Exclusive && model_instances(rs.scheduler) > 1)
                 rs.inputs.discipline.mode = SharingDiscipline::Mode::MpsConcurrent;
         PolicyScheduler sched(rs.inputs.requests, rs.scheduler, rs.inputs.cost.kv_handoff_s);
-        GpuExecutor ex(rs.inputs, sched, m, kv, opt);
+        RunOutputs outs;
         const auto w0 = std::chrono::steady_clock::now();
-        const EventLog log = ex.run();
+        const EventLog log = run_split_engine(rs.inputs, sched, m, kv, opt, &outs);
         const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - w0).count();
         std::string text = serialize_event_log(log);
         try {
@@ -525,8 +545,15 @@ extern "C" int sw_engine_run(sw_model* m, sw_kv* kv, const char* spec, char** ou
             g_last_error = std::string("ContractViolation: ") + e.what();
             text += std::string("#report_error ") + e.what() + "\n";
         }
-        text += render_pages(ex.pages()) + ex.extras();
+        text += render_pages(outs.pages) + render_outputs(log, outs);
         text += "#wall wall_s=" + fmt17(wall) + "\n";
         *out = dup_text(text);
+    });
+}
+
+extern "C" int sw_kv_capacity_pages(const sw_model_desc* desc, int device, int64_t reserve_bytes, int64_t* out) {
+    return guarded([&] {
+        if (!desc || !out) throw ConfigError("sw_kv_capacity_pages: null argument");
+        *out = derive_kv_capacity_pages(*desc, device, reserve_bytes);
     });
 }

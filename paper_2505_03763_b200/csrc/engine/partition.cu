@@ -147,3 +147,16 @@ int stream_sm_count(cudaStream_t st) {
 }
 
 }  // namespace sw
+
+// C-ABI (include/splitwise.h): the streams of a cached partition, for tools
+// and tests that enqueue prefill/decode on one SM group directly.
+extern "C" int sw_sm_partition(int device, int decode_sms, void** decode_stream, void** prefill_stream,
+                               int* decode_sms_out, int* prefill_sms_out) {
+    return sw::guarded([&] {
+        const sw::SmPartition& P = sw::sm_partition(device, decode_sms, 1);
+        if (decode_stream) *decode_stream = P.decode.front();
+        if (prefill_stream) *prefill_stream = P.prefill;
+        if (decode_sms_out) *decode_sms_out = P.decode_sms;
+        if (prefill_sms_out) *prefill_sms_out = P.prefill_sms;
+    });
+}
