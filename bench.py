@@ -1,19 +1,24 @@
 """Benchmark: split-phase vs serial tokens/s on one B200 (and request-sharded
-replicas on N GPUs), with p50 TTFT/TBT, a kernel roofline line and the CPU
-oracle timed beside it.
+replicas on N GPUs), with p50 TTFT/TBT, a whole-run roofline, kernel roofline
+lines and the CPU oracle timed beside it.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload W]
 
-A "step" is one complete engine run of the BASELINE workload (configs[1]:
-Llama-3.2-1B shape, bf16, random weights, 64 requests x prompt 512 / gen 128)
-through the C-ABI (sw_engine_run).  Split = PipelinedSplitwiser P=2 with the
-phases on concurrent streams; serial = the same task stream under the
-one-task gate; the fastest serial policy is reported beside.  value = generated tokens / device makespan
-(CUDA events inside the engine) summed over the K timed runs; e2e = the same
-tokens over the wall time of the sw_engine_run calls (prompt H2D staging and
-token/page-table D2H inside).  Under torchrun every rank runs its own engine
-on its round-robin shard of an N x 64-request trace (weak scaling); results
-are gathered with NCCL (torch.distributed) and timed as the max over ranks.
+A "step" is one complete engine run of the workload through the C-ABI
+(sw_engine_run).  The default workload is BASELINE.json configs[2] as SURVEY.md
+§8d states it -- the Llama-3-8B shape the north-star target is quoted on:
+bf16 random weights, 512 requests, prompts U[128,2048], 256 generated tokens,
+Poisson arrivals at a rate where arrivals no longer limit throughput (the rate
+sweep is in profiles/r02/).  Split = MixedBatching (one prompt task and one token
+step in flight together) with the phases on concurrent streams / SM partitions;
+serial = ContinuousBatching (the fastest serial schedule of this trace) with
+every task on one stream.  value = generated tokens / device makespan (CUDA
+events inside the engine) over the K timed runs; e2e = the same tokens over the
+wall time of the sw_engine_run calls (prompt H2D staging and token/page-table
+D2H inside).  Under torchrun every rank runs its own engine on its round-robin
+shard of an N x 512-request trace (weak scaling); the per-request results are
+gathered with one NCCL all_gather (paper_2505_03763_b200/sharded.py) and folded
+into global percentiles; device times are the max over ranks.
 """
 from __future__ import annotations
 
@@ -33,7 +38,14 @@ METRIC = "tokens/s/GPU split vs serial prefill+decode; p50 TTFT and TBT; 1/2/4/8
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
 
 WORKLOADS = {
-    # configs[1] of BASELINE.json -- the bench line
+    # configs[2] of BASELINE.json, as SURVEY.md §8d states it -- the default line: 8B shape, 512 requests,
+    # prompts U[128,2048], 256 generated, Poisson arrivals; MixedBatching split vs ContinuousBatching serial
+    "8b-cfg3": dict(model="LLAMA_8B", n=512, input="128..2048", output=256, arrival="poisson:128",
+                    max_prefill=32768, max_decode=256,
+                    split="policy=mixed_batching;max_batch=256;engine.split=1;engine.prefill_priority=1",
+                    serial="policy=continuous_batching;max_batch=256;engine.split=0",
+                    best_serial=None),
+    # configs[1] of BASELINE.json
     # split = PipelinedSplitwiser P=2 on concurrent streams (token steps of the two lanes aligned and merged);
     # serial = the SAME task stream under the one-task gate; best_serial = the fastest
     # serial policy on this closed batch (request-level batching of all 64), reported beside it
@@ -230,6 +242,10 @@ def roofline_prefill_gemm(eng, desc, tokens: int, peaks, reps: int = 10):
 
 
 # ----------------------------------------------------------------- engine runs
+# bounded CPU samples of each model (requests, prompt, generated tokens): ~10-30 s of numpy on the host cores
+CPU_SAMPLE = {"LLAMA_8B": (1, 512, 4), "LLAMA_1B": (4, 512, 8), "TINY": (8, 64, 32)}
+
+
 def spec_for(w, extra: str, rank: int, world: int) -> str:
     s = (f"n={w['n'] * world};input={w['input']};output={w['output']};seed=1;arrival={w['arrival']};"
          f"kv_capacity_blocks={w['kv_pages']};{extra}")
@@ -239,9 +255,9 @@ def spec_for(w, extra: str, rank: int, world: int) -> str:
 
 
 def gather_run_stats(dist, world: int, res: dict, device) -> dict:
-    """Result gathering across request-sharded replicas -- the only collective
-    (NCCL over NVLink on the GPU box, gloo in the CPU tests): makespan and wall
-    are the max over ranks, tokens the sum."""
+    """Scalar gather across request-sharded replicas (NCCL over NVLink on the
+    GPU box, gloo in the CPU tests): makespan and wall are the max over ranks,
+    tokens the sum."""
     import torch
 
     t = torch.tensor([res["makespan"], res["wall"], float(res["tokens"])], device=device, dtype=torch.float64)
@@ -254,29 +270,79 @@ def gather_run_stats(dist, world: int, res: dict, device) -> dict:
     return out
 
 
+def run_work(event_log: str):
+    """Algorithmic work of one run from its event log: the GPU executor prices
+    every prompt task with its prefill FLOPs and every token step with its
+    decode bytes (engine/gpu_executor.cu ModelWork)."""
+    flops = nbytes = 0.0
+    for line in event_log.splitlines():
+        if ",task_start," not in line:
+            continue
+        kv = dict(x.split("=", 1) for x in line.split(",", 2)[2].split(";") if "=" in x)
+        if kv.get("kind") == "prompt":
+            flops += float(kv["compute"])
+        else:
+            nbytes += float(kv["mem"])
+    return flops, nbytes
+
+
 def run_many(eng, spec: str, k: int):
     import paper_2505_03763_b200 as sw
+    from paper_2505_03763_b200 import sharded
 
-    tokens = 0
-    makespan = 0.0
-    wall = 0.0
-    ttft, tbt = [], []
+    runs = []
     l0 = sw.launch_count()
     h0, d0 = sw.transfer_bytes()
-    last = None
     for _ in range(k):
         t0 = time.perf_counter()
         r = eng.run(spec)
-        wall += time.perf_counter() - t0
-        tokens += int(r.report["total_output_tokens"])
-        makespan += r.report["makespan_s"]
-        ttft.append(r.report["p50_ttft_s"])
-        tbt.append(r.report["p50_tbt_s"])
-        last = r
+        wall = time.perf_counter() - t0
+        runs.append({"tokens": int(r.report["total_output_tokens"]), "makespan": r.report["makespan_s"], "wall": wall,
+                     "rows": sharded.request_rows(r), "work": run_work(r.event_log), "report": r.report})
     h1, d1 = sw.transfer_bytes()
-    return dict(tokens=tokens, makespan=makespan, wall=wall, p50_ttft=statistics.median(ttft),
-                p50_tbt=statistics.median(tbt), launches=sw.launch_count() - l0, h2d=(h1 - h0) / max(k, 1),
-                d2h=(d1 - d0) / max(k, 1), last=last)
+    return dict(runs=runs, launches=sw.launch_count() - l0, h2d=(h1 - h0) / max(k, 1), d2h=(d1 - d0) / max(k, 1))
+
+
+def fold_runs(res: dict, dist, world: int, device, n_local: int, max_out: int) -> dict:
+    """Per run: gather every rank's request rows (one all_gather, after the
+    timed region) and fold them into global metrics; then sum tokens and device
+    makespans over the K runs and take the median of the per-run percentiles."""
+    from paper_2505_03763_b200 import sharded
+
+    folds, tokens, makespan, wall = [], 0, 0.0, 0.0
+    for run in res["runs"]:
+        if dist:
+            rows, mk, wl = sharded.gather_requests(dist, world, run["rows"], run["makespan"], run["wall"], device,
+                                                   n_local + 8, max_out)
+        else:
+            rows, mk, wl = run["rows"], run["makespan"], run["wall"]
+        f = sharded.fold(rows, mk)
+        folds.append(f)
+        tokens += f["total_output_tokens"]
+        makespan += mk
+        wall += wl
+    med = lambda key: statistics.median(f[key] for f in folds)  # noqa: E731
+    return dict(tokens=tokens, makespan=makespan, wall=wall, p50_ttft=med("p50_ttft_s"), p50_tbt=med("p50_tbt_s"),
+                p99_tbt=med("p99_tbt_s"), n_requests=folds[-1]["n_requests"], launches=res["launches"],
+                h2d=res["h2d"], d2h=res["d2h"], work=res["runs"][-1]["work"], last_tokens=res["runs"][-1]["tokens"],
+                last_makespan=res["runs"][-1]["makespan"])
+
+
+def whole_run_roofline(res: dict, peaks) -> dict:
+    """F = sum of prefill FLOPs, B = sum of decode bytes of the
+    run; serial bound t_s = F/P_tc + B/BW, split bound t_p = max(F/P_tc, B/BW);
+    achieved = the run's makespan against them (P_tc the sustained bf16 peak:
+    a run is a long step)."""
+    F, B = res["work"]
+    p_tc = float(peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])) * 1e12
+    bw = float(peaks["hbm_gbs"]) * 1e9
+    t_s, t_p = F / p_tc + B / bw, max(F / p_tc, B / bw)
+    toks, mk = res["last_tokens"], res["last_makespan"]
+    return {"prefill_tflop": round(F / 1e12, 2), "decode_gb": round(B / 1e9, 2), "tokens": toks,
+            "serial_bound_tok_s": round(toks / t_s, 1), "split_bound_tok_s": round(toks / t_p, 1),
+            "achieved_tok_s": round(toks / mk, 1), "frac_of_serial_bound": round(t_s / mk, 4),
+            "frac_of_split_bound": round(t_p / mk, 4), "max_split_speedup": round(t_s / t_p, 4),
+            "peaks": {"tensor_tflops": p_tc / 1e12, "hbm_gbs": bw / 1e9}}
 
 
 def main():
@@ -285,7 +351,7 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="1b")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="8b-cfg3")
     ap.add_argument("--split", default=None, help="override the split-phase policy spec")
     ap.add_argument("--serial", default=None, help="override the serial policy spec")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -301,15 +367,17 @@ def main():
     if args.impl == "reference":
         # The reference's own CPU implementation of the path: it has no model math
         # (splitsim prices phases with a roofline law), so this arm times the fp32
-        # CPU oracle port on the host cores, rank 0 only.
+        # CPU oracle port on the host cores, rank 0 only, on a bounded sample of
+        # this workload's model.
         if rank != 0:
             return
-        samples = [cpu_sample(w["model"] if w["model"] != "LLAMA_8B" else "LLAMA_1B") for _ in range(max(args.steps, 1))]
+        n_req, prompt, gen = CPU_SAMPLE[w["model"]]
+        samples = [cpu_sample(w["model"], n_req, prompt, gen) for _ in range(max(args.steps, 1))]
         v = statistics.median(s["value"] for s in samples)
         line = {"impl": "reference", "metric": METRIC, "value": round(v, 3), "unit": "tokens/s", "n_gpus": args.gpus,
                 "steps": args.steps, "warmup": 0, "ms_per_step": round(1e3 * statistics.median(s["seconds"] for s in samples), 1),
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-                "config": {"workload": args.workload, "sample": samples[0]["sample"]},
+                "config": {"workload": args.workload, "model_shape": w["model"], "sample": samples[0]["sample"]},
                 "cpu_baseline": {k: samples[0][k] for k in ("unit", "cores", "kind", "sample")} | {"value": round(v, 3)},
                 "e2e": {"value": round(v, 3), "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line), flush=True)
@@ -329,21 +397,24 @@ def main():
     n_local = w["n"]
     in_max = int(str(w["input"]).split("..")[-1])
     pages_per = (in_max + w["output"] + 15) // 16
-    w["kv_pages"] = n_local * pages_per + 64
     t_init = time.perf_counter()
+    # KV arena: the trace's worst case, capped by what fits in free HBM (sw_kv_capacity_pages)
     eng = runtime.Engine(desc, max_prefill_tokens=w["max_prefill"], max_decode_batch=w["max_decode"],
-                         n_pages=w["kv_pages"], n_slots=n_local + 8, max_pages_per_slot=pages_per + 1,
-                         max_out=w["output"] + 1, device=local)
+                         n_pages=None, n_slots=n_local + 8, max_pages_per_slot=pages_per + 1,
+                         max_out=w["output"] + 1, device=local, kv_reserve_bytes=4 << 30,
+                         max_pages=n_local * pages_per + 64)
+    w["kv_pages"] = eng.n_pages
     t_init = time.perf_counter() - t_init
     split_spec = spec_for(w, args.split or w["split"], rank, world)
     serial_spec = spec_for(w, args.serial or w["serial"], rank, world)
-    best_spec = spec_for(w, w["best_serial"], rank, world)
+    best_spec = spec_for(w, w["best_serial"], rank, world) if w["best_serial"] else None
 
     for _ in range(args.warmup):
         eng.run(split_spec)
     for _ in range(max(1, args.warmup // 3)):
         eng.run(serial_spec)
-        eng.run(best_spec)
+        if best_spec:
+            eng.run(best_spec)
 
     def timed(spec):
         if dist:
@@ -351,14 +422,16 @@ def main():
         torch.cuda.synchronize()
         res = run_many(eng, spec, args.steps)
         torch.cuda.synchronize()
-        if dist:
-            res = gather_run_stats(dist, world, res, "cuda")
         return res
 
     with ClockSampler(local) as clocks:
-        split = timed(split_spec)
-    serial = timed(serial_spec)
-    best = timed(best_spec)
+        split_raw = timed(split_spec)
+    serial_raw = timed(serial_spec)
+    best_raw = timed(best_spec) if best_spec else None
+    dev = "cuda" if dist else None
+    split = fold_runs(split_raw, dist, world, dev, n_local, w["output"] + 1)
+    serial = fold_runs(serial_raw, dist, world, dev, n_local, w["output"] + 1)
+    best = fold_runs(best_raw, dist, world, dev, n_local, w["output"] + 1) if best_raw else serial
 
     roof = roofline_decode_gemm(eng, desc, w["max_decode"], peaks) if rank == 0 else None
     roof_prefill = roofline_prefill_gemm(eng, desc, 4096, peaks) if rank == 0 else None
@@ -377,15 +450,16 @@ def main():
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         try:
-            cpu = cpu_sample("LLAMA_1B" if w["model"] != "TINY" else "TINY")
+            n_req, prompt, gen = CPU_SAMPLE[w["model"]]
+            cpu = cpu_sample(w["model"], n_req, prompt, gen)
         except Exception as e:  # never fail the GPU line on the CPU sample
             cpu = {"value": None, "unit": "tokens/s", "cores": os.cpu_count(), "kind": "port", "sample": f"failed: {e}"}
 
     value = split["tokens"] / split["makespan"]
     serial_v = serial["tokens"] / serial["makespan"]
     best_v = best["tokens"] / best["makespan"]
-    # decode-step roofline from the best-serial run's p50 TBT (a step alone on the GPU): algorithmic bytes of a
-    # step at the batch and mean context of that run (weights + KV read + KV write + activations)
+    # decode-step roofline (closed batches): algorithmic bytes of a step at the batch and mean context of the
+    # best-serial run over its p50 TBT (a step alone on the GPU)
     step = None
     if w["arrival"] == "zero" and str(w["input"]).isdigit():
         b = min(w["n"], w["max_decode"])
@@ -414,15 +488,19 @@ def main():
         "config": {"workload": args.workload, "model_shape": w["model"], "requests_per_gpu": n_local,
                    "prompt": w["input"], "gen": w["output"], "arrival": w["arrival"],
                    "split_policy": args.split or w["split"], "serial_policy": args.serial or w["serial"],
-                   "best_serial_policy": w["best_serial"],
-                   "l2": "working set > L2: every decode step streams all weights (2.5-16 GB)",
+                   "best_serial_policy": w["best_serial"] or (args.serial or w["serial"]),
+                   "kv_pages": w["kv_pages"],
+                   "l2": "working set > L2: every decode step streams all weights (2.5-16 GB) plus the KV cache",
                    "parallelism": f"request-sharded replicas x{world}"},
-        "split": {"tokens_per_s": round(value, 1), "p50_ttft_s": split["p50_ttft"], "p50_tbt_s": split["p50_tbt"]},
+        "per_gpu_tokens_per_s": round(value / world, 1),
+        "split": {"tokens_per_s": round(value, 1), "p50_ttft_s": split["p50_ttft"], "p50_tbt_s": split["p50_tbt"],
+                  "p99_tbt_s": split["p99_tbt"], "requests": split["n_requests"]},
         "serial": {"tokens_per_s": round(serial_v, 1), "p50_ttft_s": serial["p50_ttft"],
-                   "p50_tbt_s": serial["p50_tbt"]},
+                   "p50_tbt_s": serial["p50_tbt"], "p99_tbt_s": serial["p99_tbt"]},
         "split_over_serial": round(value / serial_v, 4),
         "best_serial": {"tokens_per_s": round(best_v, 1), "p50_ttft_s": best["p50_ttft"], "p50_tbt_s": best["p50_tbt"]},
         "split_over_best_serial": round(value / best_v, 4),
+        "roofline_run": {"split": whole_run_roofline(split, peaks), "serial": whole_run_roofline(serial, peaks)},
         "roofline_decode_step": step,
         "e2e": {"value": round(split["tokens"] / split["wall"], 1), "unit": "tokens/s",
                 "h2d_bytes_per_step": int(split["h2d"]), "d2h_bytes_per_step": int(split["d2h"])},

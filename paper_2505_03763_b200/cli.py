@@ -154,23 +154,43 @@ class _Runner:
         self.backend = backend
         self.model_name = model
         self.eng = None
+        self.sizes = (0, 0, 0, 0)  # (slots, pages per slot, output tokens, decode rows) of the live engine
 
     def run(self, spec: str, cfg: dict):
         if self.backend == "sim":
             return sim_run(spec)
         from . import runtime, shapes
 
+        # size the engine from this run's actual request list (generated workload or trace file): the
+        # virtual-clock backend assembles the same requests in milliseconds; rebuild when a later sweep
+        # value needs more slots, longer page-table rows, more output tokens or a wider decode batch
+        n, ctx, out = self._extent(spec)
+        pages = (ctx + 15) // 16 + 1
+        need = (n + 8, pages, out + 1, min(256, max(1, n)))
+        if self.eng is not None and any(a > b for a, b in zip(need, self.sizes)):
+            self.eng.close()
+            self.eng = None
         if self.eng is None:
             desc = getattr(shapes, self.model_name)
-            w = cfg.get("workload", {})
-            n = int(w.get("n_requests", 1))
-            hi = lambda r: r[1] if isinstance(r, list) else r  # noqa: E731
-            ctx = hi(w.get("input_tokens", 1)) + hi(w.get("output_tokens", 1))
-            pages = (ctx + 15) // 16 + 1
-            self.eng = runtime.Engine(desc, max_prefill_tokens=32768, max_decode_batch=min(256, max(1, n)),
-                                      n_pages=n * pages + 64, n_slots=n + 8, max_pages_per_slot=pages,
-                                      max_out=hi(w.get("output_tokens", 1)) + 1)
+            self.sizes = need
+            self.eng = runtime.Engine(desc, max_prefill_tokens=32768, max_decode_batch=need[3], n_pages=None,
+                                      max_pages=need[0] * pages + 64, n_slots=need[0], max_pages_per_slot=pages,
+                                      max_out=need[2])
         return self.eng.run(spec)
+
+    @staticmethod
+    def _extent(spec: str):
+        """(requests, longest prompt + output, longest output) of the run's request list."""
+        sim_spec = ";".join(kv for kv in spec.split(";") if not kv.startswith("engine.")
+                            and not kv.startswith("output_dir=") and not kv.startswith("emit_event_log="))
+        r = sim_run(sim_spec)
+        n, ctx, out = 0, 1, 1
+        for line in r.event_log.splitlines():
+            if ",arrival," in line:
+                kv = dict(x.split("=", 1) for x in line.split(",", 2)[2].split(";"))
+                i, o = int(kv["input"]), int(kv["output"])
+                n, ctx, out = n + 1, max(ctx, i + o), max(out, o)
+        return max(n, 1), ctx, out
 
     def close(self):
         if self.eng is not None:

@@ -29,10 +29,11 @@ class Engine:
     """One model (weights generated on the device) + one paged KV arena."""
 
     def __init__(self, desc, max_prefill_tokens=4096, max_decode_batch=64, n_pages=4096, n_slots=64,
-                 max_pages_per_slot=64, max_out=64, device=0, kv_reserve_bytes=2 << 30):
+                 max_pages_per_slot=64, max_out=64, device=0, kv_reserve_bytes=2 << 30, max_pages=None):
         """n_pages=None sizes the KV arena from the device's free HBM after the
         weights are resident (sw_kv_capacity_pages: the reference's
-        derive_kv_capacity with budget = free - kv_reserve_bytes)."""
+        derive_kv_capacity with budget = free - kv_reserve_bytes), capped at
+        max_pages when given."""
         self.desc = desc
         L = lib()
         self.model = ctypes.c_void_p()
@@ -41,7 +42,7 @@ class Engine:
         if n_pages is None:
             cap = ctypes.c_int64()
             check(L.sw_kv_capacity_pages(ctypes.byref(md), device, int(kv_reserve_bytes), ctypes.byref(cap)))
-            n_pages = int(cap.value)
+            n_pages = int(cap.value) if max_pages is None else min(int(cap.value), int(max_pages))
         self.kv = ctypes.c_void_p()
         check(L.sw_kv_arena_create(self.model, n_pages, n_slots, max_pages_per_slot, max_out, ctypes.byref(self.kv)))
         self.n_pages, self.n_slots, self.max_pages, self.max_out = n_pages, n_slots, max_pages_per_slot, max_out

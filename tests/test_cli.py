@@ -144,3 +144,38 @@ def test_validate(tmp_path, capsys):
     p.write_text(json.dumps(dict(INLINE, scheduler={"policy": "multi_instance", "n_instances": 2},
                                  discipline={"mode": "exclusive"})))
     assert cli.main(["validate", "-c", str(p)]) == 2
+
+
+def test_gpu_runner_sizes_from_the_request_list(tmp_path):
+    """The B200 backend sizes its engine from each run's own request list (the
+    reference's sweep over workload.n_requests, configs/sweep_batch.json, and
+    trace workloads): _extent reads it off the virtual-clock assembly."""
+    spec = cli.config_to_spec(dict(INLINE, output_dir=""))
+    n, ctx, out = cli._Runner._extent(spec + ";engine.split=1")
+    assert n == 24 and 64 + 2 <= ctx <= 400 + 20 and 2 <= out <= 20
+    trace = tmp_path / "trace.csv"
+    trace.write_text("id,arrival_s,input_tokens,output_tokens\n0,0.0,100,5\n1,0.001,300,9\n2,0.001,50,2\n")
+    n, ctx, out = cli._Runner._extent(cli.config_to_spec({"workload": {"trace": str(trace)},
+                                                           "scheduler": {"policy": "mixed_batching"}}))
+    assert (n, ctx, out) == (3, 309, 9)
+
+
+@pytest.mark.gpu
+def test_gpu_backend_sweep_grows_the_engine(tmp_path):
+    """a B200-backend sweep over n_requests (10 -> 160) and a trace
+    workload both run (the engine is rebuilt when a value needs more capacity)."""
+    base = {"workload": {"n_requests": 10, "input_tokens": [16, 64], "output_tokens": [2, 6], "seed": 3,
+                         "arrival": "all_at_zero"},
+            "scheduler": {"policy": "continuous_batching", "max_batch": 0},
+            "engine": {"engine.split": 1}, "output_dir": str(tmp_path / "sw")}
+    p = tmp_path / "sweep.json"
+    p.write_text(json.dumps({"base": base, "axis": "workload.n_requests", "values": [10, 40, 160]}))
+    assert cli.main(["sweep", "-c", str(p), "--backend", "gpu", "--model", "TINY"]) == 0
+    rows = _read(tmp_path / "sw", "sweep.csv").splitlines()
+    assert [r.split(",")[:2] for r in rows[1:]] == [["10", "ok"], ["40", "ok"], ["160", "ok"]]
+    trace = tmp_path / "trace.csv"
+    trace.write_text("id,arrival_s,input_tokens,output_tokens\n0,0.0,100,5\n1,0.001,300,9\n2,0.001,50,2\n")
+    cfg = {"workload": {"trace": str(trace)}, "scheduler": {"policy": "mixed_batching"}}
+    code, out = _run(tmp_path, cfg, "--backend", "gpu", "--model", "TINY")
+    assert code == 0
+    assert json.loads(_read(out, "report.json"))["total_output_tokens"] == 16

@@ -38,6 +38,7 @@ def main():
     ap.add_argument("--prompts", type=int, default=8)
     ap.add_argument("--prompt-len", type=int, default=1024)
     ap.add_argument("--decode-sms", default="32,48,64,80")
+    ap.add_argument("--stream-gb", type=float, default=0.0, help="replace decode steps by a read stream of this size")
     args = ap.parse_args()
     d = getattr(shapes, args.model)
     B, S, P, Sp = args.batch, args.ctx, args.prompts, args.prompt_len
@@ -64,7 +65,17 @@ def main():
              i32([base + i * pages_pre + j for i in range(P) for j in range(pages_pre)]), i32([0] * P)]
     pb = sw.Batch(n=P, slots=pkeep[0], n_tokens=pkeep[1], tokens=pkeep[2], page_rows=pkeep[3], out_index=pkeep[4])
 
+    # --stream: the decode phase replaced by a pure HBM read stream of the same bytes as one step
+    # (torch reduction over a buffer > L2), to separate interference in the memory system from the
+    # decode kernels' own partition behaviour
+    sbuf = torch.empty(int(args.stream_gb * (1 << 30)) // 4, dtype=torch.float32, device="cuda") if args.stream_gb else None
+    sink = torch.empty(1, dtype=torch.float32, device="cuda")
+
     def dec(st):
+        if sbuf is not None:
+            with torch.cuda.stream(torch.cuda.ExternalStream(st)):
+                torch.sum(sbuf, dim=0, out=sink[0])
+            return
         sw.check(L.sw_decode_enqueue(eng.model, eng.kv, ctypes.byref(db), ctypes.c_void_p(st)))
 
     def pre(st):
