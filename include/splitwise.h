@@ -130,6 +130,15 @@ int sw_prefill_enqueue(sw_model* model, sw_kv* kv, const sw_batch* batch, void* 
 int sw_sm_partition(int device, int decode_sms, void** decode_stream, void** prefill_stream, int* decode_sms_out,
                     int* prefill_sms_out);
 int sw_decode_enqueue(sw_model* model, sw_kv* kv, const sw_batch* batch, void* stream);
+/* One fused mixed step -- the split-phase co-execution of a prompt chunk and a
+ * token step (MixedBatching's "one prompt and one step in flight together"):
+ * the decode rows of `decode` (sw_decode_enqueue semantics) ride in the
+ * prefill pass of `prefill` (sw_prefill_enqueue semantics), so each projection
+ * GEMM streams its weights once for both phases.  All prompts and decode rows
+ * must fit one launch (prompt tokens + rows <= max_prefill_tokens, prompts +
+ * rows <= 256).  prefill->logits_out (optional) receives the prompts' last-
+ * position logits followed by the decode rows'. */
+int sw_mixed_enqueue(sw_model* model, sw_kv* kv, const sw_batch* prefill, const sw_batch* decode, void* stream);
 
 /* ---- op level (kernel unit tests; device pointers, stream-ordered) ---- */
 /* C[M,N] (+)= A[M,K] . B[N,K]^T, bf16 in, fp32 accumulate.

@@ -48,6 +48,10 @@ struct GpuOptions {
     bool align = true;        // split mode: a token step requested while another is in flight waits for it and
                               // then runs merged with every other waiting step (one weight pass for all lanes)
     bool graphs = true;       // CUDA graphs for decode steps
+    bool fuse = false;        // split mode: fused mixed steps -- a prompt task runs as chunks of whole prompts and
+                              // every token step requested meanwhile rides in the next chunk's launch (one weight
+                              // stream for both phases)
+    int chunk_tokens = 0;     // fuse mode: prompt tokens per chunk (0: as many as the prefill workspace holds)
     double peak_flops = 1.6932e15;  // roofline denominators for the logged alone_s
     double peak_bytes = 6.4469e12;
 };

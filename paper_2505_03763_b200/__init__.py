@@ -109,6 +109,7 @@ def lib() -> ctypes.CDLL:
                                 ctypes.POINTER(c_int), ctypes.POINTER(c_int)],
             "sw_prefill_enqueue": [c_void_p, c_void_p, ctypes.POINTER(Batch), c_void_p],
             "sw_decode_enqueue": [c_void_p, c_void_p, ctypes.POINTER(Batch), c_void_p],
+            "sw_mixed_enqueue": [c_void_p, c_void_p, ctypes.POINTER(Batch), ctypes.POINTER(Batch), c_void_p],
             "sw_op_gemm": [c_void_p, c_void_p, c_void_p, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
                            ctypes.c_int32, c_void_p],
             "sw_op_rmsnorm": [c_void_p, c_void_p, c_void_p, ctypes.c_int32, ctypes.c_int32, ctypes.c_float,
@@ -126,7 +127,7 @@ def lib() -> ctypes.CDLL:
 EXPORTED_SYMBOLS = [
     "sw_last_error", "sw_free", "sw_launch_count", "sw_transfer_bytes", "sw_sim_run", "sw_engine_run", "sw_replay", "sw_model_create", "sw_model_destroy",
     "sw_model_weight_checksum", "sw_model_tensor", "sw_kv_arena_create", "sw_kv_arena_destroy", "sw_kv_capacity_pages",
-    "sw_kv_arena_views", "sw_sm_partition", "sw_prefill_enqueue", "sw_decode_enqueue", "sw_op_gemm", "sw_op_rmsnorm",
+    "sw_kv_arena_views", "sw_sm_partition", "sw_prefill_enqueue", "sw_decode_enqueue", "sw_mixed_enqueue", "sw_op_gemm", "sw_op_rmsnorm",
 ]
 
 

@@ -25,6 +25,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstring>
+#include <deque>
 #include <map>
 #include <string>
 #include <thread>
@@ -189,7 +190,7 @@ public:
                 schedule_pass();
             }
             flush_steps();
-            const bool inflight = !pending_steps_.empty() ||
+            const bool inflight = !pending_steps_.empty() || !jobs_.empty() ||
                                   std::any_of(launches_.begin(), launches_.end(), [](const Launch& l) { return !l.done; });
             if (!inflight && active_.empty() && next_arrival >= entries_.size()) break;
             if (!inflight && active_.empty() && evs.empty()) {
@@ -231,10 +232,12 @@ public:
         char buf[512];
         std::snprintf(buf, sizeof buf,
                       "#gpu launches=%zu;prefill_launches=%d;decode_launches=%d;split=%d;coalesce=%d;align=%d;decode_lanes=%zu;"
-                      "decode_sms=%d;prefill_sms=%d;prefill_full_gpu=%d;decode_full_gpu=%d;prefill_lean=%d;prefill_yield=%d;clock_skew_s=%.9g\n",
+                      "decode_sms=%d;prefill_sms=%d;prefill_full_gpu=%d;decode_full_gpu=%d;prefill_lean=%d;prefill_yield=%d;"
+                      "fuse=%d;mixed_launches=%d;chunk_tokens=%d;clock_skew_s=%.9g\n",
                       launches_.size(), n_prefill_, n_decode_, opt_.split ? 1 : 0, opt_.coalesce ? 1 : 0,
                       aligning() ? 1 : 0, s_decode_.size(), part_ ? part_->decode_sms : 0, part_ ? part_->prefill_sms : 0, n_prefill_full_,
-                      n_decode_full_, n_prefill_lean_, n_prefill_yield_, clock_skew_);
+                      n_decode_full_, n_prefill_lean_, n_prefill_yield_, fusing() ? 1 : 0, n_mixed_, opt_.chunk_tokens,
+                      clock_skew_);
         o.diagnostics = buf;
         o.pages = pages_;
     }
@@ -328,13 +331,18 @@ private:
                 pending_steps_.push_back(L);
                 continue;
             }
+            if (fusing() && L.kind == TaskKind::Prompt) {
+                fuse_add_prompt(L);
+                continue;
+            }
             enqueue(L);
             launches_.push_back(L);
         }
         flush_steps();
     }
 
-    bool aligning() const { return opt_.split && opt_.align; }
+    bool aligning() const { return opt_.split && (opt_.align || opt_.fuse); }
+    bool fusing() const { return opt_.split && opt_.fuse; }
 
     // decode work exists: a step in flight or waiting, or a request past its prompt
     bool decode_active() const {
@@ -357,6 +365,10 @@ private:
     // one merged launch on decode lane 0 (their TaskStart/TaskComplete events
     // are all recorded around it).
     void flush_steps() {
+        if (fusing()) {
+            fuse_dispatch();
+            return;
+        }
         if (pending_steps_.empty() || decode_inflight()) return;
         Launch M = pending_steps_.front();
         M.lane = 0;
@@ -370,36 +382,74 @@ private:
         launches_.push_back(M);
     }
 
-    void enqueue(const Launch& L) {
+    // Host staging of one launch's batch (kept alive until the enqueue returns:
+    // the forward passes stage host arrays into pinned memory themselves).
+    struct BatchBuf {
+        std::vector<int32_t> slots, ntok, pos, newp, oidx, toks, prow;
+        sw_batch b{};
+    };
+
+    std::vector<int> rids_of(const std::vector<long long>& seqs) const {
         std::vector<int> rids;
-        for (long long sq : L.task_seqs) {
+        for (long long sq : seqs) {
             const Active* a = nullptr;
             for (const Active& x : active_)
                 if (x.seq == sq) a = &x;
             if (!a) throw ContractViolation("gpu executor: enqueue of unknown task");
             rids.insert(rids.end(), a->task.batch.begin(), a->task.batch.end());
         }
+        return rids;
+    }
+
+    void build_prompt(const std::vector<int>& rids, BatchBuf& B) const {
         const int n = static_cast<int>(rids.size());
-        std::vector<int32_t> slots(n), ntok(n), pos(n), newp(n), oidx(n), toks, prow;
-        sw_batch b{};
-        b.n = n;
+        B.slots.resize(n);
+        B.ntok.resize(n);
+        B.oidx.assign(n, 0);
+        for (int i = 0; i < n; ++i) {
+            const Entry& e = entry(rids[i]);
+            B.slots[i] = slot_of_.at(rids[i]);
+            B.ntok[i] = e.req.input_tokens;
+            for (int j = 0; j < e.req.input_tokens; ++j)
+                B.toks.push_back(prompt_token(m_->desc.seed, e.req.id, j, m_->desc.vocab));
+            const std::vector<int>& row = pages_.row(rids[i]);
+            const int need = (e.req.input_tokens + kv_->page_tokens - 1) / kv_->page_tokens;
+            for (int j = 0; j < need; ++j) B.prow.push_back(row.at(static_cast<std::size_t>(j)));
+        }
+        B.b.n = n;
+        B.b.slots = B.slots.data();
+        B.b.n_tokens = B.ntok.data();
+        B.b.tokens = B.toks.data();
+        B.b.page_rows = B.prow.data();
+        B.b.out_index = B.oidx.data();
+    }
+
+    void build_step(const std::vector<int>& rids, BatchBuf& B) const {
+        const int n = static_cast<int>(rids.size());
+        B.slots.resize(n);
+        B.pos.resize(n);
+        B.newp.resize(n);
+        B.oidx.resize(n);
+        for (int i = 0; i < n; ++i) {
+            const Entry& e = entry(rids[i]);
+            B.slots[i] = slot_of_.at(rids[i]);
+            B.pos[i] = e.req.input_tokens + e.generated;  // position of the fed token x_g
+            const int pidx = B.pos[i] / kv_->page_tokens;
+            B.newp[i] = B.pos[i] % kv_->page_tokens == 0 ? pages_.row(rids[i]).at(static_cast<std::size_t>(pidx)) : -1;
+            B.oidx[i] = e.generated + 1;  // x_{g+1}
+        }
+        B.b.n = n;
+        B.b.slots = B.slots.data();
+        B.b.positions = B.pos.data();
+        B.b.new_page = B.newp.data();
+        B.b.out_index = B.oidx.data();
+    }
+
+    void enqueue(const Launch& L) {
+        const std::vector<int> rids = rids_of(L.task_seqs);
+        BatchBuf B;
         if (L.kind == TaskKind::Prompt) {
-            for (int i = 0; i < n; ++i) {
-                const Entry& e = entry(rids[i]);
-                slots[i] = slot_of_.at(rids[i]);
-                ntok[i] = e.req.input_tokens;
-                oidx[i] = 0;
-                for (int j = 0; j < e.req.input_tokens; ++j)
-                    toks.push_back(prompt_token(m_->desc.seed, e.req.id, j, m_->desc.vocab));
-                const std::vector<int>& row = pages_.row(rids[i]);
-                const int need = (e.req.input_tokens + kv_->page_tokens - 1) / kv_->page_tokens;
-                for (int j = 0; j < need; ++j) prow.push_back(row.at(static_cast<std::size_t>(j)));
-            }
-            b.slots = slots.data();
-            b.n_tokens = ntok.data();
-            b.tokens = toks.data();
-            b.page_rows = prow.data();
-            b.out_index = oidx.data();
+            build_prompt(rids, B);
             // partition mode: the prefill group's SMs only while decode work exists, else the whole GPU
             const bool active = decode_active();
             cudaStream_t ps = s_prefill_full_ && !active ? s_prefill_full_ : s_prefill_;
@@ -409,22 +459,11 @@ private:
             SW_CUDA(cudaEventRecord(events_[L.start_ev], ps));
             const int yield = opt_.split && active ? opt_.prefill_yield : 0;
             n_prefill_yield_ += yield > 0 ? 1 : 0;
-            prefill_forward(m_, kv_, b, ps, lean, yield);
+            prefill_forward(m_, kv_, B.b, ps, lean, yield);
             SW_CUDA(cudaEventRecord(events_[L.end_ev], ps));
             ++n_prefill_;
         } else {
-            for (int i = 0; i < n; ++i) {
-                const Entry& e = entry(rids[i]);
-                slots[i] = slot_of_.at(rids[i]);
-                pos[i] = e.req.input_tokens + e.generated;  // position of the fed token x_g
-                const int pidx = pos[i] / kv_->page_tokens;
-                newp[i] = pos[i] % kv_->page_tokens == 0 ? pages_.row(rids[i]).at(static_cast<std::size_t>(pidx)) : -1;
-                oidx[i] = e.generated + 1;  // x_{g+1}
-            }
-            b.slots = slots.data();
-            b.positions = pos.data();
-            b.new_page = newp.data();
-            b.out_index = oidx.data();
+            build_step(rids, B);
             cudaStream_t ds = s_decode_[static_cast<std::size_t>(L.lane)];
             if (!s_decode_full_.empty() && !prompt_inflight()) {  // partition mode, decode alone: whole GPU
                 ds = s_decode_full_[static_cast<std::size_t>(L.lane)];
@@ -432,10 +471,118 @@ private:
             }
             SW_CUDA(cudaEventRecord(events_[L.start_ev], ds));
             for (const auto& [se, ee] : L.merged_evs) SW_CUDA(cudaEventRecord(events_[se], ds));
-            decode_forward(m_, kv_, b, ds, opt_.graphs, L.lane, static_cast<int>(s_decode_.size()));
+            decode_forward(m_, kv_, B.b, ds, opt_.graphs, L.lane, static_cast<int>(s_decode_.size()));
             SW_CUDA(cudaEventRecord(events_[L.end_ev], ds));
             for (const auto& [se, ee] : L.merged_evs) SW_CUDA(cudaEventRecord(events_[ee], ds));
             ++n_decode_;
+        }
+    }
+
+    // ---- fused mixed steps (engine.fuse=1: chunked prefill with the
+    // token step riding in each chunk).  A prompt task runs as chunks of whole prompts
+    // (<= engine.chunk_tokens tokens); while it is in flight, every token step the
+    // scheduler requests is merged into the next chunk's launch (mixed_forward: one
+    // weight stream for both phases).  Launches go out one at a time on one stream, so
+    // the step that completes with a chunk can be followed by its successor in the next.
+    struct PromptJob {
+        Launch L;  // the prompt task(s): start_ev recorded at the first chunk, end_ev at the last
+        std::vector<std::vector<int>> chunks;
+        std::size_t next = 0;
+    };
+
+    void fuse_add_prompt(const Launch& L) {
+        PromptJob J;
+        J.L = L;
+        const std::vector<int> rids = rids_of(L.task_seqs);
+        const int cap = std::max(1, std::min(opt_.chunk_tokens > 0 ? opt_.chunk_tokens : (1 << 30),
+                                             m_->pre.rows - kMaxDecodeRows));
+        std::vector<int> cur;
+        int tok = 0;
+        for (int rid : rids) {
+            const int n = entry(rid).req.input_tokens;
+            if (!cur.empty() && (tok + n > cap || cur.size() >= 256)) {
+                J.chunks.push_back(cur);
+                cur.clear();
+                tok = 0;
+            }
+            cur.push_back(rid);
+            tok += n;
+        }
+        if (!cur.empty()) J.chunks.push_back(cur);
+        jobs_.push_back(std::move(J));
+    }
+
+    bool fused_busy() const {
+        return std::any_of(launches_.begin(), launches_.end(), [](const Launch& l) { return !l.done; });
+    }
+
+    void fuse_dispatch() {
+        if (fused_busy()) return;
+        PromptJob* J = jobs_.empty() ? nullptr : &jobs_.front();
+        if (!J && pending_steps_.empty()) return;
+        cudaStream_t st = s_prefill_;
+        BatchBuf P, D;
+        std::vector<int> chunk;
+        bool first_chunk = false, last_chunk = false;
+        int chunk_tok = 0;
+        if (J) {
+            chunk = J->chunks[J->next];
+            first_chunk = J->next == 0;
+            last_chunk = J->next + 1 == J->chunks.size();
+            build_prompt(chunk, P);
+            for (int v : P.ntok) chunk_tok += v;
+        }
+        // the waiting token steps, merged (one decode row set)
+        Launch M;
+        bool step = false;
+        if (!pending_steps_.empty()) {
+            M = pending_steps_.front();
+            M.lane = 0;
+            for (std::size_t i = 1; i < pending_steps_.size(); ++i) {
+                const Launch& o = pending_steps_[i];
+                M.task_seqs.insert(M.task_seqs.end(), o.task_seqs.begin(), o.task_seqs.end());
+                M.merged_evs.push_back({o.start_ev, o.end_ev});
+            }
+            build_step(rids_of(M.task_seqs), D);
+            // fuse only when the rows fit one prefill launch
+            step = !J || chunk_tok + D.b.n <= m_->pre.rows;
+            if (step) pending_steps_.clear();
+        }
+        // ---- launch start events
+        Launch C;  // the chunk's in-flight record (carries the prompt task only on its last chunk)
+        if (J) {
+            C.kind = TaskKind::Prompt;
+            C.start_ev = first_chunk ? J->L.start_ev : new_event();
+            C.end_ev = last_chunk ? J->L.end_ev : new_event();
+            if (last_chunk) C.task_seqs = J->L.task_seqs;
+            C.first_seq = J->L.first_seq;
+            SW_CUDA(cudaEventRecord(events_[C.start_ev], st));
+        }
+        if (step) {
+            SW_CUDA(cudaEventRecord(events_[M.start_ev], st));
+            for (const auto& [se, ee] : M.merged_evs) SW_CUDA(cudaEventRecord(events_[se], st));
+        }
+        // ---- the work
+        if (J && step) {
+            mixed_forward(m_, kv_, P.b, D.b, st);
+            ++n_mixed_;
+        } else if (J) {
+            prefill_forward(m_, kv_, P.b, st);
+            ++n_prefill_;
+        } else {
+            decode_forward(m_, kv_, D.b, st, opt_.graphs, 0, 1);
+            ++n_decode_;
+        }
+        // ---- end events, in-flight records
+        if (step) {
+            SW_CUDA(cudaEventRecord(events_[M.end_ev], st));
+            for (const auto& [se, ee] : M.merged_evs) SW_CUDA(cudaEventRecord(events_[ee], st));
+            launches_.push_back(M);
+        }
+        if (J) {
+            SW_CUDA(cudaEventRecord(events_[C.end_ev], st));
+            launches_.push_back(C);
+            if (++J->next == J->chunks.size()) jobs_.pop_front();
         }
     }
 
@@ -460,7 +607,8 @@ private:
     std::map<int, int> slot_of_;
     unsigned long long polls_ = 0;
     double clock_skew_ = 0.0;
-    int n_prefill_ = 0, n_decode_ = 0;
+    int n_prefill_ = 0, n_decode_ = 0, n_mixed_ = 0;
+    std::deque<PromptJob> jobs_;  // fuse mode: prompt tasks in flight as chunks
 };
 
 EventLog run_split_engine(const SimulationInputs& inputs, Scheduler& scheduler, sw_model* model, sw_kv* kv,
@@ -520,6 +668,8 @@ extern "C" int sw_engine_run(sw_model* m, sw_kv* kv, const char* spec, char** ou
             else if (k == "engine.lean_prefill") opt.lean_prefill = v == "1" || v == "true";
             else if (k == "engine.prefill_yield") opt.prefill_yield = std::stoi(v);
             else if (k == "engine.prefill_priority") opt.prefill_priority = v == "1" || v == "true";
+            else if (k == "engine.fuse") opt.fuse = v == "1" || v == "true";
+            else if (k == "engine.chunk_tokens") opt.chunk_tokens = std::stoi(v);
             else if (k == "engine.peak_flops") opt.peak_flops = std::stod(v);
             else if (k == "engine.peak_bytes") opt.peak_bytes = std::stod(v);
             else throw ConfigError("spec: unknown key '" + k + "'");

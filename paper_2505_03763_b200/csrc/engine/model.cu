@@ -44,7 +44,8 @@ extern std::atomic<unsigned long long> g_launches;
 
 namespace {
 
-constexpr int kLmRowsMax = 256;  // LM-head rows per launch (swap-AB N <= 256)
+constexpr int kLmRowsMax = 256;  // LM-head rows per GEMM pass (swap-AB N <= 256)
+constexpr int kLmBufRows = 512;  // LM-head rows per forward (a fused mixed step: prompts + up to 256 decode rows)
 constexpr int kSplitTiles = 640;     // split-K scratch: (tiles x splits) capacity
 constexpr int kSplitCounters = 1024;
 constexpr int kSsParts = 64;  // sum(x^2) partial rows per norm (d_model / 128 <= 64)
@@ -90,9 +91,9 @@ void ws_alloc(Workspace& w, const sw_model_desc& d, int rows, bool decode, int m
     w.q = dalloc<kv_t>(static_cast<size_t>(rows) * d.n_heads * d.head_dim);
     w.attn = dalloc<__nv_bfloat16>(static_cast<size_t>(rows) * d.n_heads * d.head_dim);
     w.act = dalloc<__nv_bfloat16>(static_cast<size_t>(rows) * d.ffn_dim);
-    w.xlast = dalloc<__nv_bfloat16>(static_cast<size_t>(kLmRowsMax) * d.d_model);
-    w.keys = dalloc<unsigned long long>(kLmRowsMax);
-    SW_CUDA(cudaMemset(w.keys, 0, kLmRowsMax * sizeof(unsigned long long)));
+    w.xlast = dalloc<__nv_bfloat16>(static_cast<size_t>(kLmBufRows) * d.d_model);
+    w.keys = dalloc<unsigned long long>(kLmBufRows);
+    SW_CUDA(cudaMemset(w.keys, 0, kLmBufRows * sizeof(unsigned long long)));
     SW_CUDA(cudaMemset(w.x, 0, static_cast<size_t>(rows) * d.d_model * sizeof(float)));
     SW_CUDA(cudaMemset(w.xn, 0, static_cast<size_t>(rows) * d.d_model * 2));
     SW_CUDA(cudaMemset(w.attn, 0, static_cast<size_t>(rows) * d.n_heads * d.head_dim * 2));
@@ -163,14 +164,18 @@ __global__ void install_pages_kernel(const int32_t* __restrict__ rows, const int
 
 void lm_head(sw_model* m, Workspace& w, int rows, const int* live, float* logits_out, cudaStream_t st) {
     const sw_model_desc& d = m->desc;
-    GemmProblem p = gp(w.xlast, kLmRowsMax, m->lm, d.vocab, rows, d.vocab, d.d_model, EPI_ARGMAX, true, nullptr, 0,
-                       live);
-    p.argmax = w.keys;
-    gemm_run(p, st);
-    if (logits_out) {
-        GemmProblem q = gp(w.xlast, kLmRowsMax, m->lm, d.vocab, rows, d.vocab, d.d_model, EPI_STORE_F32, true,
-                           logits_out, d.vocab, live);
-        gemm_run(q, st);
+    // passes of <= 256 rows (the swap-AB N bound); `live` (graph-captured decode) implies rows <= 256
+    for (int r0 = 0; r0 < rows; r0 += kLmRowsMax) {
+        const int n = std::min(kLmRowsMax, rows - r0);
+        const __nv_bfloat16* x = w.xlast + static_cast<size_t>(r0) * d.d_model;
+        GemmProblem p = gp(x, kLmRowsMax, m->lm, d.vocab, n, d.vocab, d.d_model, EPI_ARGMAX, true, nullptr, 0, live);
+        p.argmax = w.keys + r0;
+        gemm_run(p, st);
+        if (logits_out) {
+            GemmProblem q = gp(x, kLmRowsMax, m->lm, d.vocab, n, d.vocab, d.d_model, EPI_STORE_F32, true,
+                               logits_out + static_cast<int64_t>(r0) * d.vocab, d.vocab, live);
+            gemm_run(q, st);
+        }
     }
 }
 
@@ -184,13 +189,13 @@ int decode_bucket(int n) {
 }
 
 // ------------------------------------------------------------------ prefill
+namespace {
+void prefill_chunk(sw_model* m, sw_kv* kv, const sw_batch& b, int first, int last, int64_t tok_off, int64_t page_off,
+                   const sw_batch* dec, float* logits_out, cudaStream_t st, bool lean, int yield_tiles);
+}  // namespace
+
 void prefill_forward(sw_model* m, sw_kv* kv, const sw_batch& b, cudaStream_t st, bool lean, int yield_tiles) {
     const sw_model_desc& d = m->desc;
-    auto lp = [lean, yield_tiles](GemmProblem p) {
-        p.lean = lean;
-        p.yield_tiles = yield_tiles;
-        return p;
-    };
     Workspace& w = m->pre;
     const int B = kv->page_tokens;
     // Split the batch into chunks of whole prompts that fit the workspace.
@@ -202,170 +207,13 @@ void prefill_forward(sw_model* m, sw_kv* kv, const sw_batch& b, cudaStream_t st,
         if (last == first)
             throw ConfigError("prefill: prompt of " + std::to_string(b.n_tokens[first]) +
                               " tokens exceeds model.max_prefill_tokens=" + std::to_string(w.rows));
-        const int S = last - first;
-        // ---- stage metadata (one H2D copy)
-        int idx;
-        int32_t* h = static_cast<int32_t*>(ring_claim(m->pre_ring, idx));
-        int32_t* p = h + 16;
-        auto take = [&](int n) {
-            int32_t* q = p;
-            p += n;
-            return q;
-        };
-        int32_t *tokens = take(T), *tpos = take(T), *tslot = take(T), *cu = take(S + 1), *sslot = take(S),
-                *lastrow = take(S), *oidx = take(S), *poff = take(S + 1);
-        int n_tiles = 0;
-        for (int s = 0; s < S; ++s) n_tiles += cdiv(b.n_tokens[first + s], 64);
-        int32_t *tseq = take(n_tiles), *tq0 = take(n_tiles);
-        int n_tiles128 = 0;  // 128-row tiles of the tcgen05 attention
-        for (int s = 0; s < S; ++s) n_tiles128 += cdiv(b.n_tokens[first + s], 128);
-        int32_t *tseq128 = take(n_tiles128), *tq0128 = take(n_tiles128);
-        int n_pages_total = 0;
-        for (int s = 0; s < S; ++s) n_pages_total += cdiv(b.n_tokens[first + s], B);
-        int32_t* prow = take(n_pages_total);
-        int t = 0, ti = 0, ti128 = 0, pg = 0;
-        cu[0] = 0;
-        poff[0] = 0;
-        for (int s = 0; s < S; ++s) {
-            const int r = first + s, n = b.n_tokens[r];
-            if (b.slots[r] < 0 || b.slots[r] >= kv->n_slots) throw ContractViolation("prefill: slot out of range");
-            const int np = cdiv(n, B);
-            if (np > kv->max_pages) throw ContractViolation("prefill: prompt exceeds the slot's page-table row");
-            for (int j = 0; j < n; ++j) {
-                tokens[t + j] = b.tokens[tok_off + j];
-                if (tokens[t + j] < 0 || tokens[t + j] >= d.vocab) throw ContractViolation("prefill: token out of range");
-                tpos[t + j] = j;
-                tslot[t + j] = b.slots[r];
-            }
-            for (int j = 0; j < np; ++j) {
-                const int pid = b.page_rows[page_off + j];
-                if (pid < 0 || pid >= kv->n_pages) throw ContractViolation("prefill: page id out of range");
-                prow[pg + j] = pid;
-            }
-            for (int q0 = 0; q0 < n; q0 += 64, ++ti) {
-                tseq[ti] = s;
-                tq0[ti] = q0;
-            }
-            for (int q0 = 0; q0 < n; q0 += 128, ++ti128) {
-                tseq128[ti128] = s;
-                tq0128[ti128] = q0;
-            }
-            tok_off += n;
-            page_off += np;
-            t += n;
-            pg += np;
-            cu[s + 1] = t;
-            poff[s + 1] = pg;
-            sslot[s] = b.slots[r];
-            lastrow[s] = t - 1;
-            oidx[s] = b.out_index ? b.out_index[r] : 0;
+        prefill_chunk(m, kv, b, first, last, tok_off, page_off, nullptr,
+                      b.logits_out ? b.logits_out + static_cast<int64_t>(first) * d.vocab : nullptr, st, lean,
+                      yield_tiles);
+        for (int r = first; r < last; ++r) {
+            tok_off += b.n_tokens[r];
+            page_off += cdiv(b.n_tokens[r], B);
         }
-        h[0] = T;
-        h[1] = S;
-        h[2] = n_tiles;
-        h[3] = n_tiles128;
-        const size_t bytes = static_cast<size_t>(p - h) * sizeof(int32_t);
-        if (bytes > w.pmeta_bytes || bytes > m->pre_ring.bytes) throw ContractViolation("prefill: metadata overflow");
-        SW_CUDA(cudaMemcpyAsync(w.pmeta, h, bytes, cudaMemcpyHostToDevice, st));
-        count_transfer(bytes, 0);
-        ring_release(m->pre_ring, idx, st);
-        auto dev = [&](int32_t* hp) { return w.pmeta + (hp - h); };
-
-        install_pages_kernel<<<S, 64, 0, st>>>(dev(prow), dev(poff), dev(sslot), kv->page_table, kv->max_pages);
-        SW_LAUNCH_CHECK();
-        // ---- layers
-        const int qkv_w = (d.n_heads + 2 * d.n_kv_heads) * d.head_dim;
-        const int hdH = d.n_heads * d.head_dim;
-        embed_tokens(dev(tokens), w.pmeta, T, m->emb, w.x, d.d_model, st);
-        PrefillAttnArgs aa{};
-        aa.n_tiles = w.pmeta + 2;
-        aa.tile_seq = dev(tseq);
-        aa.tile_q0 = dev(tq0);
-        aa.cu_seqlens = dev(cu);
-        aa.seq_slot = dev(sslot);
-        aa.page_table = kv->page_table;
-        aa.max_pages = kv->max_pages;
-        aa.page_tokens = B;
-        aa.page_stride = kv->page_stride;
-        aa.kv_stride = kv->page_stride / 2;
-        aa.H = d.n_heads;
-        aa.Hkv = d.n_kv_heads;
-        aa.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(d.head_dim)));
-        // prefill attention on tcgen05 (SW_PREFILL_TC=0: the mma.sync kernel)
-        static const int tc_env = [] {
-            const char* v = std::getenv("SW_PREFILL_TC");
-            return v && *v ? std::atoi(v) : 1;
-        }();
-        const bool use_tc = tc_env && kv->tm_kv_ok && (d.n_heads / d.n_kv_heads) % 2 == 0;  // head pairs share a kv head
-        // RoPE + KV write fused into the QKV GEMM epilogue (SW_PREFILL_ROPE_FUSED=0: separate rope_kv pass)
-        static const int fuse_env = [] {
-            const char* v = std::getenv("SW_PREFILL_ROPE_FUSED");
-            return v && *v ? std::atoi(v) : 1;
-        }();
-        const bool fuse_rope = fuse_env != 0;
-        PrefillTcArgs ta{};
-        CUtensorMap tm_q{};
-        // persistent prefill attention for short prompts (1B 32 x 512 layer: 165 -> 153 us); prompts of
-        // many 128-row tiles keep one item per CTA (8B 4 x 8192: 4.37 vs 4.63 ms persistent)
-        int max_prompt = 0;
-        for (int s = 0; s < S; ++s) max_prompt = std::max(max_prompt, b.n_tokens[first + s]);
-        const bool tc_persist = max_prompt <= 1024;
-        if (use_tc) {
-            ta.n_tiles = w.pmeta + 3;
-            ta.tile_seq = dev(tseq128);
-            ta.tile_q0 = dev(tq0128);
-            ta.cu_seqlens = dev(cu);
-            ta.seq_slot = dev(sslot);
-            ta.page_table = kv->page_table;
-            ta.max_pages = kv->max_pages;
-            ta.H = d.n_heads;
-            ta.Hkv = d.n_kv_heads;
-            ta.scale_log2 = aa.scale_log2;
-            ta.page_rows = static_cast<int>(kv->page_stride / d.head_dim);
-            ta.v_rows = static_cast<int>(kv->page_stride / 2 / d.head_dim);
-            tm_q = make_tmap_heads(w.q, static_cast<uint64_t>(w.rows), d.n_heads, d.head_dim);
-        }
-        for (int l = 0; l < d.n_layers; ++l) {
-            const LayerWeights& L = m->layers[l];
-            kv_t* kvl = kv->pages + l * kv->layer_stride;
-            rmsnorm(w.x, L.g_attn, w.xn, T, d.d_model, d.norm_eps, nullptr, nullptr, st);
-            if (fuse_rope) {  // QKV GEMM with RoPE + q / paged-KV stores in its epilogue
-                GemmProblem pq = lp(gp(w.xn, w.rows, L.wqkv, qkv_w, T, qkv_w, d.d_model, EPI_QKV_ROPE, false, nullptr, 0));
-                pq.fx.pos = dev(tpos);
-                pq.fx.slot = dev(tslot);
-                pq.fx.page_table = kv->page_table;
-                pq.fx.max_pages = kv->max_pages;
-                pq.fx.page_tokens = B;
-                pq.fx.rope_cs = m->rope_cs;
-                pq.fx.q_out = w.q;
-                pq.fx.kv_layer = kvl;
-                pq.fx.page_stride = kv->page_stride;
-                pq.fx.H = d.n_heads;
-                pq.fx.Hkv = d.n_kv_heads;
-                pq.fx.hd = d.head_dim;
-                gemm_run(pq, st);
-            } else {
-                gemm_run(lp(gp(w.xn, w.rows, L.wqkv, qkv_w, T, qkv_w, d.d_model, EPI_STORE_F32, false, w.qkv, qkv_w)), st);
-                rope_kv(w.qkv, w.q, kvl, dev(tpos), dev(tslot), kv->page_table, m->rope_cs, T, nullptr, d.n_heads,
-                        d.n_kv_heads, d.head_dim, kv->max_pages, B, st);
-            }
-            if (use_tc) {
-                ta.layer_row0 = static_cast<int>(l * kv->layer_stride / d.head_dim);
-                attn_prefill_tc(tm_q, kv->tm_kv, w.attn, ta, n_tiles128, d.head_dim, tc_persist, st);
-            } else {
-                attn_prefill(w.q, kvl, w.attn, aa, n_tiles, d.head_dim, st);
-            }
-            gemm_run(lp(gp(w.attn, w.rows, L.wo, d.d_model, T, d.d_model, hdH, EPI_RESID, false, w.x, d.d_model)), st);
-            rmsnorm(w.x, L.g_mlp, w.xn, T, d.d_model, d.norm_eps, nullptr, nullptr, st);
-            gemm_run(lp(gp(w.xn, w.rows, L.wgu, 2 * d.ffn_dim, T, 2 * d.ffn_dim, d.d_model, EPI_SWIGLU, false, w.act,
-                           d.ffn_dim)),
-                     st);
-            gemm_run(lp(gp(w.act, w.rows, L.wd, d.d_model, T, d.d_model, d.ffn_dim, EPI_RESID, false, w.x, d.d_model)), st);
-        }
-        // ---- last position of every prompt -> LM head + greedy token
-        rmsnorm(w.x, m->g_final, w.xlast, S, d.d_model, d.norm_eps, nullptr, dev(lastrow), st);
-        lm_head(m, w, S, nullptr, b.logits_out ? b.logits_out + static_cast<int64_t>(first) * d.vocab : nullptr, st);
-        finalize_tokens(w.keys, dev(sslot), dev(oidx), S, nullptr, kv->last_token, kv->out_tokens, kv->max_out, st);
         first = last;
     }
 }
@@ -399,6 +247,23 @@ DecodeAttnArgs decode_attn_args(const sw_model* m, const sw_kv* kv, const Worksp
     aa.target_ctas = target;
     aa.max_ctx = kv->max_pages * kv->page_tokens;
     return aa;
+}
+
+DecodeFlatArgs decode_flat_args(const sw_model* m, const sw_kv* kv, const Workspace& w) {
+    const sw_model_desc& d = m->desc;
+    DecodeFlatArgs fa{};
+    fa.meta = w.meta;
+    fa.page_table = kv->page_table;
+    fa.max_pages = kv->max_pages;
+    fa.H = d.n_heads;
+    fa.Hkv = d.n_kv_heads;
+    fa.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(d.head_dim)));
+    fa.page_rows = static_cast<int>(kv->page_stride / d.head_dim);
+    fa.v_rows = static_cast<int>(kv->page_stride / 2 / d.head_dim);
+    fa.part_o = w.flat_o;
+    fa.part_ml = w.flat_ml;
+    fa.counters = w.attn_cnt;
+    return fa;
 }
 
 void decode_layers(sw_model* m, sw_kv* kv, int R, cudaStream_t st, int lane, bool use_flat) {
@@ -439,19 +304,7 @@ void decode_layers(sw_model* m, sw_kv* kv, int R, cudaStream_t st, int lane, boo
     static const int ablate = env_int("SW_ABLATE", 0);  // timing experiments only: skip kernel classes
     DecodeFlatArgs fa{};
     const int flat_ctas = stream_sm_count(st);
-    if (use_flat) {
-        fa.meta = w.meta;
-        fa.page_table = kv->page_table;
-        fa.max_pages = kv->max_pages;
-        fa.H = d.n_heads;
-        fa.Hkv = d.n_kv_heads;
-        fa.scale_log2 = aa.scale_log2;
-        fa.page_rows = static_cast<int>(kv->page_stride / d.head_dim);
-        fa.v_rows = static_cast<int>(kv->page_stride / 2 / d.head_dim);
-        fa.part_o = w.flat_o;
-        fa.part_ml = w.flat_ml;
-        fa.counters = w.attn_cnt;
-    }
+    if (use_flat) fa = decode_flat_args(m, kv, w);
     for (int l = 0; l < d.n_layers; ++l) {
         const LayerWeights& L = m->layers[l];
         kv_t* kvl = kv->pages + l * kv->layer_stride;
@@ -581,6 +434,264 @@ void decode_forward(sw_model* m, sw_kv* kv, const sw_batch& b, cudaStream_t st, 
     }
 }
 
+// ------------------------------------------------------------------ prefill chunk / fused mixed step
+namespace {
+
+// One launch over prompts [first, last) of b (all fit the workspace), plus --
+// for a fused mixed step -- the decode rows of `dec` appended after the prompt
+// tokens: every projection GEMM runs once over [prompt tokens | decode rows].
+void prefill_chunk(sw_model* m, sw_kv* kv, const sw_batch& b, int first, int last, int64_t tok_off, int64_t page_off,
+                   const sw_batch* dec, float* logits_out, cudaStream_t st, bool lean, int yield_tiles) {
+    const sw_model_desc& d = m->desc;
+    auto lp = [lean, yield_tiles](GemmProblem p) {
+        p.lean = lean;
+        p.yield_tiles = yield_tiles;
+        return p;
+    };
+    Workspace& w = m->pre;
+    const int B = kv->page_tokens;
+    const int D = dec ? dec->n : 0;  // fused decode rows
+    int Tp = 0;
+    for (int r = first; r < last; ++r) Tp += b.n_tokens[r];
+    const int T = Tp + D;
+    const int S = last - first;
+    const int NL = S + D;  // LM-head rows: every prompt's last position, then the decode rows
+    // ---- stage metadata (one H2D copy)
+    int idx;
+    int32_t* h = static_cast<int32_t*>(ring_claim(m->pre_ring, idx));
+    int32_t* p = h + 16;
+    auto take = [&](int n) {
+        int32_t* q = p;
+        p += n;
+        return q;
+    };
+    int32_t *tokens = take(Tp), *tpos = take(T), *tslot = take(T), *cu = take(S + 1), *sslot = take(NL),
+            *lastrow = take(NL), *oidx = take(NL), *poff = take(S + 1);
+    int n_tiles = 0;
+    for (int s = 0; s < S; ++s) n_tiles += cdiv(b.n_tokens[first + s], 64);
+    int32_t *tseq = take(n_tiles), *tq0 = take(n_tiles);
+    int n_tiles128 = 0;  // 128-row tiles of the tcgen05 attention
+    for (int s = 0; s < S; ++s) n_tiles128 += cdiv(b.n_tokens[first + s], 128);
+    int32_t *tseq128 = take(n_tiles128), *tq0128 = take(n_tiles128);
+    int n_pages_total = 0;
+    for (int s = 0; s < S; ++s) n_pages_total += cdiv(b.n_tokens[first + s], B);
+    int32_t* prow = take(n_pages_total);
+    int t = 0, ti = 0, ti128 = 0, pg = 0;
+    cu[0] = 0;
+    poff[0] = 0;
+    for (int s = 0; s < S; ++s) {
+        const int r = first + s, n = b.n_tokens[r];
+        if (b.slots[r] < 0 || b.slots[r] >= kv->n_slots) throw ContractViolation("prefill: slot out of range");
+        const int np = cdiv(n, B);
+        if (np > kv->max_pages) throw ContractViolation("prefill: prompt exceeds the slot's page-table row");
+        for (int j = 0; j < n; ++j) {
+            tokens[t + j] = b.tokens[tok_off + j];
+            if (tokens[t + j] < 0 || tokens[t + j] >= d.vocab) throw ContractViolation("prefill: token out of range");
+            tpos[t + j] = j;
+            tslot[t + j] = b.slots[r];
+        }
+        for (int j = 0; j < np; ++j) {
+            const int pid = b.page_rows[page_off + j];
+            if (pid < 0 || pid >= kv->n_pages) throw ContractViolation("prefill: page id out of range");
+            prow[pg + j] = pid;
+        }
+        for (int q0 = 0; q0 < n; q0 += 64, ++ti) {
+            tseq[ti] = s;
+            tq0[ti] = q0;
+        }
+        for (int q0 = 0; q0 < n; q0 += 128, ++ti128) {
+            tseq128[ti128] = s;
+            tq0128[ti128] = q0;
+        }
+        tok_off += n;
+        page_off += np;
+        t += n;
+        pg += np;
+        cu[s + 1] = t;
+        poff[s + 1] = pg;
+        sslot[s] = b.slots[r];
+        lastrow[s] = t - 1;
+        oidx[s] = b.out_index ? b.out_index[r] : 0;
+    }
+    // fused decode rows: token rows [Tp, T) of every projection, their own positions and slots
+    StepMeta* dm = nullptr;
+    int dm_idx = -1;
+    if (D > 0) {
+        dm = static_cast<StepMeta*>(ring_claim(m->mix_ring, dm_idx));
+        dm->n = D;
+        for (int i = 0; i < D; ++i) {
+            const int slot = dec->slots[i], pos = dec->positions[i];
+            if (slot < 0 || slot >= kv->n_slots) throw ContractViolation("mixed step: slot out of range");
+            if (pos < 0 || pos >= kv->max_pages * kv->page_tokens)
+                throw ContractViolation("mixed step: position out of range");
+            dm->slot[i] = slot;
+            dm->pos[i] = pos;
+            dm->token[i] = dec->tokens ? dec->tokens[i] : -1;
+            dm->new_page[i] = dec->new_page ? dec->new_page[i] : -1;
+            if (dm->new_page[i] >= kv->n_pages) throw ContractViolation("mixed step: page id out of range");
+            dm->out_index[i] = dec->out_index ? dec->out_index[i] : -1;
+            tpos[Tp + i] = pos;
+            tslot[Tp + i] = slot;
+            sslot[S + i] = slot;
+            lastrow[S + i] = Tp + i;
+            oidx[S + i] = dm->out_index[i];
+        }
+    }
+    h[0] = Tp;
+    h[1] = S;
+    h[2] = n_tiles;
+    h[3] = n_tiles128;
+    const size_t bytes = static_cast<size_t>(p - h) * sizeof(int32_t);
+    if (bytes > w.pmeta_bytes || bytes > m->pre_ring.bytes) throw ContractViolation("prefill: metadata overflow");
+    SW_CUDA(cudaMemcpyAsync(w.pmeta, h, bytes, cudaMemcpyHostToDevice, st));
+    count_transfer(bytes, 0);
+    ring_release(m->pre_ring, idx, st);
+    auto dev = [&](int32_t* hp) { return w.pmeta + (hp - h); };
+    Workspace& mw = m->mix;
+    if (D > 0) {
+        const size_t mbytes = offsetof(StepMeta, slot) + sizeof(StepMeta::slot) * 5;
+        SW_CUDA(cudaMemcpyAsync(mw.meta, dm, mbytes, cudaMemcpyHostToDevice, st));
+        count_transfer(mbytes, 0);
+        ring_release(m->mix_ring, dm_idx, st);
+    }
+
+    install_pages_kernel<<<S, 64, 0, st>>>(dev(prow), dev(poff), dev(sslot), kv->page_table, kv->max_pages);
+    SW_LAUNCH_CHECK();
+    // ---- layers
+    const int qkv_w = (d.n_heads + 2 * d.n_kv_heads) * d.head_dim;
+    const int hdH = d.n_heads * d.head_dim;
+    embed_tokens(dev(tokens), w.pmeta, Tp, m->emb, w.x, d.d_model, st);
+    if (D > 0)  // decode rows: the slot's last token (device resident), new pages installed first
+        embed(mw.meta, D, m->emb, m->layers[0].g_attn, w.x + static_cast<size_t>(Tp) * d.d_model,
+              w.xn + static_cast<size_t>(Tp) * d.d_model, mw.ss, d.d_model, kv->last_token, kv->page_table,
+              kv->max_pages, kv->page_tokens, st);
+    PrefillAttnArgs aa{};
+    aa.n_tiles = w.pmeta + 2;
+    aa.tile_seq = dev(tseq);
+    aa.tile_q0 = dev(tq0);
+    aa.cu_seqlens = dev(cu);
+    aa.seq_slot = dev(sslot);
+    aa.page_table = kv->page_table;
+    aa.max_pages = kv->max_pages;
+    aa.page_tokens = B;
+    aa.page_stride = kv->page_stride;
+    aa.kv_stride = kv->page_stride / 2;
+    aa.H = d.n_heads;
+    aa.Hkv = d.n_kv_heads;
+    aa.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(d.head_dim)));
+    // prefill attention on tcgen05 (SW_PREFILL_TC=0: the mma.sync kernel)
+    static const int tc_env = env_int("SW_PREFILL_TC", 1);
+    const bool use_tc = tc_env && kv->tm_kv_ok && (d.n_heads / d.n_kv_heads) % 2 == 0;  // head pairs share a kv head
+    // RoPE + KV write fused into the QKV GEMM epilogue (SW_PREFILL_ROPE_FUSED=0: separate rope_kv pass)
+    static const int fuse_env = env_int("SW_PREFILL_ROPE_FUSED", 1);
+    const bool fuse_rope = fuse_env != 0;
+    PrefillTcArgs ta{};
+    CUtensorMap tm_q{};
+    // persistent prefill attention for short prompts (1B 32 x 512 layer: 165 -> 153 us); prompts of
+    // many 128-row tiles keep one item per CTA (8B 4 x 8192: 4.37 vs 4.63 ms persistent)
+    int max_prompt = 0;
+    for (int s = 0; s < S; ++s) max_prompt = std::max(max_prompt, b.n_tokens[first + s]);
+    const bool tc_persist = max_prompt <= 1024;
+    if (use_tc) {
+        ta.n_tiles = w.pmeta + 3;
+        ta.tile_seq = dev(tseq128);
+        ta.tile_q0 = dev(tq0128);
+        ta.cu_seqlens = dev(cu);
+        ta.seq_slot = dev(sslot);
+        ta.page_table = kv->page_table;
+        ta.max_pages = kv->max_pages;
+        ta.H = d.n_heads;
+        ta.Hkv = d.n_kv_heads;
+        ta.scale_log2 = aa.scale_log2;
+        ta.page_rows = static_cast<int>(kv->page_stride / d.head_dim);
+        ta.v_rows = static_cast<int>(kv->page_stride / 2 / d.head_dim);
+        tm_q = make_tmap_heads(w.q, static_cast<uint64_t>(w.rows), d.n_heads, d.head_dim);
+    }
+    // decode rows' attention: the decode kernels over their paged contexts (q and output rows from Tp on)
+    DecodeAttnArgs da{};
+    DecodeFlatArgs fa{};
+    bool flat = false;
+    const int R = D > 0 ? decode_bucket(D) : 0;
+    if (D > 0) {
+        da = decode_attn_args(m, kv, mw);
+        long long ctx = 0;
+        for (int i = 0; i < D; ++i) ctx += dec->positions[i] + 1;
+        flat = kv->tm_kv_ok && (ctx >= 2048LL * D || D * d.n_kv_heads <= 2 * stream_sm_count(st));
+        if (flat) fa = decode_flat_args(m, kv, mw);
+    }
+    kv_t* const q_dec = w.q + static_cast<size_t>(Tp) * hdH;
+    __nv_bfloat16* const attn_dec = w.attn + static_cast<size_t>(Tp) * hdH;
+    for (int l = 0; l < d.n_layers; ++l) {
+        const LayerWeights& L = m->layers[l];
+        kv_t* kvl = kv->pages + l * kv->layer_stride;
+        rmsnorm(w.x, L.g_attn, w.xn, T, d.d_model, d.norm_eps, nullptr, nullptr, st);
+        if (fuse_rope) {  // QKV GEMM with RoPE + q / paged-KV stores in its epilogue
+            GemmProblem pq = lp(gp(w.xn, w.rows, L.wqkv, qkv_w, T, qkv_w, d.d_model, EPI_QKV_ROPE, false, nullptr, 0));
+            pq.fx.pos = dev(tpos);
+            pq.fx.slot = dev(tslot);
+            pq.fx.page_table = kv->page_table;
+            pq.fx.max_pages = kv->max_pages;
+            pq.fx.page_tokens = B;
+            pq.fx.rope_cs = m->rope_cs;
+            pq.fx.q_out = w.q;
+            pq.fx.kv_layer = kvl;
+            pq.fx.page_stride = kv->page_stride;
+            pq.fx.H = d.n_heads;
+            pq.fx.Hkv = d.n_kv_heads;
+            pq.fx.hd = d.head_dim;
+            gemm_run(pq, st);
+        } else {
+            gemm_run(lp(gp(w.xn, w.rows, L.wqkv, qkv_w, T, qkv_w, d.d_model, EPI_STORE_F32, false, w.qkv, qkv_w)), st);
+            rope_kv(w.qkv, w.q, kvl, dev(tpos), dev(tslot), kv->page_table, m->rope_cs, T, nullptr, d.n_heads,
+                    d.n_kv_heads, d.head_dim, kv->max_pages, B, st);
+        }
+        if (use_tc) {
+            ta.layer_row0 = static_cast<int>(l * kv->layer_stride / d.head_dim);
+            attn_prefill_tc(tm_q, kv->tm_kv, w.attn, ta, n_tiles128, d.head_dim, tc_persist, st);
+        } else {
+            attn_prefill(w.q, kvl, w.attn, aa, n_tiles, d.head_dim, st);
+        }
+        if (D > 0) {
+            if (flat) {
+                fa.layer_row0 = static_cast<int>(l * kv->layer_stride / d.head_dim);
+                attn_decode_flat(kv->tm_kv, q_dec, attn_dec, fa, stream_sm_count(st), d.head_dim,
+                                 d.n_heads / d.n_kv_heads, st);
+            } else {
+                attn_decode(q_dec, kvl, attn_dec, da, R, d.head_dim, st);
+            }
+        }
+        gemm_run(lp(gp(w.attn, w.rows, L.wo, d.d_model, T, d.d_model, hdH, EPI_RESID, false, w.x, d.d_model)), st);
+        rmsnorm(w.x, L.g_mlp, w.xn, T, d.d_model, d.norm_eps, nullptr, nullptr, st);
+        gemm_run(lp(gp(w.xn, w.rows, L.wgu, 2 * d.ffn_dim, T, 2 * d.ffn_dim, d.d_model, EPI_SWIGLU, false, w.act,
+                       d.ffn_dim)),
+                 st);
+        gemm_run(lp(gp(w.act, w.rows, L.wd, d.d_model, T, d.d_model, d.ffn_dim, EPI_RESID, false, w.x, d.d_model)), st);
+    }
+    // ---- last position of every prompt (+ every decode row) -> LM head + greedy token
+    rmsnorm(w.x, m->g_final, w.xlast, NL, d.d_model, d.norm_eps, nullptr, dev(lastrow), st);
+    lm_head(m, w, NL, nullptr, logits_out, st);
+    finalize_tokens(w.keys, dev(sslot), dev(oidx), NL, nullptr, kv->last_token, kv->out_tokens, kv->max_out, st);
+}
+
+}  // namespace
+
+void mixed_forward(sw_model* m, sw_kv* kv, const sw_batch& pre, const sw_batch& dec, cudaStream_t st,
+                   float* logits_out) {
+    int T = 0;
+    for (int i = 0; i < pre.n; ++i) T += pre.n_tokens[i];
+    if (pre.n < 1 || dec.n < 1) throw ConfigError("mixed step: needs at least one prompt and one decode row");
+    if (dec.n > kMaxDecodeRows) throw ContractViolation("mixed step: decode rows out of range");
+    if (pre.n > kLmRowsMax) throw ConfigError("mixed step: at most 256 prompts per launch");
+    if (T + dec.n > m->pre.rows)
+        throw ConfigError("mixed step: prompt tokens + decode rows exceed one prefill launch (max_prefill_tokens=" +
+                          std::to_string(m->pre.rows) + ")");
+    if (!m->mix.meta) {
+        ws_alloc(m->mix, m->desc, 1, true, 16);  // StepMeta + split-KV / flat partials + sum(x^2) scratch
+        ring_init(m->mix_ring, 8, sizeof(StepMeta));
+    }
+    prefill_chunk(m, kv, pre, 0, pre.n, 0, 0, &dec, logits_out, st, false, 0);
+}
+
 }  // namespace sw
 
 // ====================================================================== C-ABI
@@ -682,7 +793,7 @@ extern "C" int sw_model_destroy(sw_model* m) {
         cudaDeviceSynchronize();
         for (auto& [k, g] : m->graphs)
             if (g.exec) cudaGraphExecDestroy(g.exec);
-        std::vector<Workspace*> all{&m->pre};
+        std::vector<Workspace*> all{&m->pre, &m->mix};
         for (auto& w : m->dec) all.push_back(&w);
         for (Workspace* w : all) {
             for (void* p : {(void*)w->x, (void*)w->xn, (void*)w->qkv, (void*)w->q, (void*)w->attn, (void*)w->act,
@@ -691,7 +802,7 @@ extern "C" int sw_model_destroy(sw_model* m) {
                             (void*)w->ss, (void*)w->flat_o, (void*)w->flat_ml})
                 if (p) cudaFree(p);
         }
-        std::vector<PinnedRing*> rings{&m->pre_ring};
+        std::vector<PinnedRing*> rings{&m->pre_ring, &m->mix_ring};
         for (auto& r : m->dec_ring) rings.push_back(&r);
         for (PinnedRing* r : rings) {
             for (void* p : r->slots) cudaFreeHost(p);
@@ -835,5 +946,14 @@ extern "C" int sw_op_rmsnorm(const float* x, const void* gain, void* y, int32_t 
     return guarded([&] {
         rmsnorm(x, static_cast<const __nv_bfloat16*>(gain), static_cast<__nv_bfloat16*>(y), rows, dim, eps, nullptr,
                 nullptr, static_cast<cudaStream_t>(stream));
+    });
+}
+
+extern "C" int sw_mixed_enqueue(sw_model* m, sw_kv* kv, const sw_batch* pre, const sw_batch* dec, void* stream) {
+    return guarded([&] {
+        if (!m || !kv || !pre || !dec || !pre->slots || !pre->n_tokens || !pre->tokens || !pre->page_rows ||
+            !dec->slots || !dec->positions)
+            throw ConfigError("sw_mixed_enqueue: null argument");
+        mixed_forward(m, kv, *pre, *dec, static_cast<cudaStream_t>(stream), pre->logits_out);
     });
 }

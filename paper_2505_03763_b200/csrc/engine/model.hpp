@@ -83,11 +83,12 @@ struct sw_model {
     float* inv_freq = nullptr;
     float2* rope_cs = nullptr;  // [kMaxPositions][hd/2] (cos, sin)
     sw::Workspace pre;
+    sw::Workspace mix;  // decode-row scratch of fused mixed steps (StepMeta, split-KV partials); lazy
     // decode lanes: one workspace + staging ring + graph set per concurrent
     // decode stream (lanes of different instances may step at the same time)
     static constexpr int kMaxDecodeLanes = 4;
     sw::Workspace dec[kMaxDecodeLanes];
-    sw::PinnedRing pre_ring, dec_ring[kMaxDecodeLanes];
+    sw::PinnedRing pre_ring, mix_ring, dec_ring[kMaxDecodeLanes];
     // (arena, row bucket, lane | mode, partition): a graph runs in the context it was captured in
     std::map<std::tuple<const sw_kv*, int, int, const void*>, sw::DecodeGraph> graphs;
     unsigned long long* scratch_u64 = nullptr;
@@ -118,6 +119,16 @@ constexpr int kMaxPositions = 32768;  // RoPE table extent (max context)
 // yield_tiles: > 0 caps the tiles per GEMM CTA (decode CTAs interleave at tile granularity)
 void prefill_forward(sw_model* m, sw_kv* kv, const sw_batch& b, cudaStream_t st, bool lean = false,
                      int yield_tiles = 0);
+// One fused mixed step (the split-phase co-execution of a prompt chunk and a
+// token step): the decode rows of `dec` (sw_decode_enqueue semantics) ride in
+// the prefill pass of `pre` -- every projection GEMM runs once over
+// [prompt tokens | decode rows] (the weights stream once for both phases),
+// the prompts attend causally with the tcgen05 prefill kernel, the decode rows
+// over their paged contexts with the decode kernel.  All prompts and decode
+// rows must fit one launch (tokens + rows <= max_prefill_tokens, prompts + rows
+// <= 256).  logits (optional, parity) = prompts' last positions, then decode rows.
+void mixed_forward(sw_model* m, sw_kv* kv, const sw_batch& pre, const sw_batch& dec, cudaStream_t st,
+                   float* logits_out = nullptr);
 void decode_forward(sw_model* m, sw_kv* kv, const sw_batch& b, cudaStream_t st, bool use_graph, int lane = 0,
                     int lanes = 1);
 int decode_bucket(int n);

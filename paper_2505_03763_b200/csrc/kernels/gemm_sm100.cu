@@ -838,8 +838,9 @@ void gemm_run(const GemmProblem& p, cudaStream_t st) {
             // on the Llama-1B step (tools/profile_step.py)
             static const int dec_ctas = env_flag("SW_DEC_CTAS", 0);
             static const int s_qkv = env_flag("SW_DEC_S_QKV", 0);  // experiment: fixed split for the QKV projection
+            // (the experiment knob is clamped like the rule: a portable cluster of <= 8, >= 2 K-blocks per rank)
             const int S = p.mode == EPI_QKV_ROPE && s_qkv > 0
-                              ? s_qkv
+                              ? std::max(1, std::min({s_qkv, 8, p.K / BK / 2}))
                               : gemm_decode_splits(tiles, p.K / BK, dec_ctas > 0 ? dec_ctas : 2 * sms);
             static const int dec_log = env_flag("SW_DEC_LOG", 0);
             if (dec_log) {

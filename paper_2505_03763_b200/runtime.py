@@ -96,6 +96,29 @@ class Engine:
         torch.cuda.synchronize()
         return out.cpu().numpy() if out is not None else None
 
+    def mixed(self, slots: Sequence[int], prompts: Sequence[np.ndarray], page_rows: Sequence[Sequence[int]],
+              dec_slots, dec_positions, dec_tokens=None, dec_new_page=None, out_index=None, dec_out_index=None,
+              logits: bool = True):
+        """One fused mixed step (sw_mixed_enqueue): prompts and decode rows in one
+        pass.  Returns logits [prompts + decode rows, vocab] (prompts first)."""
+        import torch
+
+        n, nd = len(slots), len(dec_slots)
+        out = torch.empty((n + nd, self.desc.vocab), dtype=torch.float32, device="cuda") if logits else None
+        toks = np.concatenate([np.asarray(p, dtype=np.int64) for p in prompts])
+        keep = [_i32(slots), _i32([len(p) for p in prompts]), _i32(toks), _i32([x for r in page_rows for x in r]),
+                _i32(out_index if out_index is not None else [0] * n), _i32(dec_slots), _i32(dec_positions)]
+        pb = Batch(n=n, slots=keep[0], n_tokens=keep[1], tokens=keep[2], page_rows=keep[3], out_index=keep[4],
+                   logits_out=out.data_ptr() if out is not None else None)
+        db = Batch(n=nd, slots=keep[5], positions=keep[6])
+        for field, vals in (("tokens", dec_tokens), ("new_page", dec_new_page), ("out_index", dec_out_index)):
+            if vals is not None:
+                keep.append(_i32(vals))
+                setattr(db, field, keep[-1])
+        check(lib().sw_mixed_enqueue(self.model, self.kv, ctypes.byref(pb), ctypes.byref(db), self._stream()))
+        torch.cuda.synchronize()
+        return out.cpu().numpy() if out is not None else None
+
     def tensor(self, name: str):
         """(device pointer, numel) of a weight tensor."""
         p, n = ctypes.c_void_p(), ctypes.c_int64()

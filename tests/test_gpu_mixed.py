@@ -1,0 +1,141 @@
+"""Fused mixed steps (sw_mixed_enqueue): a prompt chunk and a token step in
+one pass -- every projection GEMM runs once over [prompt tokens | decode rows]
+-- against the pure fp32 oracle at the north-star bar (per-row rel-L2 and
+elementwise <= 1e-2, greedy tokens identical outside near-ties), on the tiny
+configs[0] model and at the Llama-3.2-1B / Llama-3-8B widths with wide decode
+batches, plus the token-level equivalence with the unfused prefill + decode."""
+import dataclasses
+
+import numpy as np
+import pytest
+
+pytest.importorskip("torch")
+
+from oracle import model as M
+from test_gpu_model import Bars
+
+pytestmark = pytest.mark.gpu
+
+
+def _run_mixed(eng, oracle, name, n_dec, dec_len, pre_lens, warm_steps=2, rid0=300, emu=None):
+    """Prefill n_dec prompts of dec_len tokens, decode warm_steps steps, then one
+    mixed step: prompts `pre_lens` (new slots) + one decode row per running slot."""
+    d = eng.desc
+    per = (max([dec_len + warm_steps + 2] + [L + 1 for L in pre_lens]) + 15) // 16
+    dec_slots = list(range(n_dec))
+    pre_slots = list(range(n_dec, n_dec + len(pre_lens)))
+    rows = {s: [s * per + j for j in range(per)] for s in dec_slots + pre_slots}
+    bars = Bars(name)
+
+    def call(method, *a):  # the fp32 oracle and (optionally) the one emulating the kernels' 16-bit storage points
+        return getattr(oracle, method)(*a), (getattr(emu, method)(*a) if emu else None)
+
+    prompts = [M.prompt_tokens(d.seed, rid0 + s, dec_len, d.vocab) for s in dec_slots]
+    for c0 in range(0, n_dec, 64):  # prefill the running batch (workspace-sized chunks)
+        idx = dec_slots[c0:c0 + 64]
+        eng.prefill(idx, [prompts[i] for i in idx], [rows[i][:(dec_len + 15) // 16] for i in idx], logits=False)
+    ref, _ = call("prefill", prompts, [rows[s] for s in dec_slots])
+    toks = [int(np.argmax(r)) for r in ref]
+    pos = [dec_len] * n_dec
+    for _ in range(warm_steps):
+        newp = [rows[s][pos[i] // 16] if pos[i] % 16 == 0 else -1 for i, s in enumerate(dec_slots)]
+        eng.decode(dec_slots, pos, tokens=toks, new_page=newp, logits=False)
+        ref, _ = call("decode", toks, pos, [rows[s] for s in dec_slots])
+        toks = [int(np.argmax(r)) for r in ref]
+        pos = [p + 1 for p in pos]
+    # the mixed step
+    new_prompts = [M.prompt_tokens(d.seed, rid0 + 1000 + s, L, d.vocab) for s, L in zip(pre_slots, pre_lens)]
+    newp = [rows[s][pos[i] // 16] if pos[i] % 16 == 0 else -1 for i, s in enumerate(dec_slots)]
+    lg = eng.mixed(pre_slots, new_prompts, [rows[s][:(L + 15) // 16] for s, L in zip(pre_slots, pre_lens)],
+                   dec_slots, pos, dec_tokens=toks, dec_new_page=newp)
+    ref_pre, emu_pre = call("prefill", new_prompts, [rows[s] for s in pre_slots])
+    ref_dec, emu_dec = call("decode", toks, pos, [rows[s] for s in dec_slots])
+    bars.add(lg[:len(pre_lens)], ref_pre, emu_pre)
+    bars.add(lg[len(pre_lens):], ref_dec, emu_dec)
+    # the KV the mixed step wrote is the oracle's: one more (plain) decode step over every slot
+    toks2 = [int(np.argmax(r)) for r in ref_dec] + [int(np.argmax(r)) for r in ref_pre]
+    pos2 = [p + 1 for p in pos] + list(pre_lens)
+    slots2 = dec_slots + pre_slots
+    newp2 = [rows[s][p // 16] if p % 16 == 0 else -1 for s, p in zip(slots2, pos2)]
+    lg2 = eng.decode(slots2, pos2, tokens=toks2, new_page=newp2)
+    ref2, emu2 = call("decode", toks2, pos2, [rows[s] for s in slots2])
+    bars.add(lg2, ref2, emu2)
+    bars.check()
+    for s in slots2:
+        oracle.release(rows[s])
+        if emu:
+            emu.release(rows[s])
+    return bars
+
+
+@pytest.fixture(scope="module")
+def tiny():
+    from paper_2505_03763_b200 import runtime
+
+    eng = runtime.Engine(M.TINY, max_prefill_tokens=2048, max_decode_batch=64, n_pages=2048, n_slots=96,
+                         max_pages_per_slot=16, max_out=40)
+    yield eng
+    eng.close()
+
+
+def test_mixed_step_tiny(tiny):
+    o = M.OracleModel(M.TINY)
+    emu = M.OracleModel(M.TINY, emulate_bf16=True, share_weights_with=o)
+    _run_mixed(tiny, o, "tiny mixed: 3 prompts + 5 decode rows", 5, 37, [40, 17, 64], emu=emu)
+    _run_mixed(tiny, o, "tiny mixed: 1 prompt + 40 decode rows", 40, 23, [120], rid0=900, emu=emu)
+
+
+def test_mixed_tokens_match_unfused(tiny):
+    """The fused step and the unfused prefill + decode give the same greedy
+    tokens (outside near-ties of the oracle) and the same device state."""
+    import paper_2505_03763_b200 as sw
+
+    d = M.TINY
+    slots = list(range(8))
+    rows = [[s * 8 + j for j in range(8)] for s in slots]
+    prompts = [M.prompt_tokens(d.seed, 50 + s, 30 + s, d.vocab) for s in slots[:4]]
+    late = [M.prompt_tokens(d.seed, 60 + s, 20 + 3 * s, d.vocab) for s in slots[4:]]
+    outs = []
+    for fused in (False, True):
+        tiny.prefill(slots[:4], prompts, [r[:(len(p) + 15) // 16] for r, p in zip(rows[:4], prompts)], logits=False)
+        pos = [len(p) for p in prompts]
+        newp = [rows[i][pos[i] // 16] if pos[i] % 16 == 0 else -1 for i in range(4)]
+        late_rows = [r[:(len(p) + 15) // 16] for r, p in zip(rows[4:], late)]
+        if fused:
+            lg = tiny.mixed(slots[4:], late, late_rows, slots[:4], pos, dec_new_page=newp)
+            dec, pre = lg[4:], lg[:4]
+        else:
+            pre = tiny.prefill(slots[4:], late, late_rows)
+            dec = tiny.decode(slots[:4], pos, new_page=newp)
+        outs.append((pre, dec))
+    for a, b in zip(outs[0], outs[1]):
+        for ra, rb in zip(a, b):
+            assert np.linalg.norm(ra - rb) / np.linalg.norm(rb) < 1e-2
+            if M.top2_margin(rb) > 1e-2 * np.abs(rb).max():
+                assert int(np.argmax(ra)) == int(np.argmax(rb))
+
+
+@pytest.mark.parametrize("shape,n_dec,pre_lens", [("LLAMA_1B", 128, [700, 300]), ("LLAMA_8B", 160, [513, 1000])])
+def test_mixed_step_wide(shape, n_dec, pre_lens):
+    """Wide decode batches riding in the prefill GEMMs at the real widths
+    (1B: 2 layers, hd 64; 8B: 1 layer, hd 128, vocab cut to 4096)."""
+    from paper_2505_03763_b200 import runtime
+
+    base = getattr(M, shape)
+    desc = dataclasses.replace(base, n_layers=2 if shape == "LLAMA_1B" else 1, vocab=4096)
+    eng = runtime.Engine(desc, max_prefill_tokens=4096, max_decode_batch=256, n_pages=(n_dec + 8) * 80,
+                         n_slots=n_dec + 8, max_pages_per_slot=80, max_out=16)
+    try:
+        o = M.OracleModel(desc)
+        _run_mixed(eng, o, f"{shape} mixed: {len(pre_lens)} prompts + {n_dec} decode rows", n_dec, 90, pre_lens)
+    finally:
+        eng.close()
+
+
+def test_mixed_rejects_oversized_launch(tiny):
+    import paper_2505_03763_b200 as sw
+
+    d = M.TINY
+    p = M.prompt_tokens(d.seed, 1, 2040, d.vocab)
+    with pytest.raises(sw.ConfigError):
+        tiny.mixed([90], [p], [list(range(128))], list(range(16)), [5] * 16)
