@@ -1,28 +1,33 @@
 // Prefill attention on the 5th-generation tensor cores (sm_100a tcgen05/TMEM).
 //
 // Causal flash attention for a varlen batch of prompts over the paged KV cache
-// (GQA).  One CTA = 128 query rows of one prompt for TWO query heads of the
-// same kv head: two independent 128-thread groups (warps 0-3 | 4-7), each with
-// its own S/O accumulators in TMEM, P buffer, MMA-issuing thread and barriers,
-// sharing the K/V blocks -- while one group runs its softmax the tensor core
-// works on the other group's MMAs.  Thread t of a group owns query row t (TMEM
-// lane t).  Per 128-key block j and group:
-//   S  = Q K_j^T        tcgen05.mma M=128 N=128 K=hd, Q and K from smem
-//                       (TMA SWIZZLE_128B, K-major), S fp32 in TMEM cols [0,128)
-//   softmax             each thread tcgen05.ld's its S row twice (max, then
-//                       exp2/sum), online max/sum in fp32 (log2 domain), P as
-//                       fp16 into smem in the K-major 128B-swizzled layout
-//   O += P V_j          tcgen05.mma M=128 N=hd K=128, P (K-major) and V from
-//                       smem -- V is [keys][hd] as stored, i.e. MN-major for
-//                       the B operand (instruction-descriptor transpose bit);
-//                       O fp32 in TMEM cols [128, 128+hd), rescaled in place
-//                       (tcgen05.ld/st) only when a row's max moved.
-// Q (a 3-D TMA map over [tokens][H][hd]) and K/V (one 16-row TMA box per page
-// slice, the arena-wide map of the decode attention) are loaded by thread 0:
-// K double-buffered (block j+1 lands while block j's softmax runs), V single
-// (block j+1's V lands during the next S MMA and softmax); a stage is reloaded
-// once both groups' MMAs released it (count-2 "empty" barriers).  smem: 144 KB
-// (hd 64) / 224 KB (hd 128), TMEM: 512 columns -- one CTA per SM.
+// (GQA).  One work item = 128 query rows of one prompt for TWO query heads of
+// the same kv head (they share every K/V block).  Warp-specialised CTA of 10
+// warps:
+//   warps 0-3 / 4-7   softmax of head 0 / head 1: thread t owns query row t
+//                     (TMEM lane t); per 128-key block it tcgen05.ld's its S
+//                     row ONCE (128 fp32 registers), takes the row max, writes
+//                     P = exp2(S*scale - m) as fp16 back into TMEM over the
+//                     first 64 columns of its own S accumulator, and arrives
+//                     on p_full.  The running max is lazy: O and l are
+//                     rescaled only when a block's max exceeds the max in use
+//                     by more than 2^8 (P <= 256 then, exact in the final O/l);
+//   warp 8            tcgen05.mma issuer (one thread):  S_g = Q_g K_j^T (SS,
+//                     M=128 N=128 K=hd) and O_g += P_g V_j (TS: P from TMEM,
+//                     V from smem as an MN-major B operand), in the order
+//                     PV_0(j), S_0(j+1), PV_1(j), S_1(j+1): the tensor pipe
+//                     runs one head's products while the other head's softmax
+//                     runs.  S_g(j+1) overwrites P_g(j) only after PV_g(j) in
+//                     the pipe's issue order;
+//   warp 9            TMA producer: Q of both heads (3-D map over
+//                     [tokens][H][hd]) and the K/V blocks, one 16-row box per
+//                     page slice through the arena-wide map of the decode
+//                     attention, into a ring of NS 128-key slots (K_0, Q, V_0,
+//                     K_1, V_1, ...), so loads run several blocks ahead.
+// TMEM (512 columns): S_0 [0,128), S_1 [128,256), O_0 [256,256+hd),
+// O_1 [384,384+hd).  smem: Q (2 stages at hd 64) + the K/V ring, 193 KB (hd 64)
+// / 225 KB (hd 128): one CTA per SM.  Items are dealt to a persistent grid (or
+// one per CTA) last query tile first, snake order across rounds.
 #include <cuda.h>
 
 #include <algorithm>
@@ -39,8 +44,6 @@ namespace {
 constexpr int kRows = 128;     // query rows per CTA
 constexpr int kBlk = 128;      // keys per block
 constexpr int kPg = 16;        // tokens per page
-
-__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 // 3-D TMA load (inner, middle, outer coordinates).
 __device__ __forceinline__ void tma_load_3d(void* dst, const void* tmap, uint64_t* bar, int c0, int c1, int c2) {
@@ -78,63 +81,110 @@ __device__ __forceinline__ uint64_t umma_desc_sw128_mn(uint32_t smem_byte_addr, 
     return d;
 }
 
-template <int HD>
-struct TcCfg {
-    static constexpr int NH = HD / 64;                 // 64-wide column atoms of a head row
-    static constexpr int kAtom = kRows * 128;          // one [128 rows][128 B] atom column
-    static constexpr int kQ = NH * kAtom;              // one group's Q tile
-    static constexpr int kKV = NH * kAtom;             // one K (or V) block of 128 keys
-    static constexpr int kP = 2 * kAtom;               // P: 128 rows x 128 keys bf16
-    static constexpr int kOffK = 2 * kQ;               // K: two stages
-    static constexpr int kOffV = kOffK + 2 * kKV;      // V: one stage
-    static constexpr int kOffP = kOffV + kKV;          // P: one per group
-    static constexpr int kOffBar = kOffP + 2 * kP;
-    static constexpr int kSmem = 1024 + kOffBar + 128;
-    static_assert(kSmem <= 227 * 1024, "smem budget");
-    static constexpr uint32_t kTmemCols = 512;          // group g: S [256g, 256g+128), O [256g+128, +HD)
-};
+// 32 lanes x 16 32-bit columns, registers -> TMEM (P: 32 fp16 keys per thread per call).
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+        "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+        "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+        : "memory");
+}
+
+// D[tmem] (+)= A[tmem] . B[smem]: the A operand (128 rows x 16 K, fp16 pairs per
+// 32-bit column, K-major) read from tensor memory.
+__device__ __forceinline__ void umma_f16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
+                                            uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}" ::"r"(tmem_d),
+        "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
 
 template <int HD>
-__global__ void __launch_bounds__(256, 1) attn_prefill_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
+struct TcCfg {
+    static constexpr int NH = HD / 64;           // 64-wide (128 B) column atoms of a head row
+    static constexpr int kAtom = kRows * 128;    // one [128 rows][128 B] atom column
+    static constexpr int kQ = NH * kAtom;        // one head's Q tile
+    static constexpr int NQ = HD == 64 ? 2 : 1;  // Q stages (both heads per stage)
+    static constexpr int kSlot = NH * kAtom;     // one K or V block of 128 keys
+    static constexpr int NS = HD == 64 ? 8 : 5;  // K/V ring slots
+    static constexpr int kOffRing = NQ * 2 * kQ;
+    static constexpr int kOffBar = kOffRing + NS * kSlot;
+    static constexpr int kSmem = 1024 + kOffBar + 256;
+    static_assert(kSmem <= 227 * 1024, "smem budget");
+    static constexpr uint32_t kTmemCols = 512;
+    // warpgroups: softmax head 0 | softmax head 1 | MMA warp, TMA warp, two idle warps (setmaxnreg is
+    // warpgroup-wide: the third group keeps 88 registers a thread and gives the rest to the softmax rows, 208 each)
+    static constexpr int kThreads = 384;
+};
+
+// Work item k of CTA bx (both producer and consumers walk the same sequence).
+struct Item {
+    int tile, pair, start, len, q0, nblk, npages;
+    const int32_t* ptab;
+};
+__device__ __forceinline__ bool next_item(const PrefillTcArgs& a, int k, Item& x) {
+    const int pairs = a.H / 2;
+    const int n_items = *a.n_tiles * pairs;
+    const int G = static_cast<int>(gridDim.x), bx = static_cast<int>(blockIdx.x);
+    const int idx = k * G + ((k & 1) ? G - 1 - bx : bx);
+    if (idx >= n_items) return false;
+    const int item = n_items - 1 - idx;  // last query tile first (most keys)
+    x.tile = item / pairs;
+    x.pair = item % pairs;
+    const int sq = a.tile_seq[x.tile];
+    x.q0 = a.tile_q0[x.tile];
+    x.start = a.cu_seqlens[sq];
+    x.len = a.cu_seqlens[sq + 1] - x.start;
+    const int kend = min(x.q0 + kRows, x.len);  // keys this tile attends to: [0, kend)
+    x.nblk = (kend + kBlk - 1) / kBlk;
+    x.npages = (x.len + kPg - 1) / kPg;
+    x.ptab = a.page_table + static_cast<long long>(a.seq_slot[sq]) * a.max_pages;
+    return true;
+}
+
+template <int HD>
+__global__ void __launch_bounds__(384, 1) attn_prefill_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
                                                               const __grid_constant__ CUtensorMap tm_kv,
                                                               __nv_bfloat16* __restrict__ out, PrefillTcArgs a) {
     using C = TcCfg<HD>;
+    constexpr int NS = C::NS, NQ = C::NQ;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sQ = smem;
-    uint8_t* sK = smem + C::kOffK;
-    uint8_t* sV = smem + C::kOffV;
-    uint8_t* sP = smem + C::kOffP;
+    uint8_t* sRing = smem + C::kOffRing;
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + C::kOffBar);
-    uint64_t* q_full = bar;
-    uint64_t* k_full = bar + 1;   // [2]
-    uint64_t* k_empty = bar + 3;  // [2] both groups' S MMAs of the stage retired
-    uint64_t* v_full = bar + 5;
-    uint64_t* v_empty = bar + 6;  // both groups' PV MMAs retired
-    uint64_t* s_done_g = bar + 7;  // [2] per group
-    uint64_t* o_done_g = bar + 9;  // [2] per group
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 11);
+    uint64_t* q_full = bar;             // [NQ]
+    uint64_t* q_empty = q_full + NQ;    // [NQ]  both heads' last S MMA of the item retired
+    uint64_t* kv_full = q_empty + NQ;   // [NS]
+    uint64_t* kv_empty = kv_full + NS;  // [NS]  both heads' MMAs reading the slot retired
+    uint64_t* s_full = kv_empty + NS;   // [2]   S_g of the block in TMEM
+    uint64_t* p_full = s_full + 2;      // [2]   P_g in TMEM (128 arrivals), O_g rescaled
+    uint64_t* o_done = p_full + 2;      // [2]   the item's last PV_g retired
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 2);
 
-    const int tid = threadIdx.x, warp = tid >> 5;
-    const int g = warp >> 2;              // group: query head 2 * pair + g
-    const int gt = tid & 127;             // thread within the group = query row
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     if (tid == 0) {
-        mbar_init(q_full, 1);
-        mbar_init(&k_full[0], 1);
-        mbar_init(&k_full[1], 1);
-        mbar_init(&k_empty[0], 2);
-        mbar_init(&k_empty[1], 2);
-        mbar_init(v_full, 1);
-        mbar_init(v_empty, 2);
-        for (int q = 0; q < 2; ++q) {
-            mbar_init(&s_done_g[q], 1);
-            mbar_init(&o_done_g[q], 1);
+        for (int i = 0; i < NQ; ++i) {
+            mbar_init(&q_full[i], 1);
+            mbar_init(&q_empty[i], 1);
+        }
+        for (int i = 0; i < NS; ++i) {
+            mbar_init(&kv_full[i], 1);
+            mbar_init(&kv_empty[i], 1);
+        }
+        for (int g = 0; g < 2; ++g) {
+            mbar_init(&s_full[g], 1);
+            mbar_init(&p_full[g], 128);
+            mbar_init(&o_done[g], 1);
         }
         fence_mbar_init();
         tma_prefetch_desc(&tm_q);
         tma_prefetch_desc(&tm_kv);
     }
-    if (warp == 0) {
+    if (warp == 8) {
         tmem_alloc(tmem_slot, C::kTmemCols);
         tmem_relinquish();
     }
@@ -142,208 +192,223 @@ __global__ void __launch_bounds__(256, 1) attn_prefill_tc_kernel(const __grid_co
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
-    const uint32_t tS = tmem + 256 * g, tO = tS + kBlk;
-    uint64_t* s_done = &s_done_g[g];
-    uint64_t* o_done = &o_done_g[g];
-    uint8_t* sQg = sQ + g * C::kQ;
-    uint8_t* sPg = sP + g * C::kP;
 
-    // Persistent: work items (128-row query tile, head pair) dealt to the CTAs last tile first
-    // (a prompt's later query tiles attend to more keys) in a snake order -- round k runs
-    // left to right when k is even, right to left when odd -- so the heavy and light items
-    // of consecutive rounds pair up on one CTA.  With one CTA per item (non-persistent) the
-    // same mapping makes the hardware's in-order block issue longest-first (8B 4 x 8192:
-    // 4.36 -> 4.26 ms per layer).  Barrier phases run on the CTA's global key-block count
-    // gb (K stage gb & 1) and item count it.
-    const int pairs = a.H / 2;
-    const int n_items = *a.n_tiles * pairs;
-    const int G = static_cast<int>(gridDim.x), bx = static_cast<int>(blockIdx.x);
-    int gb = 0, it = 0;
-    for (int k = 0;; ++k, ++it) {
-    const int idx = k * G + ((k & 1) ? G - 1 - bx : bx);
-    if (idx >= n_items) break;
-    const int item = n_items - 1 - idx;
-    const int tile = item / pairs, pair = item % pairs;
-    const int h = 2 * pair + g;
-    const int hk = h / (a.H / a.Hkv);     // same for both groups (H / Hkv even)
-    const int sq = a.tile_seq[tile];
-    const int q0 = a.tile_q0[tile];
-    const int start = a.cu_seqlens[sq];
-    const int len = a.cu_seqlens[sq + 1] - start;
-    const int kend = min(q0 + kRows, len);        // keys this tile attends to: [0, kend)
-    const int nblk = (kend + kBlk - 1) / kBlk;
-    const int npages = (len + kPg - 1) / kPg;
-    const int32_t* ptab = a.page_table + static_cast<long long>(a.seq_slot[sq]) * a.max_pages;
-
-    // K (v = 0) or V (v = 1) of key block j into `dst`, completing on `b` (thread 0).
-    // Page ids past the prompt read page 0 (finite data, masked).
-    auto load_blk = [&](int j, int v, uint8_t* dst, uint64_t* b) {
-        const uint64_t pol = l2_policy_evict_last();  // re-read by the prompt's later query tiles
-        int pid[kBlk / kPg];
+    if (warp >= 8) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 88;");
+    if (warp == 9) {
+        // ------------------------------------------------------------ TMA producer
+        if (lane == 0) {
+            const uint64_t pol = l2_policy_evict_last();  // K/V re-read by the prompt's later query tiles
+            int n = 0, qi = 0;
+            Item x{};
+            // slot n of the ring <- K (v = 0) or V (v = 1) of key block j; page ids past the prompt read
+            // page 0 (finite data, masked)
+            auto load_slot = [&](int j, int v) {
+                const int s = n % NS;
+                if (n >= NS) mbar_wait(&kv_empty[s], ((n / NS) - 1) & 1);
+                uint8_t* dst = sRing + s * C::kSlot;
+                const int hk = (2 * x.pair) / (a.H / a.Hkv);
+                int pid[kBlk / kPg];
 #pragma unroll
-        for (int i = 0; i < kBlk / kPg; ++i) {
-            const int pg = j * (kBlk / kPg) + i;
-            pid[i] = pg < npages ? ptab[pg] : 0;
+                for (int i = 0; i < kBlk / kPg; ++i) {
+                    const int pg = j * (kBlk / kPg) + i;
+                    pid[i] = pg < x.npages ? x.ptab[pg] : 0;
+                }
+                mbar_expect_tx(&kv_full[s], C::kSlot);
+#pragma unroll
+                for (int i = 0; i < kBlk / kPg; ++i) {
+                    const int kr = a.layer_row0 + pid[i] * a.page_rows + hk * kPg + (v ? a.v_rows : 0);
+#pragma unroll
+                    for (int c = 0; c < C::NH; ++c)
+                        tma_load_2d(dst + c * C::kAtom + i * kPg * 128, &tm_kv, &kv_full[s], c * 64, kr, pol);
+                }
+                ++n;
+            };
+            for (int k = 0; next_item(a, k, x); ++k) {
+                load_slot(0, 0);
+                const int qs = qi % NQ;
+                if (qi >= NQ) mbar_wait(&q_empty[qs], ((qi / NQ) - 1) & 1);
+                mbar_expect_tx(&q_full[qs], 2 * C::kQ);
+#pragma unroll
+                for (int g = 0; g < 2; ++g)
+#pragma unroll
+                    for (int c = 0; c < C::NH; ++c)
+                        tma_load_3d(sQ + (qs * 2 + g) * C::kQ + c * C::kAtom, &tm_q, &q_full[qs], c * 64,
+                                    2 * x.pair + g, x.start + x.q0);
+                ++qi;
+                load_slot(0, 1);
+                for (int j = 1; j < x.nblk; ++j) {
+                    load_slot(j, 0);
+                    load_slot(j, 1);
+                }
+            }
         }
-        mbar_expect_tx(b, C::kKV);
+        __syncwarp();
+    } else if (warp == 8) {
+        // ------------------------------------------------------------ MMA issuer
+        if (lane == 0) {
+            constexpr uint32_t idesc_s = umma_idesc_f16(kRows, kBlk);
+            constexpr uint32_t idesc_o = umma_idesc_f16(kRows, HD) | (1u << 16);  // B (V) MN-major
+            const uint32_t ring = smem_addr(sRing);
+            int n = 0, qi = 0, gb = 0;
+            Item x{};
+            for (int k = 0; next_item(a, k, x); ++k) {
+                const int qs = qi % NQ;
+                mbar_wait(&q_full[qs], (qi / NQ) & 1);
+                const uint32_t q_addr = smem_addr(sQ + qs * 2 * C::kQ);
+                auto issue_s = [&](int g, int slot) {
+                    const uint32_t kb = ring + slot * C::kSlot;
 #pragma unroll
-        for (int i = 0; i < kBlk / kPg; ++i) {
-            const int kr = a.layer_row0 + pid[i] * a.page_rows + hk * kPg + (v ? a.v_rows : 0);
+                    for (int c = 0; c < C::NH; ++c)
 #pragma unroll
-            for (int c = 0; c < C::NH; ++c) tma_load_2d(dst + c * C::kAtom + i * kPg * 128, &tm_kv, b, c * 64, kr, pol);
+                        for (int kk = 0; kk < 4; ++kk)
+                            umma_bf16(tmem + 128 * g, umma_desc_sw128(q_addr + g * C::kQ + c * C::kAtom + kk * 32),
+                                      umma_desc_sw128(kb + c * C::kAtom + kk * 32), idesc_s, (c | kk) != 0 ? 1u : 0u);
+                    umma_commit(&s_full[g]);
+                };
+                {
+                    const int s = n % NS;
+                    mbar_wait(&kv_full[s], (n / NS) & 1);
+                    tc_fence_after();
+                    issue_s(0, s);
+                    issue_s(1, s);
+                    umma_commit(&kv_empty[s]);
+                    if (x.nblk == 1) umma_commit(&q_empty[qs]);
+                }
+                for (int j = 0; j < x.nblk; ++j) {
+                    const int nv = n + 2 * j + 1, sv = nv % NS;
+                    const int nk = nv + 1, sk = nk % NS;
+                    const bool more = j + 1 < x.nblk;
+                    mbar_wait(&kv_full[sv], (nv / NS) & 1);
+                    const uint32_t vb = ring + sv * C::kSlot;
+#pragma unroll
+                    for (int g = 0; g < 2; ++g) {
+                        mbar_wait(&p_full[g], (gb + j) & 1);
+                        tc_fence_after();
+#pragma unroll
+                        for (int kc = 0; kc < kBlk / 16; ++kc)
+                            umma_f16_ts(tmem + 256 + 128 * g, tmem + 128 * g + kc * 8,
+                                        umma_desc_sw128_mn(vb + kc * 2048, C::kAtom), idesc_o, (j | kc) != 0 ? 1u : 0u);
+                        if (more) {
+                            if (g == 0) {
+                                mbar_wait(&kv_full[sk], (nk / NS) & 1);
+                                tc_fence_after();
+                            }
+                            issue_s(g, sk);
+                        } else {
+                            umma_commit(&o_done[g]);
+                        }
+                    }
+                    umma_commit(&kv_empty[sv]);
+                    if (more) {
+                        umma_commit(&kv_empty[sk]);
+                        if (j + 2 == x.nblk) umma_commit(&q_empty[qs]);
+                    }
+                }
+                n += 2 * x.nblk;
+                gb += x.nblk;
+                ++qi;
+            }
         }
-    };
-    if (tid == 0) {
-        // the previous item's S MMAs (both groups) retired: Q and that K stage are free
-        if (gb >= 1) mbar_wait(&k_empty[(gb - 1) & 1], ((gb - 1) >> 1) & 1);
-        mbar_expect_tx(q_full, 2 * C::kQ);
-#pragma unroll
-        for (int q = 0; q < 2; ++q)
-#pragma unroll
-            for (int c = 0; c < C::NH; ++c)
-                tma_load_3d(sQ + q * C::kQ + c * C::kAtom, &tm_q, q_full, c * 64, 2 * pair + q, start + q0);
-        if (gb >= 2) mbar_wait(&k_empty[gb & 1], ((gb - 2) >> 1) & 1);
-        load_blk(0, 0, sK + (gb & 1) * C::kKV, &k_full[gb & 1]);
-        if (gb >= 1) mbar_wait(v_empty, (gb - 1) & 1);  // both groups' last PV retired: V is free
-        load_blk(0, 1, sV, v_full);
+        __syncwarp();
     }
-
-    // fp16 operands (q, K/V cache, P: common.cuh kv_t)
-    constexpr uint32_t idesc_s = umma_idesc_f16(kRows, kBlk);
-    constexpr uint32_t idesc_o = umma_idesc_f16(kRows, HD) | (1u << 16);  // B (V) MN-major
-    const uint32_t q_addr = smem_addr(sQg), k_addr = smem_addr(sK), v_addr = smem_addr(sV), p_addr = smem_addr(sPg);
-    const int row = gt;                        // query row of this thread (TMEM lane)
-    const int qp = q0 + row;                   // its position in the prompt
-    const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
-    float m_run = -INFINITY, l_run = 0.f;
-
-    for (int j = 0; j < nblk; ++j) {
-        const int G = gb + j;  // global key-block index: barrier phases
-        const int s = G & 1;
-        // ---- S = Q K_j^T (K_{j+1} streams into the other stage once both groups' S_{G-1} retired)
-        if (tid == 0 && j + 1 < nblk) {
-            if (G >= 1) mbar_wait(&k_empty[s ^ 1], ((G - 1) >> 1) & 1);
-            load_blk(j + 1, 0, sK + (s ^ 1) * C::kKV, &k_full[s ^ 1]);
-        }
-        if (gt == 0) {
-            if (j == 0) mbar_wait(q_full, it & 1);
-            mbar_wait(&k_full[s], (G >> 1) & 1);
+    } else {
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 208;");
+        // ------------------------------------------------------------ softmax (thread = query row)
+        const int g = warp >> 2;
+        const int row = tid & 127;
+        const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
+        const uint32_t tS = tmem + lane_off + 128 * g;  // S_g; P_g over its first 64 columns
+        const uint32_t tO = tmem + lane_off + 256 + 128 * g;
+        const float sl = a.scale_log2;
+        int gb = 0, it = 0;
+        Item x{};
+        for (int k = 0; next_item(a, k, x); ++k) {
+            const int h = 2 * x.pair + g;
+            const int qp = x.q0 + row;  // this row's position in the prompt
+            float m_use = -INFINITY, l_run = 0.f;
+            for (int j = 0; j < x.nblk; ++j) {
+                mbar_wait(&s_full[g], (gb + j) & 1);
+                tc_fence_after();
+                uint32_t r[128];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) tmem_ld32(tS + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32 * c]));
+                tmem_ld_wait();
+                // the diagonal / prompt-end block (the last): keys [kbase, kbase + nvalid) are valid
+                const int nvalid = j + 1 == x.nblk ? min(kBlk, min(qp + 1, x.len) - j * kBlk) : kBlk;
+                float mx0 = -INFINITY, mx1 = -INFINITY;
+#pragma unroll
+                for (int i = 0; i < 128; i += 2) {
+                    if (i < nvalid) mx0 = fmaxf(mx0, __uint_as_float(r[i]));
+                    if (i + 1 < nvalid) mx1 = fmaxf(mx1, __uint_as_float(r[i + 1]));
+                }
+                const float mb = fmaxf(mx0, mx1) * sl;  // finite: every row has a valid key in every block
+                float alpha = 1.f;
+                if (j == 0) {
+                    m_use = mb;
+                } else if (mb > m_use + 8.f) {  // lazy rescale: only when P would exceed 2^8
+                    alpha = fast_exp2(m_use - mb);
+                    m_use = mb;
+                }
+                if (__any_sync(0xffffffffu, alpha != 1.f)) {  // O_g is stable: PV_g(j-1) retired before S_g(j)
+#pragma unroll
+                    for (int c = 0; c < HD / 32; ++c) {
+                        uint32_t o[32];
+                        tmem_ld32(tO + c * 32, o);
+                        tmem_ld_wait();
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+                        tmem_st32(tO + c * 32, o);
+                    }
+                }
+                float rs0 = 0.f, rs1 = 0.f;
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    uint32_t pk[16];
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) {
+                        const int k0 = 32 * c + 2 * i;
+                        const float p0 = k0 < nvalid ? fast_exp2(fmaf(__uint_as_float(r[k0]), sl, -m_use)) : 0.f;
+                        const float p1 = k0 + 1 < nvalid ? fast_exp2(fmaf(__uint_as_float(r[k0 + 1]), sl, -m_use)) : 0.f;
+                        rs0 += p0;
+                        rs1 += p1;
+                        pk[i] = pack_h2(p0, p1);
+                    }
+                    tmem_st16(tS + c * 16, pk);
+                }
+                l_run = l_run * alpha + (rs0 + rs1);
+                tmem_st_wait();
+                tc_fence_before();
+                mbar_arrive(&p_full[g]);
+            }
+            // ---- epilogue: O / l -> bf16 (TMEM loads are warp-collective; rows past the prompt do not store)
+            mbar_wait(&o_done[g], it & 1);
             tc_fence_after();
-#pragma unroll
-            for (int c = 0; c < C::NH; ++c)
-#pragma unroll
-                for (int k = 0; k < 4; ++k)
-                    umma_bf16(tS, umma_desc_sw128(q_addr + c * C::kAtom + k * 32),
-                              umma_desc_sw128(k_addr + s * C::kKV + c * C::kAtom + k * 32), idesc_s,
-                              (c | k) != 0 ? 1u : 0u);
-            umma_commit(s_done);
-            umma_commit(&k_empty[s]);
-        }
-        mbar_wait(s_done, G & 1);
-        tc_fence_after();
-        // ---- softmax of this thread's row (two passes over TMEM: max, then exp/sum/P)
-        const int kbase = j * kBlk;
-        const int nvalid = min(kBlk, min(qp + 1, len) - kbase);  // keys [kbase, kbase + nvalid) are valid
-        uint32_t r[32];
-        float mx = -INFINITY;
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-            tmem_ld32(tS + lane_off + c * 32, r);
-            tmem_ld_wait();
-#pragma unroll
-            for (int i = 0; i < 32; ++i)
-                if (c * 32 + i < nvalid) mx = fmaxf(mx, __uint_as_float(r[i]));
-        }
-        const float m_new = fmaxf(m_run, mx * a.scale_log2);  // finite: key 0 of block 0 is valid
-        const float alpha = fast_exp2(m_run - m_new);
-        m_run = m_new;
-        float rs = 0.f;
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-            tmem_ld32(tS + lane_off + c * 32, r);
-            tmem_ld_wait();
-            uint32_t pk[16];
-#pragma unroll
-            for (int i = 0; i < 16; ++i) {
-                const int k0 = c * 32 + 2 * i;
-                const float p0 = k0 < nvalid ? fast_exp2(fmaf(__uint_as_float(r[2 * i]), a.scale_log2, -m_new)) : 0.f;
-                const float p1 =
-                    k0 + 1 < nvalid ? fast_exp2(fmaf(__uint_as_float(r[2 * i + 1]), a.scale_log2, -m_new)) : 0.f;
-                rs += p0 + p1;
-                pk[i] = pack_h2(p0, p1);
-            }
-            // keys [32c, 32c + 32): atom c / 2, 16 B chunks (c % 2) * 4 + q, XOR-swizzled by row
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const int chunk = (c & 1) * 4 + q;
-                const uint32_t dst = p_addr + (c >> 1) * C::kAtom + row * 128 + ((chunk ^ (row & 7)) << 4);
-                asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(dst), "r"(pk[4 * q]), "r"(pk[4 * q + 1]),
-                             "r"(pk[4 * q + 2]), "r"(pk[4 * q + 3])
-                             : "memory");
-            }
-        }
-        l_run = l_run * alpha + rs;
-        // ---- rescale O in place when a row's max moved (O of block j-1 is complete: o_done waited)
-        if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
+            const float inv = 1.f / l_run;
+            __nv_bfloat16* dst = out + (static_cast<long long>(x.start) + qp) * a.H * HD + static_cast<long long>(h) * HD;
 #pragma unroll
             for (int c = 0; c < HD / 32; ++c) {
-                tmem_ld32(tO + lane_off + c * 32, r);
+                uint32_t o[32];
+                tmem_ld32(tO + c * 32, o);
                 tmem_ld_wait();
+                if (qp < x.len) {
 #pragma unroll
-                for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha);
-                tmem_st32(tO + lane_off + c * 32, r);
+                    for (int v = 0; v < 4; ++v)
+                        *reinterpret_cast<uint4*>(dst + c * 32 + v * 8) =
+                            make_uint4(pack_bf2(__uint_as_float(o[8 * v]) * inv, __uint_as_float(o[8 * v + 1]) * inv),
+                                       pack_bf2(__uint_as_float(o[8 * v + 2]) * inv, __uint_as_float(o[8 * v + 3]) * inv),
+                                       pack_bf2(__uint_as_float(o[8 * v + 4]) * inv, __uint_as_float(o[8 * v + 5]) * inv),
+                                       pack_bf2(__uint_as_float(o[8 * v + 6]) * inv, __uint_as_float(o[8 * v + 7]) * inv));
+                }
             }
-            tmem_st_wait();
-        }
-        fence_proxy_async_smem();  // P (generic-proxy stores) -> visible to the tensor core
-        tc_fence_before();
-        asm volatile("bar.sync %0, 128;" ::"r"(1 + g) : "memory");  // this group's 128 threads
-        // ---- O += P V_j
-        if (gt == 0) {
-            mbar_wait(v_full, G & 1);
-            tc_fence_after();
-#pragma unroll
-            for (int kc = 0; kc < kBlk / 16; ++kc)
-                umma_bf16(tO, umma_desc_sw128(p_addr + (kc >> 2) * C::kAtom + (kc & 3) * 32),
-                          umma_desc_sw128_mn(v_addr + kc * 2048, C::kAtom), idesc_o, (j | kc) != 0 ? 1u : 0u);
-            umma_commit(o_done);
-            umma_commit(v_empty);
-        }
-        mbar_wait(o_done, G & 1);  // this group's P and O are free again
-        tc_fence_after();
-        if (tid == 0 && j + 1 < nblk) {  // V_{j+1} once both groups' PV_j retired
-            mbar_wait(v_empty, G & 1);
-            load_blk(j + 1, 1, sV, v_full);
+            tc_fence_before();  // these O loads precede the next item's first PV (after this thread's p_full arrive)
+            gb += x.nblk;
+            ++it;
         }
     }
-
-    // ---- epilogue: O / l -> bf16 (TMEM loads are warp-collective: every lane loads, rows past the prompt
-    // do not store)
-    {
-        const float inv = 1.f / l_run;
-        __nv_bfloat16* dst = out + (static_cast<long long>(start) + qp) * a.H * HD + static_cast<long long>(h) * HD;
-#pragma unroll
-        for (int c = 0; c < HD / 32; ++c) {
-            uint32_t r[32];
-            tmem_ld32(tO + lane_off + c * 32, r);
-            tmem_ld_wait();
-            if (qp < len) {
-#pragma unroll
-                for (int v = 0; v < 4; ++v)
-                    *reinterpret_cast<uint4*>(dst + c * 32 + v * 8) =
-                        make_uint4(pack_bf2(__uint_as_float(r[8 * v]) * inv, __uint_as_float(r[8 * v + 1]) * inv),
-                                   pack_bf2(__uint_as_float(r[8 * v + 2]) * inv, __uint_as_float(r[8 * v + 3]) * inv),
-                                   pack_bf2(__uint_as_float(r[8 * v + 4]) * inv, __uint_as_float(r[8 * v + 5]) * inv),
-                                   pack_bf2(__uint_as_float(r[8 * v + 6]) * inv, __uint_as_float(r[8 * v + 7]) * inv));
-            }
-        }
-    }
-    tc_fence_before();  // this item's O loads precede the group's next PV (ordered by its next bar.sync)
-    gb += nblk;
-    }  // items
     tc_fence_before();
     __syncthreads();
-    if (warp == 0) {
+    if (warp == 8) {
         tc_fence_after();
         tmem_dealloc(tmem, C::kTmemCols);
     }
@@ -358,7 +423,7 @@ void tc_launch(const CUtensorMap& tq, const CUtensorMap& tkv, __nv_bfloat16* out
         SW_CUDA(cudaFuncSetAttribute(attn_prefill_tc_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
         cfg = true;
     }
-    // persistent: one CTA per SM of the stream's partition (smem and TMEM allow one), items round robin
+    // persistent: one CTA per SM of the stream's partition (smem and TMEM allow one), items dealt round robin
     static const int persist_env = [] {  // SW_PREFILL_TC_PERSIST=0/1 forces (A/B); default: the caller's choice
         const char* v = std::getenv("SW_PREFILL_TC_PERSIST");
         return v && *v ? std::atoi(v) : -1;
@@ -366,7 +431,7 @@ void tc_launch(const CUtensorMap& tq, const CUtensorMap& tkv, __nv_bfloat16* out
     const bool persist = persist_env >= 0 ? persist_env != 0 : persistent;
     const int items = max_tiles * (a.H / 2);
     const int grid = std::max(1, persist ? std::min(items, stream_sm_count(st)) : items);
-    launch_k(attn_prefill_tc_kernel<HD>, dim3(grid), dim3(256), C::kSmem, st, tq, tkv, out, a);
+    launch_k(attn_prefill_tc_kernel<HD>, dim3(grid), dim3(C::kThreads), C::kSmem, st, tq, tkv, out, a);
 }
 
 }  // namespace
