@@ -858,6 +858,25 @@ void gemm_run(const GemmProblem& p, cudaStream_t st) {
             // decode projections: cluster split-K, column-distributed reduction
             // two CTAs per SM fit (<= 112 KB smem each); measured: 2 x SMs beats 1 x SMs
             // on the Llama-1B step (tools/profile_step.py)
+            // more feature tiles than SMs (Llama-8B gate/up: 224 tiles): gemm_decode2.cu deals each SM
+            // tiles / SMs whole tiles plus an equal stream-K share of the remainder tiles, so every SM
+            // streams the same weight bytes (the cluster form below leaves 76 SMs with two tiles and 72
+            // with one: at b > 128 rows the MMAs of the doubled SMs set the time).  Gates (SW_GEMM_DSK=0
+            // disables): rows > SW_DSK_MINBN (128: at b <= 128 the cluster form measured faster in-step) and >= SW_DSK_MINU K-blocks of remainder per CTA.
+            static const int dsk_env = env_flag("SW_GEMM_DSK", 1);
+            static const int dsk_minu = std::max(1, env_flag("SW_DSK_MINU", 8));
+            static const int dsk_minbn = env_flag("SW_DSK_MINBN", 128);
+            if (dsk_env && tiles > grid_sms && bn > dsk_minbn) {
+                const int P = grid_sms, nk = p.K / BK;
+                const int rem = tiles % P;
+                if ((rem == 0 || rem * nk / P >= dsk_minu) && gemm_decode_sk_ws_floats(P, bn) <= p.ws_floats &&
+                    p.counters && 2 * tiles <= p.n_counters) {
+                    a.stream_k = 0;
+                    gemm_decode_sk_run(tmap_cached(p.W, p.w_rows, p.K, BM), tmap_cached(p.X, p.x_rows, p.K, bn), a, bn,
+                                       tiles, P, st);
+                    return;
+                }
+            }
             static const int dec_ctas = env_flag("SW_DEC_CTAS", 0);
             static const int s_qkv = env_flag("SW_DEC_S_QKV", 0);  // experiment: fixed split for the QKV projection
             // (the experiment knob is clamped like the rule: a portable cluster of <= 8, >= 2 K-blocks per rank)

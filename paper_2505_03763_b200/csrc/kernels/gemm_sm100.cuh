@@ -98,5 +98,9 @@ int gemm_decode_splits(int tiles, int nk, int ctas);
 size_t gemm_decode_ws_floats(int tiles, int S, int bn);
 void gemm_decode_run(const CUtensorMap& a, const CUtensorMap& b, const GemmArgs& args, int bn, int S, int tiles,
                      cudaStream_t st);
+// decode projections, stream-K over a persistent grid of P CTAs (gemm_decode2.cu)
+size_t gemm_decode_sk_ws_floats(int P, int bn);
+void gemm_decode_sk_run(const CUtensorMap& a, const CUtensorMap& b, const GemmArgs& args, int bn, int tiles, int P,
+                        cudaStream_t st);
 
 }  // namespace sw

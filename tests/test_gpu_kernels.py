@@ -71,6 +71,37 @@ def test_gemm_swiglu(swlib, M, K):
     assert _rel(C, ref) < 1e-2
 
 
+# More feature tiles than SMs at decode widths (the Llama-8B gate/up: 224 tiles): whole tiles per SM
+# plus a stream-K remainder with a deterministic partial reduction (gemm_decode2.cu).  Two calls
+# back to back also check that the per-tile counters re-arm.
+@pytest.mark.parametrize("M", [65, 129, 256])
+@pytest.mark.parametrize("N,K", [(28672, 1024), (20480, 2048), (28672, 4096)])
+def test_gemm_decode_wide(swlib, M, N, K):
+    g = torch.Generator(device="cuda").manual_seed(M * 3 + N + K)
+    A = torch.randn(M, K, device="cuda", generator=g).bfloat16()
+    B = (torch.randn(N, K, device="cuda", generator=g) / K ** 0.5).bfloat16()
+    ref = A.float() @ B.float().T
+    C = torch.zeros(M, N, device="cuda", dtype=torch.bfloat16)
+    _gemm(swlib, A, B, C, 0)
+    assert _rel(C, ref) < 8e-3, (M, N, K)
+    C2 = torch.zeros_like(C)
+    _gemm(swlib, A, B, C2, 0)
+    assert torch.equal(C, C2)
+
+
+@pytest.mark.parametrize("M", [129, 256])
+def test_gemm_swiglu_wide(swlib, M):
+    F, K = 14336, 2048  # 224 tiles of [gate 64 | up 64]
+    g = torch.Generator(device="cuda").manual_seed(M + 5)
+    A = torch.randn(M, K, device="cuda", generator=g).bfloat16()
+    W = (torch.randn(2 * F, K, device="cuda", generator=g) / K ** 0.5).bfloat16()
+    C = torch.zeros(M, F, device="cuda", dtype=torch.bfloat16)
+    _gemm(swlib, A, W, C, 2)
+    gg = (A.float() @ W.float().T).view(M, F // 64, 2, 64)
+    ref = (torch.nn.functional.silu(gg[:, :, 0]) * gg[:, :, 1]).reshape(M, F)
+    assert _rel(C, ref) < 1e-2
+
+
 @pytest.mark.parametrize("rows,dim", [(1, 256), (7, 2048), (300, 4096)])
 def test_rmsnorm(swlib, rows, dim):
     x = torch.randn(rows, dim, device="cuda") * 3
