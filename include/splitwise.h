@@ -75,7 +75,8 @@ typedef struct sw_batch {
     int32_t n;
     const int32_t* slots;
     const int32_t* n_tokens;  /* prefill */
-    const int32_t* positions; /* decode */
+    const int32_t* positions; /* decode: each row's position; prefill (may be NULL): each prompt chunk's
+                                 first position, a multiple of 128, earlier positions already in its pages */
     const int32_t* tokens;
     const int32_t* page_rows; /* prefill */
     const int32_t* new_page;  /* decode, may be NULL */

@@ -47,6 +47,8 @@ def ledger_replay(csv: str) -> List[Tuple[float, int, int, int]]:
             if kv["kind"] == "prompt":
                 inst = int(kv["inst"])
                 for rid in batches[int(kv["batch"])]:
+                    if rid in inst_of:  # a later chunk of a chunked prompt: allocated by its first chunk
+                        continue
                     totals[inst] = totals.get(inst, 0) + blocks_for(req[rid][0], B)
                     inst_of[rid] = inst
         elif kind == "task_complete":

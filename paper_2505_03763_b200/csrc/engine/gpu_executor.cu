@@ -401,24 +401,42 @@ private:
         return rids;
     }
 
+    // Prompt tokens [begin, end) a prompt task in flight covers for request rid: the whole prompt, or
+    // one chunk of it (policy chunked_prefill).
+    std::pair<int, int> chunk_range(int rid) const {
+        for (const Active& a : active_) {
+            if (a.task.kind != TaskKind::Prompt || a.task.chunk_end.empty()) continue;
+            for (std::size_t i = 0; i < a.task.batch.size(); ++i)
+                if (a.task.batch[i] == rid) return {a.task.chunk_begin[i], a.task.chunk_end[i]};
+        }
+        return {0, entry(rid).req.input_tokens};
+    }
+
     void build_prompt(const std::vector<int>& rids, BatchBuf& B) const {
         const int n = static_cast<int>(rids.size());
         B.slots.resize(n);
         B.ntok.resize(n);
+        B.pos.assign(n, 0);
         B.oidx.assign(n, 0);
+        bool chunked = false;
         for (int i = 0; i < n; ++i) {
             const Entry& e = entry(rids[i]);
+            const auto [b0, b1] = chunk_range(rids[i]);
             B.slots[i] = slot_of_.at(rids[i]);
-            B.ntok[i] = e.req.input_tokens;
-            for (int j = 0; j < e.req.input_tokens; ++j)
-                B.toks.push_back(prompt_token(m_->desc.seed, e.req.id, j, m_->desc.vocab));
+            B.ntok[i] = b1 - b0;
+            B.pos[i] = b0;
+            chunked |= b0 > 0;
+            // only a prompt's last chunk produces its first token
+            B.oidx[i] = b1 == e.req.input_tokens ? 0 : -1;
+            for (int j = b0; j < b1; ++j) B.toks.push_back(prompt_token(m_->desc.seed, e.req.id, j, m_->desc.vocab));
             const std::vector<int>& row = pages_.row(rids[i]);
-            const int need = (e.req.input_tokens + kv_->page_tokens - 1) / kv_->page_tokens;
+            const int need = (b1 + kv_->page_tokens - 1) / kv_->page_tokens;
             for (int j = 0; j < need; ++j) B.prow.push_back(row.at(static_cast<std::size_t>(j)));
         }
         B.b.n = n;
         B.b.slots = B.slots.data();
         B.b.n_tokens = B.ntok.data();
+        B.b.positions = chunked ? B.pos.data() : nullptr;
         B.b.tokens = B.toks.data();
         B.b.page_rows = B.prow.data();
         B.b.out_index = B.oidx.data();
@@ -499,7 +517,8 @@ private:
         std::vector<int> cur;
         int tok = 0;
         for (int rid : rids) {
-            const int n = entry(rid).req.input_tokens;
+            const auto [b0, b1] = chunk_range(rid);  // chunked_prefill tasks: this task's share of the prompt
+            const int n = b1 - b0;
             if (!cur.empty() && (tok + n > cap || cur.size() >= 256)) {
                 J.chunks.push_back(cur);
                 cur.clear();

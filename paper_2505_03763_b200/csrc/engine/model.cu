@@ -212,7 +212,7 @@ void prefill_forward(sw_model* m, sw_kv* kv, const sw_batch& b, cudaStream_t st,
                       yield_tiles);
         for (int r = first; r < last; ++r) {
             tok_off += b.n_tokens[r];
-            page_off += cdiv(b.n_tokens[r], B);
+            page_off += cdiv((b.positions ? b.positions[r] : 0) + b.n_tokens[r], B);
         }
         first = last;
     }
@@ -466,7 +466,10 @@ void prefill_chunk(sw_model* m, sw_kv* kv, const sw_batch& b, int first, int las
         return q;
     };
     int32_t *tokens = take(Tp), *tpos = take(T), *tslot = take(T), *cu = take(S + 1), *sslot = take(NL),
-            *lastrow = take(NL), *oidx = take(NL), *poff = take(S + 1);
+            *lastrow = take(NL), *oidx = take(NL), *poff = take(S + 1), *spos0 = take(S);
+    // chunked prefill: prompt r covers positions [pos0, pos0 + n) of its sequence; its earlier positions are
+    // already in the paged KV cache (keys [0, pos0 + q] for query position pos0 + q)
+    const int32_t* pos0_of = b.positions;
     int n_tiles = 0;
     for (int s = 0; s < S; ++s) n_tiles += cdiv(b.n_tokens[first + s], 64);
     int32_t *tseq = take(n_tiles), *tq0 = take(n_tiles);
@@ -474,20 +477,23 @@ void prefill_chunk(sw_model* m, sw_kv* kv, const sw_batch& b, int first, int las
     for (int s = 0; s < S; ++s) n_tiles128 += cdiv(b.n_tokens[first + s], 128);
     int32_t *tseq128 = take(n_tiles128), *tq0128 = take(n_tiles128);
     int n_pages_total = 0;
-    for (int s = 0; s < S; ++s) n_pages_total += cdiv(b.n_tokens[first + s], B);
+    for (int s = 0; s < S; ++s) n_pages_total += cdiv((pos0_of ? pos0_of[first + s] : 0) + b.n_tokens[first + s], B);
     int32_t* prow = take(n_pages_total);
     int t = 0, ti = 0, ti128 = 0, pg = 0;
     cu[0] = 0;
     poff[0] = 0;
     for (int s = 0; s < S; ++s) {
         const int r = first + s, n = b.n_tokens[r];
+        const int p0 = pos0_of ? pos0_of[r] : 0;
         if (b.slots[r] < 0 || b.slots[r] >= kv->n_slots) throw ContractViolation("prefill: slot out of range");
-        const int np = cdiv(n, B);
+        if (n < 1) throw ContractViolation("prefill: empty prompt");
+        if (p0 < 0 || p0 % 128 != 0) throw ContractViolation("prefill: a prompt chunk must start at a multiple of 128");
+        const int np = cdiv(p0 + n, B);
         if (np > kv->max_pages) throw ContractViolation("prefill: prompt exceeds the slot's page-table row");
         for (int j = 0; j < n; ++j) {
             tokens[t + j] = b.tokens[tok_off + j];
             if (tokens[t + j] < 0 || tokens[t + j] >= d.vocab) throw ContractViolation("prefill: token out of range");
-            tpos[t + j] = j;
+            tpos[t + j] = p0 + j;
             tslot[t + j] = b.slots[r];
         }
         for (int j = 0; j < np; ++j) {
@@ -509,6 +515,7 @@ void prefill_chunk(sw_model* m, sw_kv* kv, const sw_batch& b, int first, int las
         pg += np;
         cu[s + 1] = t;
         poff[s + 1] = pg;
+        spos0[s] = p0;
         sslot[s] = b.slots[r];
         lastrow[s] = t - 1;
         oidx[s] = b.out_index ? b.out_index[r] : 0;
@@ -582,6 +589,9 @@ void prefill_chunk(sw_model* m, sw_kv* kv, const sw_batch& b, int first, int las
     // prefill attention on tcgen05 (SW_PREFILL_TC=0: the mma.sync kernel)
     static const int tc_env = env_int("SW_PREFILL_TC", 1);
     const bool use_tc = tc_env && kv->tm_kv_ok && (d.n_heads / d.n_kv_heads) % 2 == 0;  // head pairs share a kv head
+    bool chunked = false;
+    for (int s = 0; s < S && pos0_of; ++s) chunked |= pos0_of[first + s] > 0;
+    if (chunked && !use_tc) throw ConfigError("prefill: prompt chunks past position 0 need the tcgen05 attention");
     // RoPE + KV write fused into the QKV GEMM epilogue (SW_PREFILL_ROPE_FUSED=0: separate rope_kv pass)
     static const int fuse_env = env_int("SW_PREFILL_ROPE_FUSED", 1);
     const bool fuse_rope = fuse_env != 0;
@@ -597,6 +607,7 @@ void prefill_chunk(sw_model* m, sw_kv* kv, const sw_batch& b, int first, int las
         ta.tile_seq = dev(tseq128);
         ta.tile_q0 = dev(tq0128);
         ta.cu_seqlens = dev(cu);
+        ta.seq_pos0 = dev(spos0);
         ta.seq_slot = dev(sslot);
         ta.page_table = kv->page_table;
         ta.max_pages = kv->max_pages;

@@ -166,6 +166,8 @@ protected:
         Request req;
         int generated = 0;
         long long footprint = 0;
+        int prefilled = 0;          // prompt tokens in the KV cache (chunked prefill)
+        bool chunk_active = false;  // a prompt task holding this request is in flight
     };
 
     Entry& entry(int id) {
@@ -204,7 +206,8 @@ protected:
     bool fits(const TaskRequest& tr) const {
         if (!in_.shared_kv_pool || tr.kind != TaskKind::Prompt) return true;
         long long need = 0;
-        for (int rid : tr.batch) need += entry(rid).footprint;
+        for (int rid : tr.batch)
+            if (entry(rid).req.state == RequestState::Waiting) need += entry(rid).footprint;
         return reserved_blocks(tr.instance_id) + need <= pools_.at(static_cast<std::size_t>(tr.instance_id)).capacity();
     }
     // The next pass's tasks: deferred prompts that fit now (in order), then the
@@ -237,19 +240,37 @@ protected:
             throw ContractViolation("scheduler: task for unknown instance");
         const auto inst = static_cast<std::size_t>(tr.instance_id);
         std::vector<Request> prompt_batch;
+        std::vector<int> chunk_begin;
+        const bool chunked = tr.kind == TaskKind::Prompt && !tr.chunk_end.empty();
         if (tr.kind == TaskKind::Prompt) {
+            if (chunked && tr.chunk_end.size() != tr.batch.size())
+                throw ContractViolation("scheduler: prompt chunk ends do not match the batch");
             long long need = 0;
-            for (int rid : tr.batch) {
-                const Entry& e = entry(rid);
-                if (e.req.state != RequestState::Waiting)
+            for (std::size_t i = 0; i < tr.batch.size(); ++i) {
+                const Entry& e = entry(tr.batch[i]);
+                // a chunk continues a request whose earlier chunks completed (Prompting, none in flight)
+                const bool cont = chunked && e.req.state == RequestState::Prompting && e.prefilled > 0 && !e.chunk_active;
+                if (e.req.state != RequestState::Waiting && !cont)
                     throw ContractViolation("scheduler: prompt for request not waiting");
-                prompt_batch.push_back(e.req);
-                need += e.footprint;
+                Request r = e.req;  // priced by the tokens this task prefills
+                if (chunked) {
+                    const int end = tr.chunk_end[i];
+                    if (end <= e.prefilled || end > e.req.input_tokens)
+                        throw ContractViolation("scheduler: prompt chunk out of range");
+                    if (end < e.req.input_tokens && end % kChunkAlign != 0)
+                        throw ContractViolation("scheduler: a split prompt chunk must end on a multiple of 128 tokens");
+                    r.input_tokens = end - e.prefilled;
+                    chunk_begin.push_back(e.prefilled);
+                }
+                prompt_batch.push_back(r);
+                if (e.req.state == RequestState::Waiting) need += e.footprint;
             }
             if (reserved_blocks(static_cast<int>(inst)) + need > pools_[inst].capacity())
                 throw ContractViolation("scheduler: prompt batch exceeds KV reservation capacity");
             for (int rid : tr.batch) {
                 Entry& e = entry(rid);
+                e.chunk_active = true;
+                if (e.req.state != RequestState::Waiting) continue;
                 e.req.state = RequestState::Prompting;
                 reserved_[inst] += e.footprint;
                 if (pools_[inst].alloc(rid, e.req.input_tokens) != KvBlockPool::AllocResult::Ok)
@@ -268,6 +289,10 @@ protected:
         }
         Active a;
         a.task = price(tr, prompt_batch);
+        if (chunked) {
+            a.task.chunk_begin = std::move(chunk_begin);
+            a.task.chunk_end = tr.chunk_end;
+        }
         a.seq = next_seq();
         a.id = task_counter_++;
         LogRecord r;
@@ -296,11 +321,13 @@ protected:
         r.task_id = done.id;
         append(r, at);
         if (done.task.kind == TaskKind::Prompt) {
-            for (int rid : done.task.batch) {
-                Entry& e = entry(rid);
+            for (std::size_t i = 0; i < done.task.batch.size(); ++i) {
+                Entry& e = entry(done.task.batch[i]);
                 if (e.req.state != RequestState::Prompting)
                     throw ContractViolation("engine: prompt completion for request not prompting");
-                e.req.state = RequestState::Generating;
+                e.chunk_active = false;
+                e.prefilled = done.task.chunk_end.empty() ? e.req.input_tokens : done.task.chunk_end[i];
+                if (e.prefilled == e.req.input_tokens) e.req.state = RequestState::Generating;
             }
         } else {
             for (int rid : done.task.batch) {
@@ -390,7 +417,8 @@ protected:
     long long pending_reserve_ = 0;     // shared KV quota: footprints accepted in the current pass
     void reserve_pending(const TaskRequest& tr) {
         if (!in_.shared_kv_pool || tr.kind != TaskKind::Prompt) return;
-        for (int rid : tr.batch) pending_reserve_ += entry(rid).footprint;
+        for (int rid : tr.batch)
+            if (entry(rid).req.state == RequestState::Waiting) pending_reserve_ += entry(rid).footprint;
     }
     std::vector<int> n_prompt_, n_step_;
     std::vector<Active> active_;

@@ -53,7 +53,8 @@ inline PolicyKind parse_policy(const std::string& s, const std::string& where) {
         {"pipelined_splitwiser", PolicyKind::PipelinedSplitwiser},
         {"continuous_batching", PolicyKind::ContinuousBatching},
         {"mixed_batching", PolicyKind::MixedBatching},
-        {"multi_instance", PolicyKind::MultiInstance}};
+        {"multi_instance", PolicyKind::MultiInstance},
+        {"chunked_prefill", PolicyKind::ChunkedPrefill}};
     for (const auto& [n, k] : kNames)
         if (s == n) return k;
     throw ConfigError(where + ": unknown policy '" + s + "'");
@@ -134,6 +135,10 @@ inline RunSpec build_spec(const SpecMap& m) {
         else if (k == "max_batch") s.scheduler.max_batch = static_cast<int>(integer(k, v));
         else if (k == "P") s.scheduler.splitwiser_processes = static_cast<int>(integer(k, v));
         else if (k == "n_instances") s.scheduler.n_instances = static_cast<int>(integer(k, v));
+        else if (k == "chunk_tokens") s.scheduler.chunk_tokens = static_cast<int>(integer(k, v));
+        else if (k == "tbt_target_ms") s.scheduler.tbt_target_s = num(k, v) * 1e-3;
+        else if (k == "chunk_min") s.scheduler.chunk_min = static_cast<int>(integer(k, v));
+        else if (k == "chunk_max") s.scheduler.chunk_max = static_cast<int>(integer(k, v));
         else if (k == "mode") {
             if (v == "exclusive") s.inputs.discipline.mode = SharingDiscipline::Mode::Exclusive;
             else if (v == "mps_concurrent") s.inputs.discipline.mode = SharingDiscipline::Mode::MpsConcurrent;

@@ -73,6 +73,10 @@ struct PhaseTask {
     double mem_demand = 0.0;
     double duration_alone_s = 0.0;
     int instance_id = 0;
+    // Chunked prefill (new): a prompt task may cover prompt
+    // tokens [chunk_begin[i], chunk_end[i]) of batch[i] instead of whole
+    // prompts.  Empty = whole prompts (the reference's only form).
+    std::vector<int> chunk_begin, chunk_end;
 };
 
 inline double roofline_duration(double compute, double mem, const GpuSpec& g, double overhead_s) {

@@ -52,6 +52,7 @@ struct PrefillTcArgs {
     const int32_t* tile_seq;   // device [tiles]
     const int32_t* tile_q0;    // device [tiles]
     const int32_t* cu_seqlens; // device [seqs + 1]
+    const int32_t* seq_pos0;   // device [seqs]: first position of each prompt chunk (multiple of 128), or null
     const int32_t* seq_slot;   // device [seqs]
     const int32_t* page_table; // device [slots][max_pages]
     int max_pages;

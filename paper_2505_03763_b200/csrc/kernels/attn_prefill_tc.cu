@@ -122,7 +122,7 @@ struct TcCfg {
 
 // Work item k of CTA bx (both producer and consumers walk the same sequence).
 struct Item {
-    int tile, pair, start, len, q0, nblk, npages;
+    int tile, pair, start, len, q0, nblk, npages, pos0;
     const int32_t* ptab;
 };
 __device__ __forceinline__ bool next_item(const PrefillTcArgs& a, int k, Item& x) {
@@ -138,9 +138,12 @@ __device__ __forceinline__ bool next_item(const PrefillTcArgs& a, int k, Item& x
     x.q0 = a.tile_q0[x.tile];
     x.start = a.cu_seqlens[sq];
     x.len = a.cu_seqlens[sq + 1] - x.start;
-    const int kend = min(x.q0 + kRows, x.len);  // keys this tile attends to: [0, kend)
+    // a prompt chunk at positions [pos0, pos0 + len) attends to the cached prefix too; pos0 is a multiple
+    // of 128, so the key blocks are aligned exactly as for a whole prompt and the last one is the diagonal
+    x.pos0 = a.seq_pos0 ? a.seq_pos0[sq] : 0;
+    const int kend = x.pos0 + min(x.q0 + kRows, x.len);  // keys this tile attends to: [0, kend)
     x.nblk = (kend + kBlk - 1) / kBlk;
-    x.npages = (x.len + kPg - 1) / kPg;
+    x.npages = (x.pos0 + x.len + kPg - 1) / kPg;
     x.ptab = a.page_table + static_cast<long long>(a.seq_slot[sq]) * a.max_pages;
     return true;
 }
@@ -325,7 +328,8 @@ __global__ void __launch_bounds__(384, 1) attn_prefill_tc_kernel(const __grid_co
         Item x{};
         for (int k = 0; next_item(a, k, x); ++k) {
             const int h = 2 * x.pair + g;
-            const int qp = x.q0 + row;  // this row's position in the prompt
+            const int qr = x.q0 + row;    // this row in the prompt chunk
+            const int qp = x.pos0 + qr;   // its position in the sequence
             float m_use = -INFINITY, l_run = 0.f;
             for (int j = 0; j < x.nblk; ++j) {
                 mbar_wait(&s_full[g], (gb + j) & 1);
@@ -335,7 +339,7 @@ __global__ void __launch_bounds__(384, 1) attn_prefill_tc_kernel(const __grid_co
                 for (int c = 0; c < 4; ++c) tmem_ld32(tS + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32 * c]));
                 tmem_ld_wait();
                 // the diagonal / prompt-end block (the last): keys [kbase, kbase + nvalid) are valid
-                const int nvalid = j + 1 == x.nblk ? min(kBlk, min(qp + 1, x.len) - j * kBlk) : kBlk;
+                const int nvalid = j + 1 == x.nblk ? min(kBlk, min(qp + 1, x.pos0 + x.len) - j * kBlk) : kBlk;
                 float mx0 = -INFINITY, mx1 = -INFINITY;
 #pragma unroll
                 for (int i = 0; i < 128; i += 2) {
@@ -385,13 +389,13 @@ __global__ void __launch_bounds__(384, 1) attn_prefill_tc_kernel(const __grid_co
             mbar_wait(&o_done[g], it & 1);
             tc_fence_after();
             const float inv = 1.f / l_run;
-            __nv_bfloat16* dst = out + (static_cast<long long>(x.start) + qp) * a.H * HD + static_cast<long long>(h) * HD;
+            __nv_bfloat16* dst = out + (static_cast<long long>(x.start) + qr) * a.H * HD + static_cast<long long>(h) * HD;
 #pragma unroll
             for (int c = 0; c < HD / 32; ++c) {
                 uint32_t o[32];
                 tmem_ld32(tO + c * 32, o);
                 tmem_ld_wait();
-                if (qp < x.len) {
+                if (qr < x.len) {
 #pragma unroll
                     for (int v = 0; v < 4; ++v)
                         *reinterpret_cast<uint4*>(dst + c * 32 + v * 8) =

@@ -63,16 +63,22 @@ class Engine:
         return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 
     def prefill(self, slots: Sequence[int], prompts: Sequence[np.ndarray], page_rows: Sequence[Sequence[int]],
-                out_index: Optional[Sequence[int]] = None, logits: bool = True):
+                out_index: Optional[Sequence[int]] = None, logits: bool = True,
+                positions: Optional[Sequence[int]] = None):
+        """Prefill prompts (or prompt chunks: `positions` = each chunk's first position, a multiple of
+        128, with the earlier positions already in the slot's pages; page_rows then cover [0, pos + len))."""
         import torch
 
         n = len(slots)
         out = torch.empty((n, self.desc.vocab), dtype=torch.float32, device="cuda") if logits else None
         toks = np.concatenate([np.asarray(p, dtype=np.int64) for p in prompts])
         keep = [_i32(slots), _i32([len(p) for p in prompts]), _i32(toks), _i32([x for r in page_rows for x in r]),
-                _i32(out_index if out_index is not None else [0] * n)]
+                _i32(out_index if out_index is not None else [0] * n),
+                _i32(positions) if positions is not None else None]
         b = Batch(n=n, slots=keep[0], n_tokens=keep[1], tokens=keep[2], page_rows=keep[3], out_index=keep[4],
                   logits_out=out.data_ptr() if out is not None else None)
+        if keep[5] is not None:
+            b.positions = keep[5]
         check(lib().sw_prefill_enqueue(self.model, self.kv, ctypes.byref(b), self._stream()))
         torch.cuda.synchronize()
         return out.cpu().numpy() if out is not None else None

@@ -369,3 +369,60 @@ def test_attention_geometries_prefill_and_decode(shape, flat):
     print(f"\n{shape} flat={flat}: prefill/decode vs fp32 {errs[0]:.4f}/{errs[1]:.4f}, vs emulated "
           f"{errs[2]:.4f}/{errs[3]:.4f}")
     assert max(errs) <= LOGIT_RTOL, errs
+
+
+@pytest.mark.parametrize("shape", ["TINY", "LLAMA_1B_2L", "LLAMA_8B_1L"])
+def test_chunked_prefill_bit_identical_to_whole_prompts(shape):
+    """Chunked prefill (policy chunked_prefill): prompts run as
+    128-aligned chunks whose attention reads the earlier chunks' K/V from the
+    paged cache.  Every per-row computation is the same as in one whole-prompt
+    launch (GEMM rows are independent, the attention walks the same key blocks
+    in the same order), so the last-chunk logits are bit-identical to the
+    whole-prompt prefill's; both are held to the oracle, and decode steps
+    teacher-forced over the chunk-written cache are checked too."""
+    if shape == "TINY":
+        d = M.TINY
+    elif shape == "LLAMA_1B_2L":
+        d = dataclasses.replace(M.LLAMA_1B, n_layers=2)
+    else:
+        d = dataclasses.replace(M.LLAMA_8B, n_layers=1, vocab=4096)
+    per = 72
+    eng = _engine(d, per, n_slots=8)
+    try:
+        o = M.OracleModel(d)
+        lens = [700, 1030, 130]
+        rows_a = [[i * per + j for j in range(per)] for i in range(3)]
+        rows_b = [[(i + 3) * per + j for j in range(per)] for i in range(3)]
+        prompts = [M.prompt_tokens(d.seed, 900 + i, L, d.vocab) for i, L in enumerate(lens)]
+        whole = eng.prefill([0, 1, 2], prompts, [r[:(L + 15) // 16] for r, L in zip(rows_a, lens)])
+        # chunks: [0, 256) | [256, 640) | [640, end) -- ragged last chunks, one prompt done after its first
+        cuts = [0, 256, 640]
+        last = [None] * 3
+        for c, c0 in enumerate(cuts):
+            c1 = cuts[c + 1] if c + 1 < len(cuts) else 1 << 30
+            idx = [i for i, L in enumerate(lens) if L > c0]
+            seg = [prompts[i][c0:min(c1, lens[i])] for i in idx]
+            ends = [min(c1, lens[i]) for i in idx]
+            lg = eng.prefill([3 + i for i in idx], seg, [rows_b[i][:(e + 15) // 16] for i, e in zip(idx, ends)],
+                             out_index=[0 if e == lens[i] else -1 for i, e in zip(idx, ends)],
+                             positions=[c0] * len(idx))
+            for k, i in enumerate(idx):
+                if ends[k] == lens[i]:
+                    last[i] = lg[k]
+        chunked = np.stack(last)
+        assert np.array_equal(chunked, whole), np.abs(chunked - whole).max()
+        ref = o.prefill(prompts, rows_b)
+        bars = Bars(f"{shape} chunked prefill")
+        bars.add(chunked, ref)
+        toks = [int(np.argmax(r)) for r in ref]
+        pos = list(lens)
+        for _ in range(3):
+            newp = [rows_b[i][pos[i] // 16] if pos[i] % 16 == 0 else -1 for i in range(3)]
+            lg = eng.decode([3, 4, 5], pos, tokens=toks, new_page=newp)
+            r = o.decode(toks, pos, rows_b)
+            bars.add(lg, r)
+            toks = [int(np.argmax(x)) for x in r]
+            pos = [p + 1 for p in pos]
+        bars.check()
+    finally:
+        eng.close()

@@ -74,6 +74,28 @@ def make_case(seed: int) -> str:
             f"arrival={arrival};{policy};kv_capacity_blocks={cap};{mode}")
 
 
+N_CHUNKED = 8
+
+
+def make_chunked_case(seed: int) -> str:
+    """Chunked prefill (policy chunked_prefill): prompts long enough to be
+    split at 128-token boundaries, fixed or adaptive budgets, fused or separate launches."""
+    rng = random.Random(seed)
+    n = rng.randint(2, 8)
+    in_lo = rng.randint(60, 180)
+    in_hi = in_lo + rng.randint(0, 50)
+    out_lo = rng.randint(1, 10)
+    out_hi = out_lo + rng.randint(0, 6)
+    arrival = rng.choice(["zero", "poisson:200", "poisson:2000"])
+    budget = rng.choice(["chunk_tokens=128", "chunk_tokens=256", "chunk_tokens=384",
+                         "chunk_tokens=0;tbt_target_ms=0.5;chunk_max=512"])
+    mode = rng.choice(["engine.split=1;engine.fuse=1", "engine.split=0", "engine.split=1"])
+    cap = min(N_PAGES, P.blocks_for(in_hi + out_hi) + rng.randint(0, 60))
+    return (f"n={n};input={in_lo}..{in_hi};output={out_lo}..{out_hi};seed={rng.randint(1, 1 << 30)};"
+            f"arrival={arrival};policy=chunked_prefill;{budget};max_batch={rng.randint(0, 4)};"
+            f"kv_capacity_blocks={cap};{mode}")
+
+
 @pytest.fixture(scope="module")
 def runs():
     from paper_2505_03763_b200 import runtime
@@ -84,6 +106,9 @@ def runs():
     try:
         for i in range(N_CASES):
             spec = make_case(1000 + i)
+            out.append((spec, eng.run(spec)))
+        for i in range(N_CHUNKED):
+            spec = make_chunked_case(5000 + i)
             out.append((spec, eng.run(spec)))
     finally:
         eng.close()
