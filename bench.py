@@ -44,7 +44,10 @@ WORKLOADS = {
                     max_prefill=32768, max_decode=256,
                     split="policy=mixed_batching;max_batch=256;engine.split=1;engine.prefill_priority=1",
                     serial="policy=continuous_batching;max_batch=256;engine.split=0",
-                    best_serial=None),
+                    best_serial=None,
+                    # chunked prefill, 8192-token chunks fused with the token step
+                    # (profiles/r02s4/cfg3_chunked_sweep.txt: the best throughput of the budgets swept)
+                    chunked="policy=chunked_prefill;max_batch=256;chunk_tokens=8192;engine.split=1;engine.fuse=1"),
     # configs[1] of BASELINE.json
     # split = PipelinedSplitwiser P=2 on concurrent streams (token steps of the two lanes aligned and merged);
     # serial = the SAME task stream under the one-task gate; best_serial = the fastest
@@ -408,6 +411,7 @@ def main():
     split_spec = spec_for(w, args.split or w["split"], rank, world)
     serial_spec = spec_for(w, args.serial or w["serial"], rank, world)
     best_spec = spec_for(w, w["best_serial"], rank, world) if w["best_serial"] else None
+    chunk_spec = spec_for(w, w["chunked"], rank, world) if w.get("chunked") else None
 
     for _ in range(args.warmup):
         eng.run(split_spec)
@@ -415,6 +419,8 @@ def main():
         eng.run(serial_spec)
         if best_spec:
             eng.run(best_spec)
+        if chunk_spec:
+            eng.run(chunk_spec)
 
     def timed(spec):
         if dist:
@@ -428,10 +434,12 @@ def main():
         split_raw = timed(split_spec)
     serial_raw = timed(serial_spec)
     best_raw = timed(best_spec) if best_spec else None
+    chunk_raw = timed(chunk_spec) if chunk_spec else None
     dev = "cuda" if dist else None
     split = fold_runs(split_raw, dist, world, dev, n_local, w["output"] + 1)
     serial = fold_runs(serial_raw, dist, world, dev, n_local, w["output"] + 1)
     best = fold_runs(best_raw, dist, world, dev, n_local, w["output"] + 1) if best_raw else serial
+    chunked = fold_runs(chunk_raw, dist, world, dev, n_local, w["output"] + 1) if chunk_raw else None
 
     roof = roofline_decode_gemm(eng, desc, w["max_decode"], peaks) if rank == 0 else None
     roof_prefill = roofline_prefill_gemm(eng, desc, 4096, peaks) if rank == 0 else None
@@ -500,6 +508,10 @@ def main():
         "split_over_serial": round(value / serial_v, 4),
         "best_serial": {"tokens_per_s": round(best_v, 1), "p50_ttft_s": best["p50_ttft"], "p50_tbt_s": best["p50_tbt"]},
         "split_over_best_serial": round(value / best_v, 4),
+        "chunked": ({"policy": w["chunked"], "tokens_per_s": round(chunked["tokens"] / chunked["makespan"], 1),
+                     "p50_ttft_s": chunked["p50_ttft"], "p50_tbt_s": chunked["p50_tbt"], "p99_tbt_s": chunked["p99_tbt"],
+                     "over_best_serial": round(chunked["tokens"] / chunked["makespan"] / best_v, 4)}
+                    if chunked else None),
         "roofline_run": {"split": whole_run_roofline(split, peaks), "serial": whole_run_roofline(serial, peaks)},
         "roofline_decode_step": step,
         "e2e": {"value": round(split["tokens"] / split["wall"], 1), "unit": "tokens/s",
