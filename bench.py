@@ -212,7 +212,10 @@ def roofline_decode_gemm(eng, desc, rows: int, peaks, reps: int = 20):
     nbytes = 2 * F * d * 2 + rows * d * 2 + rows * F * 2
     achieved = nbytes / t / 1e9
     peak = float(peaks["hbm_gbs"])
-    return {"kernel": "gemm_decode_kernel<BN,SWIGLU> (decode gate/up, cluster split-K, rows=%d)" % rows, "bound": "hbm",
+    form = ("gemm_dsk_kernel<256,SWIGLU> (decode gate/up: whole tiles per SM + stream-K remainder, rows=%d)" % rows
+            if rows > 128 and 2 * F // 128 > torch.cuda.get_device_properties(0).multi_processor_count else
+            "gemm_decode_kernel<BN,SWIGLU> (decode gate/up, cluster split-K, rows=%d)" % rows)
+    return {"kernel": form, "bound": "hbm",
             "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
             "bytes_per_launch": nbytes, "us_per_launch": round(t * 1e6, 2)}
 

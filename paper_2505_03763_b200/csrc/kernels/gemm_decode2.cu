@@ -169,6 +169,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (threadIdx.x == 0) DSK_STAMP(0);
     Piece pcs[kMaxPieces];
     const int npcs = piece_list(pl, c, pcs);
+    // Split tail: the last piece is a whole tile (its epilogue is the only work left after the last MMA),
+    // so warps 0-3 -- idle by then -- emit its tokens [128, n) while warps 4-7 emit [0, 128).
+    const bool split_tail = BN > 128 && npcs > 0 && pcs[npcs - 1].np == 1;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < NW; ++s) {
@@ -272,6 +275,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int n_live = args.live_tokens ? min(args.valid_tokens, *args.live_tokens) : args.valid_tokens;
         fill_tok_tables<MODE>(args, n_live, e, 128, tok_inv, tok_pos, tok_kv);
         asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (split_tail) asm volatile("bar.arrive 4, 256;" ::: "memory");  // token tables, TMEM base -> warps 0-3
         const uint32_t tb = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
         int buf = 0, nred = 0;
         unsigned* done = args.counters + pl.T;
@@ -283,15 +287,17 @@ __global__ void __launch_bounds__(kThreads, 1)
             uint32_t r[32];
             const TokCtx tc{&args, tok_inv, tok_pos, tok_kv, p.tile * BM};
             if (p.np == 1) {
-                // whole tile: TMEM (thread = feature) -> smem token-major -> one warp per token
-                for (int c0 = 0; c0 < n_live; c0 += 32, buf ^= 1) {
+                // whole tile: TMEM (thread = feature) -> smem token-major -> one warp per token; the last
+                // whole tile's tokens >= 128 go to warps 0-3 (split tail)
+                const int c_end = split_tail && q + 1 == npcs ? min(n_live, 128) : n_live;
+                for (int c0 = 0; c0 < c_end; c0 += 32, buf ^= 1) {
                     tmem_ld32(tb + ab * BN + c0, r);
                     tmem_ld_wait();
                     float* T = xt + buf * 32 * kTs;
 #pragma unroll
                     for (int j = 0; j < 32; ++j) T[j * kTs + row] = __uint_as_float(r[j]);
                     asm volatile("bar.sync 1, 128;" ::: "memory");
-                    const int cnt = min(32, n_live - c0);
+                    const int cnt = min(32, c_end - c0);
                     for (int j = ew; j < cnt; j += 4)
                         emit_tok<MODE>(tc, c0 + j, lane, *reinterpret_cast<const float4*>(T + j * kTs + 4 * lane),
                                        pre_tok<MODE>(tc, c0 + j, lane));
@@ -380,6 +386,36 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
                 ++nred;
             }
+        }
+    }
+    if (split_tail && warp < kEpiWarp0) {
+        // ------------------------------------------------------------ split tail (warps 0-3)
+        asm volatile("bar.sync 4, 256;" ::: "memory");  // token tables filled, TMEM base published
+        griddep_wait();
+        const int n_live = args.live_tokens ? min(args.valid_tokens, *args.live_tokens) : args.valid_tokens;
+        if (n_live > 128) {
+            const int q = npcs - 1, ab = q & 1;
+            mbar_wait(&acc_full[ab], (q >> 1) & 1);  // the last MMA retired: the weight ring is free
+            tc_fence_after();
+            const uint32_t tb = *tmem_slot + (static_cast<uint32_t>(warp * 32) << 16) + ab * BN;
+            const int row = warp * 32 + lane;
+            float* xb = reinterpret_cast<float*>(sW);  // two 32-token transpose buffers in the drained ring
+            const TokCtx tc{&args, tok_inv, tok_pos, tok_kv, pcs[q].tile * BM};
+            int buf = 0;
+            for (int c0 = 128; c0 < n_live; c0 += 32, buf ^= 1) {
+                uint32_t r[32];
+                tmem_ld32(tb + c0, r);
+                tmem_ld_wait();
+                float* T = xb + buf * 32 * kTs;
+#pragma unroll
+                for (int j = 0; j < 32; ++j) T[j * kTs + row] = __uint_as_float(r[j]);
+                asm volatile("bar.sync 3, 128;" ::: "memory");
+                const int cnt = min(32, n_live - c0);
+                for (int j = warp; j < cnt; j += 4)
+                    emit_tok<MODE>(tc, c0 + j, lane, *reinterpret_cast<const float4*>(T + j * kTs + 4 * lane),
+                                   pre_tok<MODE>(tc, c0 + j, lane));
+            }
+            tc_fence_before();
         }
     }
     __syncthreads();
