@@ -104,8 +104,11 @@ def config_to_spec(cfg: dict) -> str:
         if k in c:
             kv[sk] = _num(c[k])
     s = cfg.get("scheduler", {})
-    _expect(s, "scheduler", {"policy", "max_batch", "P", "n_instances", "inner"})
-    for k in ("policy", "max_batch", "P", "n_instances", "inner"):
+    # chunk_tokens / tbt_target_ms / chunk_min / chunk_max: policy "chunked_prefill" (new)
+    sched_keys = ("policy", "max_batch", "P", "n_instances", "inner", "chunk_tokens", "tbt_target_ms", "chunk_min",
+                  "chunk_max")
+    _expect(s, "scheduler", set(sched_keys))
+    for k in sched_keys:
         if k in s:
             kv[k] = str(s[k])
     d = cfg.get("discipline", {})

@@ -275,7 +275,7 @@ int main() {
         const EventLog log = run_split_engine(in, sched, m, kv, opt, &o);
         check_run(log, reqs, o, tokens, split ? "scripted, 2 instances, split" : "scripted, 2 instances, serial");
     }
-    for (const char* pol : {"mixed", "pipelined", "sequential"}) {
+    for (const char* pol : {"mixed", "pipelined", "sequential", "chunked"}) {
         for (bool split : {true, false}) {
             SchedulerConfig cfg;
             int instances = 1;
@@ -287,6 +287,10 @@ int main() {
                 cfg.splitwiser_processes = 2;
                 cfg.max_batch = 2;
                 instances = 2;
+            } else if (std::string(pol) == "chunked") {  // 128-token prompt chunks
+                cfg.policy = PolicyKind::ChunkedPrefill;
+                cfg.chunk_tokens = 128;
+                cfg.max_batch = 4;
             } else {
                 cfg.policy = PolicyKind::Sequential;
                 cfg.max_batch = 3;
@@ -296,6 +300,7 @@ int main() {
             if (instances > 1) in.discipline.mode = SharingDiscipline::Mode::MpsConcurrent;
             GpuOptions opt;
             opt.split = split;
+            opt.fuse = split && std::string(pol) == "chunked";  // chunk + token step in one launch
             RunOutputs o;
             const EventLog log = run_split_engine(in, sched, m, kv, opt, &o);
             const std::string what = std::string("PolicyScheduler ") + pol + (split ? ", split" : ", serial");

@@ -179,3 +179,21 @@ def test_gpu_backend_sweep_grows_the_engine(tmp_path):
     code, out = _run(tmp_path, cfg, "--backend", "gpu", "--model", "TINY")
     assert code == 0
     assert json.loads(_read(out, "report.json"))["total_output_tokens"] == 16
+
+
+def test_chunked_prefill_config_and_replay(tmp_path, capsys):
+    """The new chunked_prefill policy through the JSON front end, a --set sweep of its
+    budget, and replay of the written event log to the same report."""
+    cfg = dict(INLINE, scheduler={"policy": "chunked_prefill", "max_batch": 8, "chunk_tokens": 256})
+    code, out = _run(tmp_path, cfg, "--set", "scheduler.chunk_tokens=128")
+    assert code == 0
+    line = capsys.readouterr().out.strip()
+    assert cli.main(["replay", str(out / "events.csv")]) == 0
+    assert capsys.readouterr().out.strip() == line
+    assert _read(out, "replay_report.json") == _read(out, "report.json")
+    cfg["scheduler"] = {"policy": "chunked_prefill", "chunk_tokens": 0, "tbt_target_ms": 5.0}
+    code, _ = _run(tmp_path, cfg)
+    assert code == 0
+    cfg["scheduler"] = {"policy": "chunked_prefill", "chunk_tokens": 100}
+    code, _ = _run(tmp_path, cfg)
+    assert code == 2  # ConfigError
