@@ -300,7 +300,6 @@ int main() {
             if (instances > 1) in.discipline.mode = SharingDiscipline::Mode::MpsConcurrent;
             GpuOptions opt;
             opt.split = split;
-            opt.fuse = split && std::string(pol) == "chunked";  // chunk + token step in one launch
             RunOutputs o;
             const EventLog log = run_split_engine(in, sched, m, kv, opt, &o);
             const std::string what = std::string("PolicyScheduler ") + pol + (split ? ", split" : ", serial");
