@@ -403,7 +403,75 @@ protected:
         sorted.reserve(order.size());
         for (std::size_t i : order) sorted.push_back(log_.records[i]);
         log_.records.swap(sorted);
+        rederive_kv_records();
         return delta;
+    }
+
+    // Device-clock backends: the kv records of the time-ordered log, derived with the engine's own
+    // ledger rules (engine.hpp:284-387: a prompt allocates blocks_for(in) at its start, a token step
+    // grows each request to blocks_for(in + g) or frees it at its last token; one record per change,
+    // after the task's records).  The host ledger takes the same steps in host order, which can
+    // differ from device order: a prompt queued behind an in-flight launch is accepted (allocated)
+    // before that launch's completion is polled, but starts on the device after it.  The host
+    // pool's end state is checked against the derived one.
+    void rederive_kv_records() {
+        std::vector<LogRecord> out;
+        out.reserve(log_.records.size());
+        std::vector<long long> total(pools_.size(), 0), logged(pools_.size(), 0);
+        std::map<int, std::pair<TaskKind, int>> task;  // id -> (kind, batch id)
+        std::map<int, int> gen;
+        std::map<int, bool> alloc;
+        int pending = -1;  // instance whose record follows the current task's records
+        auto flush = [&]() {
+            if (pending < 0) return;
+            const auto i = static_cast<std::size_t>(pending);
+            if (total[i] != logged[i]) {
+                LogRecord k;
+                k.kind = LogKind::Kv;
+                k.instance = pending;
+                k.kv_blocks = total[i];
+                k.time_s = out.back().time_s;
+                out.push_back(k);
+                logged[i] = total[i];
+            }
+            pending = -1;
+        };
+        for (const LogRecord& r : log_.records) {
+            if (r.kind == LogKind::Kv) continue;
+            if (r.kind != LogKind::RequestFinish) flush();
+            out.push_back(r);
+            if (r.kind == LogKind::TaskStart) {
+                task[r.task_id] = {r.task_kind, r.batch_id};
+                if (r.task_kind != TaskKind::Prompt) continue;
+                for (int rid : log_.batches.at(static_cast<std::size_t>(r.batch_id))) {
+                    if (alloc[rid]) continue;  // a later chunk of a chunked prompt
+                    alloc[rid] = true;
+                    total.at(static_cast<std::size_t>(r.instance)) += pools_[0].blocks_for(entry(rid).req.input_tokens);
+                }
+                pending = r.instance;
+            } else if (r.kind == LogKind::TaskComplete) {
+                const auto& [kind, batch] = task.at(r.task_id);
+                if (kind != TaskKind::TokenStep) continue;
+                int inst = -1;
+                for (int rid : log_.batches.at(static_cast<std::size_t>(batch))) {
+                    const Entry& e = entry(rid);
+                    inst = sched_.instance_of(rid);
+                    const long long in = e.req.input_tokens;
+                    const int g = ++gen[rid];
+                    auto& t = total.at(static_cast<std::size_t>(inst));
+                    if (g == e.req.output_tokens)
+                        t -= pools_[0].blocks_for(in + g - 1);
+                    else
+                        t += pools_[0].blocks_for(in + g) - pools_[0].blocks_for(in + g - 1);
+                }
+                pending = inst;
+            }
+        }
+        flush();
+        log_.records.swap(out);
+        for (std::size_t i = 0; i < pools_.size(); ++i)
+            if (total[i] != pools_[i].total_allocated())
+                throw ContractViolation("engine: device-ordered KV ledger disagrees with the host ledger");
     }
 
     SimulationInputs in_;
