@@ -562,12 +562,14 @@ void prefill_chunk(sw_model* m, sw_kv* kv, const sw_batch& b, int first, int las
         ring_release(m->mix_ring, dm_idx, st);
     }
 
-    install_pages_kernel<<<S, 64, 0, st>>>(dev(prow), dev(poff), dev(sslot), kv->page_table, kv->max_pages);
-    SW_LAUNCH_CHECK();
+    if (S > 0) {
+        install_pages_kernel<<<S, 64, 0, st>>>(dev(prow), dev(poff), dev(sslot), kv->page_table, kv->max_pages);
+        SW_LAUNCH_CHECK();
+    }
     // ---- layers
     const int qkv_w = (d.n_heads + 2 * d.n_kv_heads) * d.head_dim;
     const int hdH = d.n_heads * d.head_dim;
-    embed_tokens(dev(tokens), w.pmeta, Tp, m->emb, w.x, d.d_model, st);
+    if (Tp > 0) embed_tokens(dev(tokens), w.pmeta, Tp, m->emb, w.x, d.d_model, st);
     if (D > 0)  // decode rows: the slot's last token (device resident), new pages installed first
         embed(mw.meta, D, m->emb, m->layers[0].g_attn, w.x + static_cast<size_t>(Tp) * d.d_model,
               w.xn + static_cast<size_t>(Tp) * d.d_model, mw.ss, d.d_model, kv->last_token, kv->page_table,
@@ -656,7 +658,9 @@ void prefill_chunk(sw_model* m, sw_kv* kv, const sw_batch& b, int first, int las
             rope_kv(w.qkv, w.q, kvl, dev(tpos), dev(tslot), kv->page_table, m->rope_cs, T, nullptr, d.n_heads,
                     d.n_kv_heads, d.head_dim, kv->max_pages, B, st);
         }
-        if (use_tc) {
+        if (Tp == 0) {
+            // decode rows only (a token step through the prefill kernels): no prompt attention
+        } else if (use_tc) {
             ta.layer_row0 = static_cast<int>(l * kv->layer_stride / d.head_dim);
             attn_prefill_tc(tm_q, kv->tm_kv, w.attn, ta, n_tiles128, d.head_dim, tc_persist, st);
         } else {
@@ -690,7 +694,7 @@ void mixed_forward(sw_model* m, sw_kv* kv, const sw_batch& pre, const sw_batch& 
                    float* logits_out) {
     int T = 0;
     for (int i = 0; i < pre.n; ++i) T += pre.n_tokens[i];
-    if (pre.n < 1 || dec.n < 1) throw ConfigError("mixed step: needs at least one prompt and one decode row");
+    if (pre.n < 0 || dec.n < 1) throw ConfigError("mixed step: needs at least one decode row");
     if (dec.n > kMaxDecodeRows) throw ContractViolation("mixed step: decode rows out of range");
     if (pre.n > kLmRowsMax) throw ConfigError("mixed step: at most 256 prompts per launch");
     if (T + dec.n > m->pre.rows)

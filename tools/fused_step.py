@@ -29,7 +29,7 @@ def main():
     args = ap.parse_args()
     d = getattr(M, args.model)
     B, S = args.batch, args.ctx
-    chunks = [int(c) for c in args.chunks.split(",")]
+    chunks = [int(c) for c in args.chunks.split(",")] if args.chunks != "none" else [128]
     cmax = max(chunks)
     per_d = (S + 16 + 15) // 16  # decode rows' pages
     per = max(per_d, (cmax + 15) // 16)
@@ -90,6 +90,13 @@ def main():
         return
     t_dec = timed(lambda: sw.check(L.sw_decode_enqueue(eng.model, eng.kv, ctypes.byref(db), sp)), 10)
     print(f"{args.model} decode step b={B} ctx={S}: {t_dec:.3f} ms", flush=True)
+    # the same token step through the prefill kernels (normal-mode CTA-pair GEMMs, T = B rows)
+    eb = sw.Batch(n=0, slots=arr([0]), n_tokens=arr([0]), tokens=arr([0]), page_rows=arr([0]), out_index=arr([0]))
+    t_dp = timed(lambda: sw.check(L.sw_mixed_enqueue(eng.model, eng.kv, ctypes.byref(eb), ctypes.byref(db), sp)), 10)
+    print(f"{args.model} decode step b={B} ctx={S} through the prefill kernels: {t_dp:.3f} ms", flush=True)
+    if args.chunks == "none":
+        eng.close()
+        return
     for C in chunks:
         pb = pre_batch(C)
         t_pre = timed(lambda: sw.check(L.sw_prefill_enqueue(eng.model, eng.kv, ctypes.byref(pb), sp)), 3)
