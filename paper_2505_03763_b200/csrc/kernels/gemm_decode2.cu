@@ -64,16 +64,21 @@ template <int BN>
 struct SkCfg {
     static constexpr int kW = BM * BK * 2;  // one weight k-block: 16 KB
     static constexpr int kX = BN * BK * 2;  // one activation k-block
-    static constexpr int kXt = 2 * 32 * kTs * 4;  // two 32-token transpose buffers
-    static constexpr int kTok = 256 * 16;         // tok_inv, tok_pos, tok_kv
+    static constexpr int kXtRaw = 2 * 32 * kTs * 4;  // two 32-token transpose buffers
+    static constexpr int kTok = 256 * 16;            // tok_inv, tok_pos, tok_kv
     static constexpr int kBudget = 224 * 1024;
     static constexpr int NX = BN >= 128 ? 3 : 4;  // activations from L2: ~1 us of k-blocks in flight
+    // The only whole tile of a CTA is its last piece (the host keeps tiles < 2 x CTAs), whose epilogue
+    // runs after the last MMA: the transpose buffers alias the drained activation ring when it is large
+    // enough, and the weight ring takes the space (BN = 256: 7 weight stages instead of 5).
+    static constexpr bool kXtAlias = NX * kX >= kXtRaw;
+    static constexpr int kXt = kXtAlias ? 0 : kXtRaw;
     static constexpr int NWraw = (kBudget - 1024 - 512 - kXt - kTok - NX * kX) / kW;
     static constexpr int NW = NWraw > 8 ? 8 : NWraw;
     static_assert(NW >= 4, "weight ring too shallow");
     static constexpr int kOffX = NW * kW;
-    static constexpr int kOffXt = kOffX + NX * kX;
-    static constexpr int kOffTok = kOffXt + kXt;
+    static constexpr int kOffXt = kXtAlias ? kOffX : kOffX + NX * kX;
+    static constexpr int kOffTok = kOffX + NX * kX + kXt;
     static constexpr int kOffBar = kOffTok + kTok;
     static constexpr int kSmem = 1024 + kOffBar + 512;
     static constexpr uint32_t kTmemCols = 2 * BN < 32 ? 32 : 2 * BN;
@@ -219,6 +224,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int kb = p.kb0; kb < p.kb1; ++kb, ++i) {
                     const int s = i % NX;
                     if (i >= NX) mbar_wait(&x_empty[s], ((i / NX) - 1) & 1);
+                    if (pl.trace == 2 && i >= NX) {  // diagnostic (SW_DSK_TRACE=2): stale activations, no L2 reads
+                        mbar_arrive(&x_full[s]);
+                        continue;
+                    }
                     mbar_expect_tx(&x_full[s], C::kX);
                     tma_load_2d(sX + s * C::kX, &tmB, &x_full[s], kb * BK, 0, pol);
                 }

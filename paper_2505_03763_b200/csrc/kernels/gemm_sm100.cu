@@ -866,7 +866,7 @@ void gemm_run(const GemmProblem& p, cudaStream_t st) {
             static const int dsk_env = env_flag("SW_GEMM_DSK", 1);
             static const int dsk_minu = std::max(1, env_flag("SW_DSK_MINU", 8));
             static const int dsk_minbn = env_flag("SW_DSK_MINBN", 128);
-            if (dsk_env && tiles > grid_sms && bn > dsk_minbn) {
+            if (dsk_env && tiles > grid_sms && tiles < 2 * grid_sms && bn > dsk_minbn) {
                 const int P = grid_sms, nk = p.K / BK;
                 const int rem = tiles % P;
                 if ((rem == 0 || rem * nk / P >= dsk_minu) && gemm_decode_sk_ws_floats(P, bn) <= p.ws_floats &&
