@@ -45,6 +45,15 @@ constexpr int kThreads = 224;  // 7 warps: 2 producers, MMA, 4 epilogue
 constexpr int kEpiWarp0 = 3;
 constexpr int kMaxSplit = 8;   // portable cluster size
 
+// diagnostic (SW_DEC_TRACE=1): per-CTA globaltimer stamps of the last traced launch
+// [start, last MMA issued, partials stored / cluster joined, exit] (tools/dsk_trace.py --cluster)
+__device__ unsigned long long g_dec_trace[512][4];
+__device__ __forceinline__ unsigned long long dec_gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
 template <int BN>
 struct DecCfg {
     static constexpr int kABytes = BM * BK * 2;
@@ -91,6 +100,8 @@ __global__ void __launch_bounds__(kThreads, 2)
     const int S = static_cast<int>(gridDim.x);  // cluster spans x
     const int rank = static_cast<int>(blockIdx.x);
     const int tile = static_cast<int>(blockIdx.y);
+    const int trace_id = args.trace ? tile * S + rank : -1;
+    if (trace_id >= 0 && trace_id < 512 && threadIdx.x == 0) g_dec_trace[trace_id][0] = dec_gtimer();
     const int m0 = tile * BM;
     const int nk_total = args.K / BK;
     const int kb0 = rank * nk_total / S;
@@ -155,6 +166,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                 umma_commit(&empty[s]);
             }
             umma_commit(acc_ready);
+            if (trace_id >= 0 && trace_id < 512) g_dec_trace[trace_id][1] = dec_gtimer();
         }
         __syncwarp();
     }
@@ -228,6 +240,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     }
     if (S > 1) {
         cluster_sync_all();  // every rank's partial is in L2
+        if (trace_id >= 0 && trace_id < 512 && threadIdx.x == 0) g_dec_trace[trace_id][2] = dec_gtimer();
         // rank r owns tokens [r*n/S, (r+1)*n/S): add the S partials in rank order
         // (deterministic).  All warps of the CTA take part (the producer and MMA
         // warps are idle by now; the cluster barrier published the epilogue
@@ -267,6 +280,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         }
     }
     __syncthreads();
+    if (trace_id >= 0 && trace_id < 512 && threadIdx.x == 0) g_dec_trace[trace_id][3] = dec_gtimer();
     if (warp == 2) {
         tc_fence_after();
         tmem_dealloc(tmem, C::kTmemCols);
@@ -354,3 +368,8 @@ void gemm_decode_run(const CUtensorMap& a, const CUtensorMap& b, const GemmArgs&
 }
 
 }  // namespace sw
+
+extern "C" int sw_dbg_dec_trace(unsigned long long* host, int n) {
+    if (n > 512 * 4) n = 512 * 4;
+    return cudaMemcpyFromSymbol(host, sw::g_dec_trace, sizeof(unsigned long long) * n) == cudaSuccess ? 0 : -1;
+}

@@ -893,6 +893,8 @@ void gemm_run(const GemmProblem& p, cudaStream_t st) {
             }
             if (S == 1 || gemm_decode_ws_floats(tiles, S, bn) <= p.ws_floats) {
                 a.stream_k = 0;
+                static const int dec_trace = env_flag("SW_DEC_TRACE", 0);
+                a.trace = dec_trace;
                 gemm_decode_run(tmap_cached(p.W, p.w_rows, p.K, BM), tmap_cached(p.X, p.x_rows, p.K, bn), a, bn, S,
                                 tiles, st);
                 return;

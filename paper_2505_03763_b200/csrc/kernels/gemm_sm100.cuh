@@ -56,6 +56,7 @@ struct GemmArgs {
     unsigned long long* argmax;
     int feature_offset;
     int stream_k;        // decode: (tile, K-block) iterations split evenly over the CTAs
+    int trace;           // diagnostic: SW_DEC_TRACE=1 stamps per-CTA phase times (gemm_decode.cu)
     float* ws;           // stream-K partial tiles [ctas][2][BN][128]
     unsigned* counters;  // stream-K arrival counters [tiles], zero between launches
     DecodeFusion fx;

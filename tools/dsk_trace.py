@@ -25,13 +25,19 @@ def main():
         sw.check(lib.sw_op_gemm(ctypes.c_void_p(X.data_ptr()), ctypes.c_void_p(W[i % 4].data_ptr()),
                                 ctypes.c_void_p(out.data_ptr()), rows, F, K, epi, None))
     torch.cuda.synchronize()
-    buf = (ctypes.c_ulonglong * (256 * 8))()
-    lib.sw_dbg_dsk_trace(buf, 256 * 8)
-    a = np.array(buf, dtype=np.float64).reshape(256, 8)
+    if os.environ.get("SW_DEC_TRACE"):  # the cluster split-K kernel (gemm_decode.cu)
+        buf = (ctypes.c_ulonglong * (512 * 4))()
+        lib.sw_dbg_dec_trace(buf, 512 * 4)
+        a = np.array(buf, dtype=np.float64).reshape(512, 4)
+        names = ["start", "mma_done", "joined", "exit"]
+    else:
+        buf = (ctypes.c_ulonglong * (256 * 8))()
+        lib.sw_dbg_dsk_trace(buf, 256 * 8)
+        a = np.array(buf, dtype=np.float64).reshape(256, 8)
+        names = ["start", "first_kb", "mma_done", "joined", "wait1", "red1", "wait2", "red2/exit"]
     live = a[:, 0] > 0
     a = a[live]
     t0 = a[:, 0].min()
-    names = ["start", "first_kb", "mma_done", "joined", "wait1", "red1", "wait2", "red2/exit"]
     print(f"F={F} K={K} epi={epi} rows={rows}: {live.sum()} CTAs")
     for j, n in enumerate(names):
         v = a[:, j]
@@ -40,6 +46,9 @@ def main():
             continue
         v = (v - t0) / 1e3
         print(f"  {n:10s} min {v.min():7.2f}  med {np.median(v):7.2f}  max {v.max():7.2f} us")
+        if n == "start":  # CTA start histogram: a second wave shows as a late group
+            h, e = np.histogram(v, bins=8)
+            print("    start histogram:", " ".join(f"{c}@{x:.1f}" for c, x in zip(h, e[:-1])))
 
 
 if __name__ == "__main__":
