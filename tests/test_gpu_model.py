@@ -371,6 +371,26 @@ def test_attention_geometries_prefill_and_decode(shape, flat):
     assert max(errs) <= LOGIT_RTOL, errs
 
 
+def test_chunked_prefill_configs4_prompt():
+    """configs[4] scale: one 8192-token prompt at the 8B widths prefilled as four 2048-token chunks
+    (each chunk's attention reads up to 6144 cached keys) is bit-identical to the whole prompt."""
+    d = dataclasses.replace(M.LLAMA_8B, n_layers=1, vocab=4096)
+    per = 8192 // 16 + 2
+    eng = _engine(d, per, n_slots=2, max_prefill=8192)
+    try:
+        p = M.prompt_tokens(d.seed, 77, 8192, d.vocab)
+        rows = [list(range(per)), list(range(per, 2 * per))]
+        whole = eng.prefill([0], [p], [rows[0][:512]])
+        last = None
+        for c0 in range(0, 8192, 2048):
+            end = c0 + 2048
+            last = eng.prefill([1], [p[c0:end]], [rows[1][:end // 16]], out_index=[0 if end == 8192 else -1],
+                               positions=[c0])
+        assert np.array_equal(last, whole), np.abs(last - whole).max()
+    finally:
+        eng.close()
+
+
 @pytest.mark.parametrize("shape", ["TINY", "LLAMA_1B_2L", "LLAMA_8B_1L"])
 def test_chunked_prefill_bit_identical_to_whole_prompts(shape):
     """Chunked prefill (policy chunked_prefill): prompts run as
