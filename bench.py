@@ -391,12 +391,19 @@ def main():
 
     import torch
 
+    # SW_BENCH_BACKEND=gloo: the multi-rank path with every rank on the visible GPUs round robin and the
+    # gather on host tensors -- a functional check of the N > 1 line on a one-GPU box (tests, not timing)
+    backend = os.environ.get("SW_BENCH_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     from paper_2505_03763_b200 import runtime, shapes
 
     desc = getattr(shapes, w["model"])
@@ -438,7 +445,7 @@ def main():
     serial_raw = timed(serial_spec)
     best_raw = timed(best_spec) if best_spec else None
     chunk_raw = timed(chunk_spec) if chunk_spec else None
-    dev = "cuda" if dist else None
+    dev = ("cuda" if backend == "nccl" else "cpu") if dist else None
     split = fold_runs(split_raw, dist, world, dev, n_local, w["output"] + 1)
     serial = fold_runs(serial_raw, dist, world, dev, n_local, w["output"] + 1)
     best = fold_runs(best_raw, dist, world, dev, n_local, w["output"] + 1) if best_raw else serial
