@@ -71,7 +71,9 @@ WORKLOADS = {
                     max_decode=112,
                     split="policy=mixed_batching;max_batch=112;engine.split=1",
                     serial="policy=continuous_batching;max_batch=112;engine.split=0",
-                    best_serial="policy=sequential;max_batch=112;engine.split=0"),
+                    best_serial="policy=sequential;max_batch=112;engine.split=0",
+                    # chunked prefill: p50 TTFT 12.8 -> 6.8 s at 0.99x (profiles/r02s4/bench_8b_long_chunked16384.jsonl)
+                    chunked="policy=chunked_prefill;max_batch=112;chunk_tokens=16384;engine.split=1;engine.fuse=1"),
     # configs[0] shape on the GPU (fast sanity run)
     "tiny": dict(model="TINY", n=8, input=64, output=32, arrival="zero", max_prefill=1024, max_decode=16,
                  split="policy=pipelined_splitwiser;P=2;max_batch=4;engine.split=1",
