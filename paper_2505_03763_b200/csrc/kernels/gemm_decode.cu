@@ -152,10 +152,16 @@ __global__ void __launch_bounds__(kThreads, 2)
     } else if (warp == 2) {
         // -------------------------------------------------------- MMA issuer
         if (lane == 0) {
-            constexpr uint32_t idesc = umma_idesc_bf16(BM, BN);
+            // UMMA N trimmed to the live rows (multiple of 16): a bucket of BN rows computes only the
+            // columns in use; each output column's K order is unchanged (results bit-identical)
+            // (the count is loaded now and used after the first stage lands, so its latency hides there)
+            griddep_wait();  // the live row count comes from the predecessor
+            const int live = args.live_tokens ? min(args.valid_tokens, *args.live_tokens) : args.valid_tokens;
+            uint32_t idesc = 0;
             for (int i = 0; i < nk; ++i) {
                 const int s = i % NS;
                 mbar_wait(&full[s], (i / NS) & 1);
+                if (i == 0) idesc = umma_idesc_bf16(BM, min(BN, max(16, (live + 15) & ~15)));
                 tc_fence_after();
                 const uint32_t a0 = smem_addr(sA + s * C::kABytes);
                 const uint32_t b0 = smem_addr(sB + s * C::kBBytes);

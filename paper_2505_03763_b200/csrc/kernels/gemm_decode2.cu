@@ -243,7 +243,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_after();
         const uint32_t tmem = *tmem_slot;
         if (lane == 0) {
-            constexpr uint32_t idesc = umma_idesc_bf16(BM, BN);
+            // UMMA N trimmed to the live rows (multiple of 16): a bucket of BN rows computes only the
+            // columns in use; each output column's K order is unchanged (results bit-identical)
+            // (the count is loaded now and used after the first stage lands, so its latency hides there)
+            griddep_wait();  // the live row count comes from the predecessor
+            const int live = args.live_tokens ? min(args.valid_tokens, *args.live_tokens) : args.valid_tokens;
+            uint32_t idesc = 0;
             int i = 0;
             for (int q = 0; q < npcs; ++q) {
                 const Piece& p = pcs[q];
@@ -255,6 +260,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const int sw = i % NW, sx = i % NX;
                     mbar_wait(&w_full[sw], (i / NW) & 1);
                     mbar_wait(&x_full[sx], (i / NX) & 1);
+                    if (i == 0) idesc = umma_idesc_bf16(BM, min(BN, max(16, (live + 15) & ~15)));
                     tc_fence_after();
                     if (i == 0) DSK_STAMP(1);
                     const uint32_t a0 = smem_addr(sW + sw * C::kW);
