@@ -47,7 +47,8 @@ WORKLOADS = {
                     best_serial=None,
                     # chunked prefill, 8192-token chunks fused with the token step
                     # (profiles/r02s4/cfg3_chunked_sweep.txt: the best throughput of the budgets swept)
-                    chunked="policy=chunked_prefill;max_batch=256;chunk_tokens=8192;engine.split=1;engine.fuse=1"),
+                    chunked="policy=chunked_prefill;max_batch=256;chunk_tokens=8192;engine.split=1;engine.fuse=1",
+                    dominant="attention"),
     # configs[1] of BASELINE.json
     # split = PipelinedSplitwiser P=2 on concurrent streams (token steps of the two lanes aligned and merged);
     # serial = the SAME task stream under the one-task gate; best_serial = the fastest
@@ -73,7 +74,8 @@ WORKLOADS = {
                     serial="policy=continuous_batching;max_batch=112;engine.split=0",
                     best_serial="policy=sequential;max_batch=112;engine.split=0",
                     # chunked prefill: p50 TTFT 12.8 -> 6.8 s at 0.99x (profiles/r02s4/bench_8b_long_chunked16384.jsonl)
-                    chunked="policy=chunked_prefill;max_batch=112;chunk_tokens=16384;engine.split=1;engine.fuse=1"),
+                    chunked="policy=chunked_prefill;max_batch=112;chunk_tokens=16384;engine.split=1;engine.fuse=1",
+                    dominant="attention"),
     # configs[0] shape on the GPU (fast sanity run)
     "tiny": dict(model="TINY", n=8, input=64, output=32, arrival="zero", max_prefill=1024, max_decode=16,
                  split="policy=pipelined_splitwiser;P=2;max_batch=4;engine.split=1",
@@ -220,6 +222,55 @@ def roofline_decode_gemm(eng, desc, rows: int, peaks, reps: int = 20):
     return {"kernel": form, "bound": "hbm",
             "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
             "bytes_per_launch": nbytes, "us_per_launch": round(t * 1e6, 2)}
+
+
+def roofline_decode_attention(eng, desc, rows: int, ctx: int, peaks, reps: int = 5):
+    """The dominant kernel of the decode-heavy 8B runs (the launch lists in profiles/r02s4: ~52% of a
+    b = 256 decode step, the largest kernel class of configs[2]): paged-KV decode attention.  `rows`
+    synthetic prompts of `ctx` tokens are prefilled into the arena, then one step's attention -- every
+    layer's launch of the kernel the step picks -- runs back to back through sw_op_decode_attention,
+    timed with CUDA events on the launching stream.  Algorithmic bytes per layer launch = the rows'
+    K and V pages (rows * (ctx + 1) * 2 * Hkv * hd * 2) + q in and attention out (rows * H * hd * 2 each)."""
+    import ctypes
+    import numpy as np
+    import torch
+    import paper_2505_03763_b200 as sw
+
+    per = (ctx + 1 + 15) // 16
+    pages = [[i * per + j for j in range(per)] for i in range(rows)]
+    chunk = max(1, 32768 // ctx)
+    for c0 in range(0, rows, chunk):
+        idx = list(range(c0, min(rows, c0 + chunk)))
+        prompts = [np.arange(ctx, dtype=np.int64) * 7919 % desc.vocab for _ in idx]
+        eng.prefill(idx, prompts, [pages[i][:(ctx + 15) // 16] for i in idx], logits=False)
+    keep = []
+
+    def arr(xs):
+        a = (ctypes.c_int32 * len(xs))(*[int(v) for v in xs])
+        keep.append(a)
+        return a
+
+    b = sw.Batch(n=rows, slots=arr(range(rows)), positions=arr([ctx] * rows))
+    b.new_page = arr([pages[i][ctx // 16] if ctx % 16 == 0 else -1 for i in range(rows)])
+    st = torch.cuda.current_stream()
+    sp = ctypes.c_void_p(st.cuda_stream)
+    lib = sw.lib()
+    for _ in range(2):
+        sw.check(lib.sw_op_decode_attention(eng.model, eng.kv, ctypes.byref(b), sp))
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for _ in range(reps):
+        sw.check(lib.sw_op_decode_attention(eng.model, eng.kv, ctypes.byref(b), sp))
+    e1.record(st)
+    torch.cuda.synchronize()
+    t_layer = e0.elapsed_time(e1) / 1e3 / reps / desc.n_layers
+    nbytes = rows * (ctx + 1) * 2 * desc.n_kv_heads * desc.head_dim * 2 + 2 * rows * desc.n_heads * desc.head_dim * 2
+    achieved = nbytes / t_layer / 1e9
+    peak = float(peaks["hbm_gbs"])
+    return {"kernel": f"attn_decode (paged-KV decode attention, {rows} rows x ctx {ctx + 1}, per layer)",
+            "bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+            "frac": round(achieved / peak, 4), "bytes_per_launch": nbytes, "us_per_launch": round(t_layer * 1e6, 2)}
 
 
 def roofline_prefill_gemm(eng, desc, tokens: int, peaks, reps: int = 10):
@@ -454,6 +505,12 @@ def main():
     chunked = fold_runs(chunk_raw, dist, world, dev, n_local, w["output"] + 1) if chunk_raw else None
 
     roof = roofline_decode_gemm(eng, desc, w["max_decode"], peaks) if rank == 0 else None
+    # decode-heavy 8B runs: the dominant kernel is the decode attention (its roofline is the line's
+    # `roofline`; the decode gate/up's stays beside it as `roofline_decode_gemm`)
+    roof_attn = None
+    if rank == 0 and w.get("dominant") == "attention":
+        in_mean = (int(str(w["input"]).split("..")[0]) + in_max) // 2
+        roof_attn = roofline_decode_attention(eng, desc, w["max_decode"], in_mean + w["output"] // 2, peaks)
     roof_prefill = roofline_prefill_gemm(eng, desc, 4096, peaks) if rank == 0 else None
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "roofline_traffic.json")
@@ -537,9 +594,18 @@ def main():
         "init_s": round(t_init, 1),
     }
     if roof:
-        line["roofline"] = {"bound": roof["bound"], "achieved": roof["achieved"], "peak": roof["peak"],
-                            "unit": roof["unit"], "frac": roof["frac"], "traffic": traffic, "kernel": roof["kernel"],
-                            "us_per_launch": roof["us_per_launch"], "bytes_per_launch": roof["bytes_per_launch"]}
+        gemm_roof = {"bound": roof["bound"], "achieved": roof["achieved"], "peak": roof["peak"],
+                     "unit": roof["unit"], "frac": roof["frac"], "traffic": traffic, "kernel": roof["kernel"],
+                     "us_per_launch": roof["us_per_launch"], "bytes_per_launch": roof["bytes_per_launch"]}
+        if roof_attn:
+            attn_traffic = None
+            if os.path.exists(tpath):
+                with open(tpath) as f:
+                    attn_traffic = json.load(f).get(args.workload, {}).get("decode_attention_bytes")
+            line["roofline"] = dict(roof_attn, traffic=attn_traffic)
+            line["roofline_decode_gemm"] = gemm_roof
+        else:
+            line["roofline"] = gemm_roof
     print(json.dumps(line), flush=True)
     if dist:
         dist.barrier()

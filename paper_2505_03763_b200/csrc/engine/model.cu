@@ -353,7 +353,9 @@ void decode_layers(sw_model* m, sw_kv* kv, int R, cudaStream_t st, int lane, boo
 
 }  // namespace
 
-void decode_forward(sw_model* m, sw_kv* kv, const sw_batch& b, cudaStream_t st, bool use_graph, int lane, int lanes) {
+// Stage one decode step's metadata (StepMeta, one H2D copy) on `lane` and pick its attention kernel;
+// returns the row bucket.
+static int stage_decode(sw_model* m, sw_kv* kv, const sw_batch& b, cudaStream_t st, int lane, bool& flat) {
     const sw_model_desc& d = m->desc;
     if (lane < 0 || lane >= sw_model::kMaxDecodeLanes) throw ContractViolation("decode: lane out of range");
     Workspace& w = m->dec[lane];
@@ -385,7 +387,7 @@ void decode_forward(sw_model* m, sw_kv* kv, const sw_batch& b, cudaStream_t st, 
     // SW_ATTN_FLAT=0/1 forces one (profiles/r01c/attn_flat_sweep.txt)
     static const int flat_env = env_int("SW_ATTN_FLAT", 2);
     static const int flat_ctx = env_int("SW_ATTN_FLAT_CTX", 2048);
-    bool flat = false;
+    flat = false;
     if (kv->tm_kv_ok && flat_env == 1) {
         flat = true;
     } else if (kv->tm_kv_ok && flat_env == 2) {
@@ -395,6 +397,14 @@ void decode_forward(sw_model* m, sw_kv* kv, const sw_batch& b, cudaStream_t st, 
         for (int i = 0; i < b.n; ++i) ctx += b.positions[i] + 1;
         flat = ctx >= static_cast<long long>(flat_ctx) * b.n || b.n * d.n_kv_heads <= 2 * stream_sm_count(st);
     }
+    return R;
+}
+
+void decode_forward(sw_model* m, sw_kv* kv, const sw_batch& b, cudaStream_t st, bool use_graph, int lane, int lanes) {
+    const sw_model_desc& d = m->desc;
+    bool flat = false;
+    const int R = stage_decode(m, kv, b, st, lane, flat);
+    Workspace& w = m->dec[lane];
     auto run = [&](cudaStream_t s) {
         decode_layers(m, kv, R, s, lane, flat);
     };
@@ -431,6 +441,29 @@ void decode_forward(sw_model* m, sw_kv* kv, const sw_batch& b, cudaStream_t st, 
         q.fx.norm_dim = d.d_model;
         q.fx.norm_eps = d.norm_eps;
         gemm_run(q, st);
+    }
+}
+
+// One decode step's attention alone -- every layer's launch of the kernel the step would pick -- over
+// the rows' paged contexts (bench.py: the roofline of the dominant kernel of a decode-heavy run; the
+// q rows are whatever the workspace holds, the KV reads are the step's).
+static void decode_attention_only(sw_model* m, sw_kv* kv, const sw_batch& b, cudaStream_t st) {
+    bool flat = false;
+    const int R = stage_decode(m, kv, b, st, 0, flat);
+    const sw_model_desc& d = m->desc;
+    PdlScope pdl(true);
+    Workspace& w = m->dec[0];
+    DecodeAttnArgs aa = decode_attn_args(m, kv, w);
+    DecodeFlatArgs fa = decode_flat_args(m, kv, w);
+    const int flat_ctas = stream_sm_count(st);
+    for (int l = 0; l < d.n_layers; ++l) {
+        kv_t* kvl = kv->pages + l * kv->layer_stride;
+        if (flat) {
+            fa.layer_row0 = static_cast<int>(l * kv->layer_stride / d.head_dim);
+            attn_decode_flat(kv->tm_kv, w.q, w.attn, fa, flat_ctas, d.head_dim, d.n_heads / d.n_kv_heads, st);
+        } else {
+            attn_decode(w.q, kvl, w.attn, aa, R, d.head_dim, st);
+        }
     }
 }
 
@@ -961,6 +994,13 @@ extern "C" int sw_op_rmsnorm(const float* x, const void* gain, void* y, int32_t 
     return guarded([&] {
         rmsnorm(x, static_cast<const __nv_bfloat16*>(gain), static_cast<__nv_bfloat16*>(y), rows, dim, eps, nullptr,
                 nullptr, static_cast<cudaStream_t>(stream));
+    });
+}
+
+extern "C" int sw_op_decode_attention(sw_model* m, sw_kv* kv, const sw_batch* b, void* stream) {
+    return guarded([&] {
+        if (!m || !kv || !b || !b->slots || !b->positions) throw ConfigError("sw_op_decode_attention: null argument");
+        decode_attention_only(m, kv, *b, static_cast<cudaStream_t>(stream));
     });
 }
 
