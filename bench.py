@@ -63,7 +63,10 @@ WORKLOADS = {
     # configs[2]: 8B shape, Poisson arrivals of mixed prompts, mixed batching vs continuous batching
     "8b-poisson": dict(model="LLAMA_8B", n=128, input="128..2048", output=256, arrival="poisson:32",
                        max_prefill=32768, max_decode=128,
-                       split="policy=mixed_batching;max_batch=128;engine.split=1",  # prefill || decode, one instance
+                       # prefill || decode, one instance; the prefill stream outranks the decode stream:
+                       # with decode first, back-to-back PDL-chained steps starve the prompts (p50 TTFT 1.38 s,
+                       # 5264 tok/s; profiles/r02s4/poisson32_priority.txt)
+                       split="policy=mixed_batching;max_batch=128;engine.split=1;engine.prefill_priority=1",
                        serial="policy=mixed_batching;max_batch=128;engine.split=0",
                        best_serial="policy=continuous_batching;max_batch=128;engine.split=0"),
     # configs[4]: 8B long-context decode-heavy, prompt 8192 / gen 512, the KV arena near HBM capacity

@@ -43,7 +43,8 @@ struct GpuOptions {
     int decode_sms = 0;       // split mode: > 0 partitions the SMs with green contexts (decode | prefill)
     bool lean_prefill = false;  // split mode: prompts launched while decode work exists use co-resident GEMM tiles
     int prefill_yield = 0;      // split mode: prompts launched while decode work exists cap GEMM tiles per CTA
-    bool prefill_priority = false;  // split mode: prefill stream at the higher stream priority
+    bool prefill_priority = true;   // split mode: prefill stream at the higher stream priority (decode-first
+                                    // streams starve prompts under back-to-back steps; engine.prefill_priority=0)
     bool coalesce = true;     // one launch per kind per scheduling pass
     bool align = true;        // split mode: a token step requested while another is in flight waits for it and
                               // then runs merged with every other waiting step (one weight pass for all lanes)

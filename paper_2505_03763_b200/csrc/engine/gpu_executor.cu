@@ -686,7 +686,7 @@ extern "C" int sw_engine_run(sw_model* m, sw_kv* kv, const char* spec, char** ou
             else if (k == "engine.decode_sms") opt.decode_sms = std::stoi(v);
             else if (k == "engine.lean_prefill") opt.lean_prefill = v == "1" || v == "true";
             else if (k == "engine.prefill_yield") opt.prefill_yield = std::stoi(v);
-            else if (k == "engine.prefill_priority") opt.prefill_priority = v == "1" || v == "true";
+            else if (k == "engine.prefill_priority") opt.prefill_priority = !(v == "0" || v == "false");
             else if (k == "engine.fuse") opt.fuse = v == "1" || v == "true";
             else if (k == "engine.chunk_tokens") opt.chunk_tokens = std::stoi(v);
             else if (k == "engine.peak_flops") opt.peak_flops = std::stod(v);
