@@ -46,7 +46,7 @@ struct GpuOptions {
     bool prefill_priority = true;   // split mode: prefill stream at the higher stream priority (decode-first
                                     // streams starve prompts under back-to-back steps; engine.prefill_priority=0)
     bool coalesce = true;     // one launch per kind per scheduling pass
-    bool align = true;        // split mode: a token step requested while another is in flight waits for it and
+    bool align = true;        // a token step requested while another is in flight waits for it and
                               // then runs merged with every other waiting step (one weight pass for all lanes)
     bool graphs = true;       // CUDA graphs for decode steps
     bool fuse = false;        // split mode: fused mixed steps -- a prompt task runs as chunks of whole prompts and

@@ -104,9 +104,9 @@ public:
         }
         int lo, hi;
         SW_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-        // engine.prefill_priority=1: the prefill stream outranks the decode streams (a prompt
-        // that shares the GPU with token steps finishes first -- the lanes' steps then merge
-        // sooner); default: token steps outrank prompts (TBT first)
+        // engine.prefill_priority=1 (default): the prefill stream outranks the decode streams (a
+        // prompt that shares the GPU with token steps finishes first -- the lanes' steps then merge
+        // sooner, and back-to-back steps cannot starve prompts); =0: token steps first
         const int p_pre = opt_.prefill_priority ? hi : lo, p_dec = opt_.prefill_priority ? lo : hi;
         SW_CUDA(cudaStreamCreateWithPriority(&s_prefill_, cudaStreamNonBlocking, p_pre));
         for (int i = 0; i < lanes; ++i) {
@@ -341,7 +341,10 @@ private:
         flush_steps();
     }
 
-    bool aligning() const { return opt_.split && (opt_.align || opt_.fuse); }
+    // token steps of several lanes requested while one is in flight wait and run as one merged
+    // launch -- in split mode and (round 2) in the serial arm too, so "serial" is the same task
+    // stream on one stream, not a stream that re-reads the weights once per lane
+    bool aligning() const { return opt_.align || (opt_.split && opt_.fuse); }
     bool fusing() const { return opt_.split && opt_.fuse; }
 
     // decode work exists: a step in flight or waiting, or a request past its prompt
