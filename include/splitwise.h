@@ -125,7 +125,8 @@ int sw_kv_capacity_pages(const sw_model_desc* desc, int device, int64_t reserve_
 int sw_kv_arena_views(sw_kv* kv, int32_t** page_table, int32_t** last_token, int32_t** out_tokens, void** pages);
 
 /* One decode step's attention alone (every layer, the kernel the step would pick) over the batch's
- * paged contexts -- the timing probe bench.py uses for the roofline of the dominant decode kernel. */
+ * paged contexts -- the timing probe bench.py uses for the roofline of the dominant decode kernel.
+ * It uses decode lane 0's workspace: not concurrent with sw_decode_enqueue on the same model. */
 int sw_op_decode_attention(sw_model* model, sw_kv* kv, const sw_batch* batch, void* stream);
 int sw_prefill_enqueue(sw_model* model, sw_kv* kv, const sw_batch* batch, void* stream);
 /* The co-scheduler's SM partition (green contexts, cached per device): a

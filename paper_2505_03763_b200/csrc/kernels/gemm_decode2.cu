@@ -224,10 +224,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int kb = p.kb0; kb < p.kb1; ++kb, ++i) {
                     const int s = i % NX;
                     if (i >= NX) mbar_wait(&x_empty[s], ((i / NX) - 1) & 1);
-                    if (pl.trace == 2 && i >= NX) {  // diagnostic (SW_DSK_TRACE=2): stale activations, no L2 reads
-                        mbar_arrive(&x_full[s]);
-                        continue;
-                    }
                     mbar_expect_tx(&x_full[s], C::kX);
                     tma_load_2d(sX + s * C::kX, &tmB, &x_full[s], kb * BK, 0, pol);
                 }
