@@ -34,7 +34,7 @@ from oracle import pages as P
 
 pytestmark = pytest.mark.gpu
 
-N_CASES = 30
+N_CASES = int(os.environ.get("SW_PROP_CASES", "30"))  # a longer soak: SW_PROP_CASES=150
 N_PAGES = 512
 
 
@@ -74,7 +74,7 @@ def make_case(seed: int) -> str:
             f"arrival={arrival};{policy};kv_capacity_blocks={cap};{mode}")
 
 
-N_CHUNKED = 8
+N_CHUNKED = int(os.environ.get("SW_PROP_CHUNKED", "8"))
 
 
 def make_chunked_case(seed: int) -> str:
