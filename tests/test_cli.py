@@ -124,6 +124,21 @@ def test_gpu_backend_run(tmp_path, capsys):
     assert _read(out, "replay_report.json") == _read(out, "report.json")
 
 
+@pytest.mark.gpu
+def test_gpu_backend_chunked_prefill(tmp_path):
+    """chunked_prefill through the JSON front end on the B200 engine: prompts of 130-300 tokens cut
+    into 128-token chunks fused with the token steps; the written log replays to its report."""
+    cfg = {"workload": {"n_requests": 6, "input_tokens": [130, 300], "output_tokens": [4, 9], "arrival": "all_at_zero"},
+           "scheduler": {"policy": "chunked_prefill", "max_batch": 4, "chunk_tokens": 128},
+           "engine": {"engine.split": 1, "engine.fuse": 1}}
+    code, out = _run(tmp_path, cfg, "--backend", "gpu", "--model", "TINY")
+    assert code == 0
+    rep = json.loads(_read(out, "report.json"))
+    assert rep["n_requests"] == 6
+    assert cli.main(["replay", str(out / "events.csv")]) == 0
+    assert _read(out, "replay_report.json") == _read(out, "report.json")
+
+
 def test_trace_workload_config(tmp_path):
     trace = tmp_path / "trace.csv"
     trace.write_text("id,arrival_s,input_tokens,output_tokens\n0,0.0,100,5\n1,0.001,300,9\n2,0.001,50,2\n")
