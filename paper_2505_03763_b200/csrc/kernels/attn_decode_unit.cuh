@@ -50,10 +50,12 @@ __device__ __forceinline__ int swz(int row, int chunk) {
 constexpr int kPage = 16;            // tokens per KV page (fixed: shifts, not divisions, in the address math)
 constexpr int kPartSplits = 16;      // stride of the split-partial buffers (>= any split count)
 constexpr int kMaxChunkPages = 512;  // page ids of one decode split staged in smem (8192 keys)
-
+// keys per K/V block of a warp's ring: 16 at every head dim (hd 64 used 32: with 16, a warp of a
+// short unit has twice the blocks to pipeline and the ring half the smem -- Llama-1B b=64 ctx 512
+// step 0.992 -> 0.969 ms; profiles/r02s4/decode_attention_kb_ab.txt)
 template <int HD>
 constexpr int decode_kb() {
-    return HD <= 64 ? 32 : 16;
+    return 16;
 }
 // dynamic smem of one unit runner (4 warps): per-warp NS-stage K/V rings + warp-merge scratch
 template <int HD, int G, int NS = 2>
