@@ -1,32 +1,36 @@
-// Decode projection GEMM for sm_100a, stream-K form: swap-AB tcgen05 over a
-// persistent grid of one CTA per SM, the weight stream cut into equal shares.
+// Decode projection GEMM for sm_100a for projections wider than the GPU (used for
+// the Llama-8B gate/up at > 128 rows): swap-AB tcgen05 over a persistent grid of
+// one CTA per SM, every SM streaming the same weight bytes.
 //
 //   Y[t, f] = sum_k X[t, k] W[f, k]   W: weights bf16 [F, K] (UMMA M = 128 rows)
 //                                     X: decode rows bf16 [BN, K] (UMMA N = BN)
 //
-// A decode step at b <= 256 rows streams every weight once; the four
-// projections of a layer have 24..224 feature tiles of 128 rows, which never
-// divide evenly over 148 SMs (the 8B gate/up: 224 tiles = 1.51 waves), and
-// the cluster split-K form (gemm_decode.cu) needs whole clusters co-resident
-// inside one GPC.  Here the (tile, 64-wide K-block) units of the projection are
-// numbered tile-major and CTA c of P takes units [c*U/P, (c+1)*U/P): every SM
-// streams the same number of weight bytes.  A CTA's range is a list of pieces
-// (tile, K-blocks [kb0, kb1)); each piece accumulates into one of two TMEM
-// accumulators (the epilogue of piece i overlaps the MMAs of piece i+1):
-//   * a piece that is a whole tile is emitted directly: TMEM (thread =
-//     feature) -> smem token-major -> one warp per token runs the fused
-//     epilogue (emit_tok: residual + RMSNorm sums, SwiGLU, RoPE + paged KV);
-//   * a tile cut over np CTAs: every piece parks its fp32 partial token-major
-//     in an L2 scratch and counts itself in; after its last MMA each of the np
-//     CTAs waits for the count and reduces its 1/np of the tile's tokens --
-//     the np partials added in K order (deterministic: the pieces depend on
-//     the weight shape and P only, never on the batch) -- and emits them.
+// The 8B gate/up has 224 feature tiles of 128 rows: 1.51 waves on 148 SMs, so
+// the cluster split-K form (gemm_decode.cu) leaves 76 SMs with two tiles and 72
+// with one, and at 256 rows the doubled SMs' MMAs set the time.  Here each of
+// the P CTAs takes w = T / P whole tiles plus an equal stream-K share of the
+// remaining T - w*P tiles (their (tile, 64-wide K-block) units numbered
+// tile-major, CTA c taking units [c*R/P, (c+1)*R/P)).  A CTA's work is a list of
+// pieces (tile, K-blocks [kb0, kb1)), its stream-K pieces FIRST; each piece
+// accumulates into one of two TMEM accumulators (the epilogue of piece i
+// overlaps the MMAs of piece i+1):
+//   * a cut tile: every piece parks its fp32 partial token-major in an L2
+//     scratch and counts itself in; after its last cut piece each of the np
+//     CTAs waits for the count and reduces its 1/np of the tile's tokens -- the
+//     np partials added in K order (deterministic: the pieces depend on the
+//     weight shape and P only, never on the batch) -- and emits them, while the
+//     MMA warp runs the whole tiles;
+//   * a whole tile: TMEM (thread = feature) -> smem token-major -> one warp per
+//     token runs the fused epilogue (emit_tok: residual + RMSNorm sums, SwiGLU,
+//     RoPE + paged KV).  The last one is the only work left after the last MMA:
+//     warps 4-7 emit its tokens 0-127 and warps 0-3 (idle by then) tokens
+//     128-255, each set transposing through a drained ring.
 // Warps: 0 weight TMA (never waits for the predecessor: weights are constant,
 // so the ring fills under programmatic dependent launch), 1 activation TMA
-// (after griddepcontrol.wait), 2 MMA issuer, 3 spare, 4-7 epilogue; all eight
-// take part in the final reductions.  Weight and activation rings are
-// separate: at b = 256 an activation k-block is twice a weight k-block, and
-// only the weights come from HBM.
+// (after griddepcontrol.wait), 2 MMA issuer (UMMA N trimmed to the live rows),
+// 3 spare, 4-7 epilogue.  Weight and activation rings are separate: at b = 256
+// an activation k-block is twice a weight k-block, and only the weights come
+// from HBM.
 #include <cuda.h>
 
 #include <algorithm>
