@@ -222,9 +222,15 @@ def roofline_decode_gemm(eng, desc, rows: int, peaks, reps: int = 20):
     form = ("gemm_dsk_kernel<256,SWIGLU> (decode gate/up: whole tiles per SM + stream-K remainder, rows=%d)" % rows
             if rows > 128 and 2 * F // 128 > torch.cuda.get_device_properties(0).multi_processor_count else
             "gemm_decode_kernel<BN,SWIGLU> (decode gate/up, cluster split-K, rows=%d)" % rows)
+    # at 256 rows the launch sits at the ridge point (2*rows FLOP per weight byte = 256 FLOP/B against
+    # 1650.6 TFLOP/s / 6449 GB/s = 256): the tensor fraction is reported beside the HBM one
+    flops = 2.0 * rows * 2 * F * d
+    tpeak = float(peaks["bf16_tflops"])
     return {"kernel": form, "bound": "hbm",
             "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
-            "bytes_per_launch": nbytes, "us_per_launch": round(t * 1e6, 2)}
+            "bytes_per_launch": nbytes, "us_per_launch": round(t * 1e6, 2),
+            "flops_per_launch": flops, "tensor_tflops": round(flops / t / 1e12, 1),
+            "tensor_frac": round(flops / t / 1e12 / tpeak, 4)}
 
 
 def roofline_decode_attention(eng, desc, rows: int, ctx: int, peaks, reps: int = 5):
@@ -599,7 +605,8 @@ def main():
     if roof:
         gemm_roof = {"bound": roof["bound"], "achieved": roof["achieved"], "peak": roof["peak"],
                      "unit": roof["unit"], "frac": roof["frac"], "traffic": traffic, "kernel": roof["kernel"],
-                     "us_per_launch": roof["us_per_launch"], "bytes_per_launch": roof["bytes_per_launch"]}
+                     "us_per_launch": roof["us_per_launch"], "bytes_per_launch": roof["bytes_per_launch"],
+                     "tensor_frac": roof["tensor_frac"]}
         if roof_attn:
             attn_traffic = None
             if os.path.exists(tpath):
