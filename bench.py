@@ -171,6 +171,38 @@ def cpu_sample(desc_name: str, n_req: int = 4, prompt: int = 512, gen: int = 8):
             "seconds": dt}
 
 
+def reference_simulator(w: dict, kv_pages: int) -> dict | None:
+    """The unmodified reference simulator (oracle/_ref/refsim, compiled from the
+    reference's own headers) on the same trace and policies: its wall time is the
+    reference's scheduling-only cost of the path, and its report is what the
+    reference's roofline pricing predicts for split vs serial (on its modelled
+    GPU, not a B200).  Engine-only keys (engine.*) are stripped; None when the
+    binary is absent."""
+    exe = os.path.join(ROOT, "oracle", "_ref", "refsim")
+    if not os.access(exe, os.X_OK):
+        return None
+    out = {"binary": "oracle/_ref/refsim (reference splitsim headers, unmodified)"}
+    for arm in ("split", "serial"):
+        items = [x for x in w[arm].split(";") if x]
+        pol = ";".join(x for x in items if not x.startswith("engine."))
+        if "policy=pipelined_splitwiser" in items:  # multi-lane: the reference's concurrent (MPS) law for the
+            # split arm, its time-sliced law (one lane's task at a time) for the one-stream serial arm
+            pol += ";mode=mps_concurrent" if "engine.split=1" in items else ";mode=time_sliced"
+        spec = (f"n={w['n']};input={w['input']};output={w['output']};seed=1;arrival={w['arrival']};"
+                f"kv_capacity_blocks={kv_pages};{pol}")
+        t0 = time.perf_counter()
+        r = subprocess.run([exe, spec], capture_output=True, text=True)
+        wall = time.perf_counter() - t0
+        rep = next((l for l in r.stdout.splitlines() if l.startswith("#report ")), None)
+        if r.returncode != 0 or rep is None:
+            return dict(out, error=f"refsim exit {r.returncode}: {r.stderr.strip()[:200]}")
+        kv = dict(x.split("=", 1) for x in rep[len("#report "):].split(";") if "=" in x)
+        out[arm] = {"policy": pol, "wall_s": round(wall, 4), "simulated_tokens_per_s": round(float(kv["tokens_per_s"]), 1)}
+    out["simulated_split_over_serial"] = round(out["split"]["simulated_tokens_per_s"] /
+                                               out["serial"]["simulated_tokens_per_s"], 4)
+    return out
+
+
 # ----------------------------------------------------------------- roofline
 def graph_time(launch, reps: int) -> float:
     """Average device time of one launch: `reps` launches captured in one CUDA
@@ -311,7 +343,7 @@ def roofline_prefill_gemm(eng, desc, tokens: int, peaks, reps: int = 10):
 
 # ----------------------------------------------------------------- engine runs
 # bounded CPU samples of each model (requests, prompt, generated tokens): ~10-30 s of numpy on the host cores
-CPU_SAMPLE = {"LLAMA_8B": (1, 512, 4), "LLAMA_1B": (4, 512, 8), "TINY": (8, 64, 32)}
+CPU_SAMPLE = {"LLAMA_8B": (2, 512, 4), "LLAMA_1B": (4, 512, 8), "TINY": (8, 64, 32)}
 
 
 def spec_for(w, extra: str, rank: int, world: int) -> str:
@@ -448,6 +480,8 @@ def main():
                 "config": {"workload": args.workload, "model_shape": w["model"], "sample": samples[0]["sample"]},
                 "cpu_baseline": {k: samples[0][k] for k in ("unit", "cores", "kind", "sample")} | {"value": round(v, 3)},
                 "e2e": {"value": round(v, 3), "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        in_max = int(str(w["input"]).split("..")[-1])
+        line["reference_simulator"] = reference_simulator(w, w["n"] * ((in_max + w["output"] + 15) // 16) + 64)
         print(json.dumps(line), flush=True)
         return
 
@@ -598,6 +632,7 @@ def main():
         "roofline": None,
         "roofline_prefill": roof_prefill,
         "cpu_baseline": cpu,
+        "reference_simulator": reference_simulator(w, w["kv_pages"]) if world == 1 else None,
         "clocks": clocks.summary(),
         "peaks_source": peaks_src,
         "init_s": round(t_init, 1),
