@@ -372,9 +372,25 @@ def roofline_prefill_gemm(eng, desc, tokens: int, peaks, reps: int = 10):
 CPU_SAMPLE = {"LLAMA_8B": (2, 512, 4), "LLAMA_1B": (4, 512, 8), "TINY": (8, 64, 32)}
 
 
+def global_arrival(arrival: str, world: int) -> str:
+    """Weak scaling: every GPU sees the single-GPU workload -- `n` requests at the
+    workload's rate.  The global trace therefore has n * world requests arriving
+    world times as fast; its round-robin shards (`shard=r/N`, the reference's
+    multi_instance_split) each carry the per-GPU rate.  With the rate left global,
+    each shard would see rate / world and the run would turn arrival-bound as N
+    grows (configs[2] at 16 requests/s per GPU: 4.3k instead of 9.6k tok/s)."""
+    if world <= 1:
+        return arrival
+    if arrival.startswith("poisson:"):
+        return f"poisson:{float(arrival[len('poisson:'):]) * world:g}"
+    if arrival.startswith("fixed:"):
+        return f"fixed:{float(arrival[len('fixed:'):]) / world:g}"
+    return arrival  # all at zero
+
+
 def spec_for(w, extra: str, rank: int, world: int) -> str:
-    s = (f"n={w['n'] * world};input={w['input']};output={w['output']};seed=1;arrival={w['arrival']};"
-         f"kv_capacity_blocks={w['kv_pages']};{extra}")
+    s = (f"n={w['n'] * world};input={w['input']};output={w['output']};seed=1;"
+         f"arrival={global_arrival(w['arrival'], world)};kv_capacity_blocks={w['kv_pages']};{extra}")
     if world > 1:
         s += f";shard={rank}/{world}"
     return s
@@ -634,6 +650,7 @@ def main():
         "data": "synthetic (SplitMix64 random-init weights and prompts)",
         "config": {"workload": args.workload, "model_shape": w["model"], "requests_per_gpu": n_local,
                    "prompt": w["input"], "gen": w["output"], "arrival": w["arrival"],
+                   "arrival_global": global_arrival(w["arrival"], world),
                    "split_policy": args.split or w["split"], "serial_policy": args.serial or w["serial"],
                    "best_serial_policy": w["best_serial"] or (args.serial or w["serial"]),
                    "kv_pages": w["kv_pages"],

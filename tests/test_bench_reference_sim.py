@@ -36,3 +36,27 @@ def test_reference_simulator_matches_sim_run(name):
         ours = sw.sim_run(spec)
         assert round(float(ours.report["tokens_per_s"]), 1) == r[arm]["simulated_tokens_per_s"]
     assert r["simulated_split_over_serial"] > 0
+
+
+def test_weak_scaling_keeps_the_per_gpu_rate():
+    """bench.spec_for at N ranks: n * N requests at N times the rate, so each
+    round-robin shard is the single-GPU workload (512 requests over ~4 s on
+    configs[2]), not an N-times thinner arrival-bound stream."""
+    import bench
+    import paper_2505_03763_b200 as sw
+
+    assert bench.global_arrival("poisson:128", 1) == "poisson:128"
+    assert bench.global_arrival("poisson:128", 4) == "poisson:512"
+    assert bench.global_arrival("fixed:0.02", 2) == "fixed:0.01"
+    assert bench.global_arrival("zero", 8) == "zero"
+    w = dict(bench.WORKLOADS["8b-cfg3"], kv_pages=73792)
+
+    def arrivals(rank, world):
+        r = sw.sim_run(bench.spec_for(w, "policy=continuous_batching;max_batch=256", rank, world))
+        return [float(l.split(",", 1)[0]) for l in r.event_log.splitlines() if ",arrival," in l]
+
+    one = arrivals(0, 1)
+    for world in (2, 4, 8):
+        shard = arrivals(world - 1, world)
+        assert len(shard) == len(one) == 512
+        assert abs(shard[-1] - one[-1]) / one[-1] < 0.25, (world, shard[-1], one[-1])
