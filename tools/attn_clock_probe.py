@@ -51,14 +51,35 @@ def main():
 
     state = {"prefilled": False}
 
+    big = torch.empty(2 << 30, device="cuda", dtype=torch.bfloat16)  # 4 GiB: a read-only stream (sum) and a copy
+    big.fill_(1.0)
+    dst = torch.empty(1 << 30, device="cuda", dtype=torch.bfloat16)
+
+    def streams():
+        torch.cuda.synchronize()
+        e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        e0.record()
+        for _ in range(5):
+            big.sum(dtype=torch.float32)
+        e1.record()
+        for _ in range(5):
+            dst.copy_(big[: 1 << 30])
+        e2.record()
+        torch.cuda.synchronize()
+        rd = 5 * big.numel() * 2 / (e0.elapsed_time(e1) / 1e3) / 1e9
+        cp = 5 * 2 * dst.numel() * 2 / (e1.elapsed_time(e2) / 1e3) / 1e9
+        return rd, cp
+
     def probe(tag, settle=0.0):
         with bench.ClockSampler(0) as c:
             r = bench.roofline_decode_attention(eng, desc, args.rows, args.ctx, peaks, reps=args.reps,
                                                 prefilled=state["prefilled"], settle_s=settle)
         state["prefilled"] = True
         s = c.summary()
+        rd, cp = streams()  # right after, in the same power state
         print(f"{tag:28s} {r['us_per_launch']:7.2f} us/layer  {r['achieved']:7.1f} GB/s  frac {r['frac']:.4f}  "
-              f"SM {s['sm_mhz']} MHz  {s['reasons']}", flush=True)
+              f"SM {s['sm_mhz']} MHz  {s['reasons']} | torch read stream {rd:7.1f} GB/s, copy {cp:7.1f} GB/s",
+              flush=True)
 
     probe("right after its prefill")
     probe("again (no settle)")
