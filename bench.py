@@ -191,7 +191,10 @@ def reference_simulator(w: dict, kv_pages: int) -> dict | None:
         spec = (f"n={w['n']};input={w['input']};output={w['output']};seed=1;arrival={w['arrival']};"
                 f"kv_capacity_blocks={kv_pages};{pol}")
         t0 = time.perf_counter()
-        r = subprocess.run([exe, spec], capture_output=True, text=True)
+        try:
+            r = subprocess.run([exe, spec], capture_output=True, text=True, timeout=120)
+        except (OSError, subprocess.TimeoutExpired) as e:  # never fail the bench line on the reference leg
+            return dict(out, error=f"refsim: {e}")
         wall = time.perf_counter() - t0
         rep = next((l for l in r.stdout.splitlines() if l.startswith("#report ")), None)
         if r.returncode != 0 or rep is None:
